@@ -1,0 +1,147 @@
+/*
+ * tsdiscord_b200.h — C-ABI of the B200-native PALMAD / MERLIN library
+ * (libtsdiscord_b200.so).  Plain pointers and sizes only; no torch or C++ types.
+ *
+ * Every entry point replaces one function of the reference's C++ discord API
+ * (/root/reference/proj/include/tsdiscord); the C++ drop-in headers in
+ * include/tsdiscord/ are implemented on top of this layer and rethrow the
+ * status codes as the reference's exception types:
+ *
+ *   TSD_EINVAL   -> std::invalid_argument  (preconditions: src/types.cpp:9-11,27-30,
+ *                                           src/stats.cpp:9,41, src/merlin.cpp:60-62)
+ *   TSD_ELOGIC   -> std::logic_error       (src/merlin.cpp:19,54)
+ *   TSD_ERUNTIME -> std::runtime_error     (I/O, src/io.cpp)
+ *   TSD_ECUDA    -> std::runtime_error     (device failure; never a silent CPU fallback)
+ *
+ * Indices in and out are 1-based, like the reference (types.hpp:11).
+ * A context owns one CUDA device, its stream, the resident series and all
+ * device-side state; contexts are not thread-safe (one per calling thread).
+ */
+#ifndef TSDISCORD_B200_H
+#define TSDISCORD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    TSD_OK = 0,
+    TSD_EINVAL = 1,
+    TSD_ELOGIC = 2,
+    TSD_ERUNTIME = 3,
+    TSD_ECUDA = 4
+};
+
+typedef struct tsd_ctx tsd_ctx;
+
+/* One discord: replaces tsdiscord::DiscordRecord (include/tsdiscord/types.hpp:50-54). */
+typedef struct {
+    int64_t index;     /* 1-based start */
+    double nn_dist_sq; /* squared z-normalised ED to the nearest non-self match */
+    double nn_dist;    /* sqrt(nn_dist_sq) */
+} tsd_record;
+
+/* Replaces tsdiscord::MerlinOptions (include/tsdiscord/merlin.hpp:32-38).
+ * `workers` is accepted for source compatibility and ignored (the device
+ * schedules itself; results never depend on it, as in the reference). */
+typedef struct {
+    int64_t top_k;       /* default 1 */
+    int64_t seglen;      /* default 512; only validated, the device tiling is its own */
+    int64_t workers;     /* default 1; ignored */
+    int64_t max_retries; /* default 100 */
+    int32_t reuse_stats; /* default 1: advance stats with Eq. 7-8 instead of recomputing */
+} tsd_merlin_opts;
+
+/* Per-run counters (device-side work accounting, for the roofline). */
+typedef struct {
+    uint64_t cells;         /* (candidate, subsequence) correlations updated by the FP32 scan */
+    uint64_t seed_dots;     /* directly seeded dot products (m FMAs each, FP64) */
+    uint64_t seed_flops;    /* sum over seeds of 2*m */
+    uint64_t rechecks;      /* knife-edge pairs resolved with the exact FP64 distance */
+    uint64_t exact_pairs;   /* near-minimum pairs rebuilt exactly for survivors */
+    uint64_t pardrag_calls; /* DRAG tries */
+    uint64_t scan_launches; /* launches of the tile scan kernel */
+    uint64_t kernel_launches; /* all kernel launches issued by the library */
+    double scan_ms;         /* device time inside the scan kernel (CUDA events) */
+    double total_ms;        /* device time of the last merlin/pardrag call (CUDA events) */
+} tsd_counters;
+
+/* ---- context ------------------------------------------------------------ */
+int tsd_ctx_create(int device, tsd_ctx** out);
+void tsd_ctx_destroy(tsd_ctx* ctx);
+const char* tsd_last_error(const tsd_ctx* ctx); /* message of the last failing call */
+/* Message of a failed tsd_ctx_create (no context to attach it to). */
+const char* tsd_create_error(void);
+
+/* Multi-GPU: join a segment-sharded group of `world` contexts (one process per
+ * GPU).  `nccl_id` is the 128-byte ncclUniqueId produced by tsd_nccl_unique_id
+ * on rank 0 and broadcast by the caller.  With world == 1 this is a no-op. */
+int tsd_nccl_unique_id(uint8_t out[128]);
+int tsd_ctx_join(tsd_ctx* ctx, int rank, int world, const uint8_t nccl_id[128]);
+
+/* ---- series (replaces tsdiscord::TimeSeries, types.hpp:16-32) ------------
+ * Validates n >= 3 and finiteness (src/types.cpp:8-13), uploads once. */
+int tsd_series_set(tsd_ctx* ctx, const double* values, int64_t n);
+int64_t tsd_series_len(const tsd_ctx* ctx);
+
+/* ---- rolling statistics (stats.hpp:29,33; src/stats.cpp:7-58) -------------
+ * init: Eq. 4 running sums for length m; mu/sigma receive n-m+1 values.
+ * advance: Eq. 7-8 from length m to m+1 given mu/sigma of length m
+ * (n-m+1 values in); writes n-m values.  Both run on the device and are
+ * bit-identical to the reference's FP64 arithmetic. */
+int tsd_init_stats(tsd_ctx* ctx, int64_t m, double* mu, double* sigma);
+int tsd_advance_stats(tsd_ctx* ctx, int64_t m, const double* mu_in, const double* sigma_in,
+                      double* mu_out, double* sigma_out);
+
+/* ---- layout and threshold schedule (host arithmetic, bit-exact) ----------
+ * compute_layout: src/types.cpp:26-39 -> out = {seglen, seg_n, num_seg, pad}.
+ * next_threshold: src/merlin.cpp:35-55; phase 0 first, 1 warmup, 2 steady;
+ * history = per-length minimal nn distances (unsquared). */
+int tsd_compute_layout(int64_t n, int64_t m, int64_t seglen, int64_t out[4]);
+int tsd_next_threshold(const double* history, int64_t history_len, int phase, int64_t min_len,
+                       double last_r, int failed, double* out);
+
+/* ---- PD3 range-discord scan (pardrag.hpp:87-93; src/pardrag.cpp:421-434) --
+ * Returns every subsequence whose exact nearest-neighbour distance^2 is
+ * >= r_sq, with that exact distance, sorted (nn desc, index asc).
+ * `seglen` is validated with compute_layout exactly like the reference.
+ * mu/sigma (nullable): caller-supplied stats for length m (n-m+1 values);
+ * NULL means "compute init_stats(m) on the device".
+ * *count receives the number of records; at most `cap` are written. */
+int tsd_pardrag(tsd_ctx* ctx, int64_t m, double r_sq, int64_t seglen, const double* mu,
+                const double* sigma, tsd_record* out, int64_t cap, int64_t* count);
+
+/* ---- MERLIN (merlin.hpp:50-54; src/merlin.cpp:57-137) ---------------------
+ * Arrays have L = max_len-min_len+1 entries (recs: L*top_k, row-major).
+ * counts[k]  records kept for length min_len+k (0 for failed lengths)
+ * failed[k]  1 if the length is in failed_lengths
+ * final_r[k], retries[k] as MerlinReport. */
+int tsd_merlin(tsd_ctx* ctx, int64_t min_len, int64_t max_len, const tsd_merlin_opts* opts,
+               int64_t* counts, tsd_record* recs, double* final_r, int64_t* retries,
+               uint8_t* failed);
+
+/* ---- exact nearest-neighbour profile on the device -----------------------
+ * brute_force_nn (drag.hpp:38; src/drag.cpp:137-149): exact nn^2 of every
+ * subsequence (n-m+1 values) with the reference arithmetic. */
+int tsd_brute_force_nn(tsd_ctx* ctx, int64_t m, double* out);
+
+/* ---- host utilities the reference API also exposes (io.hpp) --------------
+ * gen_randomwalk: src/io.cpp:110-119 (libstdc++ mt19937_64 + normal_distribution). */
+int tsd_gen_randomwalk(int64_t n, uint64_t seed, double* out);
+
+/* ---- accounting ---------------------------------------------------------- */
+int tsd_get_counters(const tsd_ctx* ctx, tsd_counters* out);
+int tsd_reset_counters(tsd_ctx* ctx);
+/* Diagnostic: FP32 FFMA throughput of `device` (TFLOP/s, 2 flops per FFMA),
+ * measured with a dependent-chain-free FFMA loop over all SMs. */
+int tsd_fp32_peak_probe(int device, double* tflops);
+/* Tuning knobs (testing only): key in {"dense_rows","sparse_rows","err_scale"}. */
+int tsd_set_param(tsd_ctx* ctx, const char* key, double value);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

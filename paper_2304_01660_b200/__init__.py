@@ -1,0 +1,350 @@
+"""paper_2304_01660_b200 — B200-native PALMAD (arXiv 2304.01660) discord discovery.
+
+Python binding of ``libtsdiscord_b200.so`` (C-ABI in ``include/tsdiscord_b200.h``).
+The names mirror the reference's C++ API (``/root/reference/proj/include/tsdiscord``):
+``merlin``, ``merlin_full``, ``pardrag``, ``init_stats``, ``advance_stats``,
+``compute_layout``, ``next_threshold``, ``brute_force_nn``, ``gen_randomwalk``, with the
+same argument meaning and the same exception kinds (``ValueError`` for the
+reference's ``std::invalid_argument``, ``LogicError`` for ``std::logic_error``,
+``RuntimeError`` otherwise).  Every compute call runs on the GPU; a missing
+library or device raises — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtsdiscord_b200.so")
+
+TSD_OK, TSD_EINVAL, TSD_ELOGIC, TSD_ERUNTIME, TSD_ECUDA = range(5)
+
+RECORD_DTYPE = np.dtype([("index", np.int64), ("nn_dist_sq", np.float64), ("nn_dist", np.float64)])
+
+# Every symbol include/tsdiscord_b200.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "tsd_ctx_create", "tsd_ctx_destroy", "tsd_last_error", "tsd_create_error",
+    "tsd_nccl_unique_id", "tsd_ctx_join", "tsd_series_set", "tsd_series_len",
+    "tsd_init_stats", "tsd_advance_stats", "tsd_compute_layout", "tsd_next_threshold",
+    "tsd_pardrag", "tsd_merlin", "tsd_brute_force_nn", "tsd_gen_randomwalk",
+    "tsd_get_counters", "tsd_reset_counters", "tsd_set_param", "tsd_fp32_peak_probe",
+)
+
+
+class LogicError(RuntimeError):
+    """std::logic_error of the reference (e.g. merlin.cpp:19 window too short)."""
+
+
+class _Opts(C.Structure):
+    _fields_ = [("top_k", C.c_int64), ("seglen", C.c_int64), ("workers", C.c_int64),
+                ("max_retries", C.c_int64), ("reuse_stats", C.c_int32)]
+
+
+class Counters(C.Structure):
+    _fields_ = [("cells", C.c_uint64), ("seed_dots", C.c_uint64), ("seed_flops", C.c_uint64),
+                ("rechecks", C.c_uint64), ("exact_pairs", C.c_uint64),
+                ("pardrag_calls", C.c_uint64), ("scan_launches", C.c_uint64),
+                ("kernel_launches", C.c_uint64),
+                ("scan_ms", C.c_double), ("total_ms", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_ip = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+_u8 = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
+_i64 = C.c_int64
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Loads (once) and binds the C-ABI.  Raises if the library was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built: run `python -m paper_2304_01660_b200.build`")
+    L = C.CDLL(path)
+
+    def f(name, res, args):
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+
+    vp = C.c_void_p
+    f("tsd_ctx_create", C.c_int, [C.c_int, C.POINTER(vp)])
+    f("tsd_ctx_destroy", None, [vp])
+    f("tsd_last_error", C.c_char_p, [vp])
+    f("tsd_create_error", C.c_char_p, [])
+    f("tsd_nccl_unique_id", C.c_int, [C.c_char_p])
+    f("tsd_ctx_join", C.c_int, [vp, C.c_int, C.c_int, C.c_char_p])
+    f("tsd_series_set", C.c_int, [vp, _dp, _i64])
+    f("tsd_series_len", _i64, [vp])
+    f("tsd_init_stats", C.c_int, [vp, _i64, _dp, _dp])
+    f("tsd_advance_stats", C.c_int, [vp, _i64, _dp, _dp, _dp, _dp])
+    f("tsd_compute_layout", C.c_int, [_i64, _i64, _i64, _ip])
+    f("tsd_next_threshold", C.c_int, [_dp, _i64, C.c_int, _i64, C.c_double, C.c_int,
+                                      C.POINTER(C.c_double)])
+    f("tsd_pardrag", C.c_int, [vp, _i64, C.c_double, _i64, vp, vp, vp, _i64, C.POINTER(_i64)])
+    f("tsd_merlin", C.c_int, [vp, _i64, _i64, C.POINTER(_Opts), _ip, vp, _dp, _ip, _u8])
+    f("tsd_brute_force_nn", C.c_int, [vp, _i64, _dp])
+    f("tsd_gen_randomwalk", C.c_int, [_i64, C.c_uint64, _dp])
+    f("tsd_get_counters", C.c_int, [vp, C.POINTER(Counters)])
+    f("tsd_reset_counters", C.c_int, [vp])
+    f("tsd_set_param", C.c_int, [vp, C.c_char_p, C.c_double])
+    f("tsd_fp32_peak_probe", C.c_int, [C.c_int, C.POINTER(C.c_double)])
+    _lib = L
+    return L
+
+
+def _raise(code: int, msg: str):
+    if code == TSD_EINVAL:
+        raise ValueError(msg)
+    if code == TSD_ELOGIC:
+        raise LogicError(msg)
+    raise RuntimeError(msg)
+
+
+def _host_check(rc):
+    if rc != TSD_OK:
+        _raise(rc, (load_library().tsd_last_error(None) or b"").decode())
+
+
+# ---------------------------------------------------------------------------
+# host arithmetic (bit-exact restatements, no device needed)
+def compute_layout(n: int, m: int, seglen: int) -> dict:
+    """src/types.cpp:26-39 -> {seglen, seg_n, num_seg, pad}; ValueError on bad input."""
+    out = np.zeros(4, np.int64)
+    _host_check(load_library().tsd_compute_layout(n, m, seglen, out))
+    return dict(seglen=int(out[0]), seg_n=int(out[1]), num_seg=int(out[2]), pad=int(out[3]))
+
+
+FIRST, WARMUP, STEADY = 0, 1, 2
+
+
+def next_threshold(history, phase: int, min_len: int, last_r: float, failed: bool) -> float:
+    """src/merlin.cpp:35-55 (phase 0 first, 1 warmup, 2 steady)."""
+    h = np.ascontiguousarray(history, dtype=np.float64) if len(history) else np.zeros(1)
+    r = C.c_double(0.0)
+    _host_check(load_library().tsd_next_threshold(h, len(history), phase, min_len, last_r,
+                                                   1 if failed else 0, C.byref(r)))
+    return r.value
+
+
+def fp32_peak_tflops(device: int = 0) -> float:
+    """Measured FP32 FFMA peak of the device (diagnostic microbenchmark)."""
+    v = C.c_double(0.0)
+    _host_check(load_library().tsd_fp32_peak_probe(device, C.byref(v)))
+    return v.value
+
+
+def gen_randomwalk(n: int, seed: int) -> np.ndarray:
+    """src/io.cpp:110-119: x1 = 0, x_{i+1} = x_i + N(0,1) (libstdc++ mt19937_64)."""
+    out = np.empty(max(n, 1), np.float64)
+    _host_check(load_library().tsd_gen_randomwalk(n, seed, out))
+    return out[:n]
+
+
+# ---------------------------------------------------------------------------
+@dataclass
+class MerlinReport:
+    """merlin.hpp:40-44; per_length maps m -> structured array of records."""
+    min_len: int
+    max_len: int
+    per_length: dict = field(default_factory=dict)
+    failed_lengths: list = field(default_factory=list)
+    final_r: np.ndarray = None
+    retries: np.ndarray = None
+    device_ms: float = 0.0
+
+
+class Engine:
+    """One GPU context (device, stream, resident series, scan state)."""
+
+    def __init__(self, device: int = 0):
+        L = load_library()
+        self._L = L
+        h = C.c_void_p()
+        rc = L.tsd_ctx_create(device, C.byref(h))
+        if rc != TSD_OK:
+            _raise(rc, (L.tsd_create_error() or b"").decode())
+        self._h = h
+        self._series = None
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.tsd_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != TSD_OK:
+            _raise(rc, (self._L.tsd_last_error(self._h) or b"").decode())
+
+    # -- multi-GPU --------------------------------------------------------
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _host_check(load_library().tsd_nccl_unique_id(buf))
+        return buf.raw
+
+    def join(self, rank: int, world: int, nccl_id: bytes | None = None):
+        idb = C.create_string_buffer(nccl_id or b"\0" * 128, 128)
+        self._check(self._L.tsd_ctx_join(self._h, rank, world, idb))
+
+    # -- series / stats -----------------------------------------------------
+    def set_series(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        self._check(self._L.tsd_series_set(self._h, x, len(x)))
+        self._series = x
+
+    @property
+    def n(self) -> int:
+        return int(self._L.tsd_series_len(self._h))
+
+    def init_stats(self, m: int):
+        N = max(self.n - m + 1, 1)
+        mu, sg = np.empty(N), np.empty(N)
+        self._check(self._L.tsd_init_stats(self._h, m, mu, sg))
+        return mu, sg
+
+    def advance_stats(self, m: int, mu, sigma):
+        mu = np.ascontiguousarray(mu, dtype=np.float64)
+        sigma = np.ascontiguousarray(sigma, dtype=np.float64)
+        N = max(self.n - m, 1)
+        mo, so = np.empty(N), np.empty(N)
+        self._check(self._L.tsd_advance_stats(self._h, m, mu, sigma, mo, so))
+        return mo, so
+
+    # -- scans --------------------------------------------------------------
+    def pardrag(self, m: int, r_sq: float, seglen: int, stats=None) -> np.ndarray:
+        N = max(self.n - m + 1, 1)
+        out = np.zeros(N, RECORD_DTYPE)
+        cnt = _i64(0)
+        mu = sg = None
+        if stats is not None:
+            mu = np.ascontiguousarray(stats[0], dtype=np.float64)
+            sg = np.ascontiguousarray(stats[1], dtype=np.float64)
+        self._check(self._L.tsd_pardrag(
+            self._h, m, float(r_sq), seglen,
+            mu.ctypes.data if mu is not None else None,
+            sg.ctypes.data if sg is not None else None,
+            out.ctypes.data, N, C.byref(cnt)))
+        return out[: cnt.value].copy()
+
+    def brute_force_nn(self, m: int) -> np.ndarray:
+        out = np.empty(max(self.n - m + 1, 1))
+        self._check(self._L.tsd_brute_force_nn(self._h, m, out))
+        return out
+
+    def merlin_full(self, min_len: int, max_len: int, top_k: int = 1, seglen: int = 512,
+                    workers: int = 1, max_retries: int = 100, reuse_stats: bool = True) -> MerlinReport:
+        Ln = max(max_len - min_len + 1, 1)
+        k = max(top_k, 1)
+        counts = np.zeros(Ln, np.int64)
+        recs = np.zeros((Ln, k), RECORD_DTYPE)
+        final_r = np.zeros(Ln)
+        retries = np.zeros(Ln, np.int64)
+        failed = np.zeros(Ln, np.uint8)
+        o = _Opts(top_k, seglen, workers, max_retries, 1 if reuse_stats else 0)
+        self._check(self._L.tsd_merlin(self._h, min_len, max_len, C.byref(o), counts,
+                                       recs.ctypes.data, final_r, retries, failed))
+        rep = MerlinReport(min_len, max_len, final_r=final_r[: max_len - min_len + 1],
+                           retries=retries[: max_len - min_len + 1])
+        for i in range(max_len - min_len + 1):
+            m = min_len + i
+            if failed[i]:
+                rep.failed_lengths.append(m)
+            else:
+                rep.per_length[m] = recs[i][: counts[i]].copy()
+        rep.device_ms = self.counters()["total_ms"]
+        return rep
+
+    # -- accounting / knobs ---------------------------------------------------
+    def counters(self) -> dict:
+        c = Counters()
+        self._check(self._L.tsd_get_counters(self._h, C.byref(c)))
+        return c.as_dict()
+
+    def reset_counters(self):
+        self._check(self._L.tsd_reset_counters(self._h))
+
+    def set_param(self, key: str, value: float):
+        self._check(self._L.tsd_set_param(self._h, key.encode(), float(value)))
+
+
+_default: Engine | None = None
+
+
+def default_engine() -> Engine:
+    global _default
+    if _default is None:
+        _default = Engine(int(os.environ.get("TSD_DEVICE", "0")))
+    return _default
+
+
+def _with_series(x) -> Engine:
+    e = default_engine()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    if e._series is None or len(e._series) != len(x) or not np.array_equal(e._series, x):
+        e.set_series(x)
+    return e
+
+
+# reference-named module-level API -------------------------------------------
+def init_stats(x, m: int):
+    """stats.hpp:29 — (mu, sigma) for length m, computed on the GPU."""
+    return _with_series(x).init_stats(m)
+
+
+def advance_stats(x, m: int, mu, sigma):
+    """stats.hpp:33 — Eq. 7-8 from length m to m+1 on the GPU."""
+    return _with_series(x).advance_stats(m, mu, sigma)
+
+
+def pardrag(x, m: int, r_sq: float, seglen: int, workers: int = 1, early_exit: bool = True):
+    """pardrag.hpp:87-89 — range discords {i : nn(i)^2 >= r_sq}, sorted."""
+    return _with_series(x).pardrag(m, r_sq, seglen)
+
+
+def brute_force_nn(x, m: int):
+    """drag.hpp:38 — exact nn^2 profile (GPU)."""
+    return _with_series(x).brute_force_nn(m)
+
+
+def merlin_full(x, min_len: int, max_len: int, top_k: int = 1, seglen: int = 512, workers: int = 1,
+                max_retries: int = 100, reuse_stats: bool = True) -> MerlinReport:
+    """merlin.hpp:50-51."""
+    return _with_series(x).merlin_full(min_len, max_len, top_k, seglen, workers, max_retries,
+                                       reuse_stats)
+
+
+def merlin(x, min_len: int, max_len: int, top_k: int = 1, seglen: int = 512, workers: int = 1,
+           max_retries: int = 100, reuse_stats: bool = True) -> MerlinReport:
+    """merlin.hpp:53-54 (returns the report; .per_length / .failed_lengths)."""
+    return merlin_full(x, min_len, max_len, top_k, seglen, workers, max_retries, reuse_stats)
+
+
+def format_double(v: float) -> str:
+    """io.cpp:42-46 shortest round-trip (Python repr is the same algorithm)."""
+    r = repr(float(v))
+    return r[:-2] if r.endswith(".0") and "e" not in r else r
+
+
+def discords_csv(per_length: dict) -> str:
+    """write_discords_csv (io.cpp:121-130)."""
+    lines = ["length,index,nn_dist,nn_dist_sq,score"]
+    for m in sorted(per_length):
+        for r in per_length[m]:
+            lines.append(f"{m},{int(r['index'])},{format_double(r['nn_dist'])},"
+                         f"{format_double(r['nn_dist_sq'])},{format_double(r['nn_dist_sq'] / (2.0 * m))}")
+    return "\n".join(lines) + "\n"

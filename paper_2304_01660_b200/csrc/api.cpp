@@ -1,0 +1,335 @@
+// C++ drop-in API (namespace tsdiscord) over the C-ABI of libtsdiscord_b200.so.
+//
+// Callers of the reference library (/root/reference/proj/include/tsdiscord)
+// relink against this library unchanged: the same declarations, the same
+// exception types for the same preconditions, results equal to the
+// reference's.  Every compute entry point goes to the GPU through one
+// thread-local context (device from $TSD_DEVICE, default 0); a missing or
+// failing GPU raises std::runtime_error — there is no CPU fallback.
+#include <algorithm>
+#include <charconv>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <ostream>
+#include <sstream>
+#include <string>
+
+#include "tsdiscord/drag.hpp"
+#include "tsdiscord/io.hpp"
+#include "tsdiscord/merlin.hpp"
+#include "tsdiscord/pardrag.hpp"
+#include "tsdiscord/stats.hpp"
+#include "tsdiscord/types.hpp"
+#include "tsdiscord_b200.h"
+
+namespace tsdiscord {
+
+namespace {
+
+[[noreturn]] void rethrow(int code, const char* msg) {
+    const std::string m = msg ? msg : "";
+    switch (code) {
+        case TSD_EINVAL: throw std::invalid_argument(m);
+        case TSD_ELOGIC: throw std::logic_error(m);
+        default: throw std::runtime_error(m);
+    }
+}
+
+struct Ctx {
+    tsd_ctx* c = nullptr;
+    std::vector<double> uploaded;
+    Ctx() {
+        const char* dev = std::getenv("TSD_DEVICE");
+        const int rc = tsd_ctx_create(dev ? std::atoi(dev) : 0, &c);
+        if (rc != TSD_OK) rethrow(TSD_ERUNTIME, tsd_create_error());
+    }
+    ~Ctx() { tsd_ctx_destroy(c); }
+    void check(int rc) {
+        if (rc != TSD_OK) rethrow(rc, tsd_last_error(c));
+    }
+    void series(const TimeSeries& s) {
+        const auto& v = s.values();
+        if (v.size() == uploaded.size() && std::memcmp(v.data(), uploaded.data(), v.size() * 8) == 0)
+            return;
+        check(tsd_series_set(c, v.data(), (int64_t)v.size()));
+        uploaded = v;
+    }
+};
+
+Ctx& ctx() {
+    thread_local std::unique_ptr<Ctx> c;
+    if (!c) c = std::make_unique<Ctx>();
+    return *c;
+}
+
+std::vector<DiscordRecord> to_records(const std::vector<tsd_record>& r, size_t n) {
+    std::vector<DiscordRecord> out(n);
+    for (size_t i = 0; i < n; ++i) out[i] = {(index_t)r[i].index, r[i].nn_dist_sq, r[i].nn_dist};
+    return out;
+}
+
+std::vector<DiscordRecord> run_pardrag(const TimeSeries& series, index_t m, double r_sq,
+                                       index_t seglen, const RollingStats* stats) {
+    Ctx& c = ctx();
+    c.series(series);
+    const index_t N = series.n() - m + 1;
+    std::vector<tsd_record> buf(std::max<index_t>(N, 1));
+    int64_t cnt = 0;
+    const bool use_stats = stats && (index_t)stats->mu.size() >= N && stats->m == m;
+    c.check(tsd_pardrag(c.c, m, r_sq, seglen, use_stats ? stats->mu.data() : nullptr,
+                        use_stats ? stats->sigma.data() : nullptr, buf.data(), (int64_t)buf.size(), &cnt));
+    return to_records(buf, (size_t)cnt);
+}
+
+}  // namespace
+
+// ---- types (reference: src/types.cpp) ---------------------------------------
+TimeSeries::TimeSeries(std::vector<double> values) : v_(std::move(values)) {
+    if (n() < 3) throw std::invalid_argument("time series needs at least 3 points");
+    for (double x : v_)
+        if (!std::isfinite(x)) throw std::invalid_argument("time series contains a non-finite value");
+}
+
+void sort_discords(std::vector<DiscordRecord>& r) {
+    std::sort(r.begin(), r.end(), [](const DiscordRecord& a, const DiscordRecord& b) {
+        return a.nn_dist_sq != b.nn_dist_sq ? a.nn_dist_sq > b.nn_dist_sq : a.index < b.index;
+    });
+}
+
+bool non_self_match(index_t i, index_t j, index_t m) { return (i > j ? i - j : j - i) >= m; }
+
+SegmentLayout compute_layout(index_t n, index_t m, index_t seglen) {
+    int64_t o[4];
+    const int rc = tsd_compute_layout(n, m, seglen, o);
+    if (rc != TSD_OK) rethrow(rc, tsd_last_error(nullptr));
+    return SegmentLayout{(index_t)o[0], (index_t)o[1], (index_t)o[2], (index_t)o[3]};
+}
+
+// ---- stats -------------------------------------------------------------------
+RollingStats init_stats(const TimeSeries& series, index_t m) {
+    if (m < 2 || m > series.n() - 1) throw std::invalid_argument("init_stats: length out of range");
+    Ctx& c = ctx();
+    c.series(series);
+    RollingStats s;
+    s.m = m;
+    s.valid_count = series.n() - m + 1;
+    s.mu.resize((size_t)s.valid_count);
+    s.sigma.resize((size_t)s.valid_count);
+    c.check(tsd_init_stats(c.c, m, s.mu.data(), s.sigma.data()));
+    return s;
+}
+
+RollingStats advance_stats(const RollingStats& stats, const TimeSeries& series) {
+    if (stats.m + 1 > series.n() - 1) throw std::invalid_argument("advance_stats: next length out of range");
+    Ctx& c = ctx();
+    c.series(series);
+    RollingStats next = stats;  // stale tail entries carry over, as in the reference
+    next.m = stats.m + 1;
+    next.valid_count = stats.valid_count - 1;
+    std::vector<double> mu((size_t)next.valid_count), sg((size_t)next.valid_count);
+    c.check(tsd_advance_stats(c.c, stats.m, stats.mu.data(), stats.sigma.data(), mu.data(), sg.data()));
+    std::copy(mu.begin(), mu.end(), next.mu.begin());
+    std::copy(sg.begin(), sg.end(), next.sigma.begin());
+    return next;
+}
+
+// ---- pardrag / drag ------------------------------------------------------------
+std::vector<DiscordRecord> pardrag(const TimeSeries& series, index_t m, double r_sq, index_t seglen,
+                                   index_t /*workers*/, bool /*early_exit*/) {
+    return run_pardrag(series, m, r_sq, seglen, nullptr);
+}
+
+std::vector<DiscordRecord> pardrag(const TimeSeries& series, index_t m, double r_sq,
+                                   const RollingStats& stats, const SegmentLayout& layout,
+                                   const ParOptions& /*opts*/) {
+    return run_pardrag(series, m, r_sq, layout.seglen, &stats);
+}
+
+std::vector<DiscordRecord> drag(const TimeSeries& series, index_t m, double r_sq, bool) {
+    // same range-discord set; the segment length only shapes the reference's schedule
+    return run_pardrag(series, m, r_sq, std::min<index_t>(std::max<index_t>(2 * m, 512), series.n()),
+                       nullptr);
+}
+
+std::vector<double> brute_force_nn(const TimeSeries& series, index_t m) {
+    Ctx& c = ctx();
+    c.series(series);
+    std::vector<double> nn((size_t)(series.n() - m + 1));
+    c.check(tsd_brute_force_nn(c.c, m, nn.data()));
+    return nn;
+}
+
+std::vector<DiscordRecord> brute_force_topk(const TimeSeries& series, index_t m, index_t k) {
+    const index_t count = series.subseq_count(m);
+    if (k < 1 || k > count) throw std::invalid_argument("brute_force_topk: k out of range");
+    const auto nn = brute_force_nn(series, m);
+    std::vector<DiscordRecord> all((size_t)count);
+    for (index_t i = 0; i < count; ++i) all[(size_t)i] = {i + 1, nn[(size_t)i], std::sqrt(nn[(size_t)i])};
+    sort_discords(all);
+    all.resize((size_t)k);
+    return all;
+}
+
+// ---- merlin ---------------------------------------------------------------------
+double ThresholdHistory::window_mean() const {
+    if (nn_dist.size() < 5) throw std::logic_error("threshold history window too short");
+    double s = 0.0;
+    for (size_t k = nn_dist.size() - 5; k < nn_dist.size(); ++k) s += nn_dist[k];
+    return s / 5.0;
+}
+
+double ThresholdHistory::window_std() const {
+    const double mu = window_mean();
+    double s = 0.0;
+    for (size_t k = nn_dist.size() - 5; k < nn_dist.size(); ++k) s += (nn_dist[k] - mu) * (nn_dist[k] - mu);
+    return std::sqrt(s / 5.0);
+}
+
+double next_threshold(const ThresholdHistory& h, ThresholdPhase phase, index_t min_len, double last_r,
+                      bool failed) {
+    double out = 0.0;
+    const int rc = tsd_next_threshold(h.nn_dist.data(), (int64_t)h.nn_dist.size(),
+                                      phase == ThresholdPhase::first ? 0 : phase == ThresholdPhase::warmup ? 1 : 2,
+                                      min_len, last_r, failed ? 1 : 0, &out);
+    if (rc != TSD_OK) rethrow(rc, tsd_last_error(nullptr));
+    return out;
+}
+
+MerlinReport merlin_full(const TimeSeries& series, index_t min_len, index_t max_len,
+                         const MerlinOptions& opts) {
+    Ctx& c = ctx();
+    c.series(series);
+    const index_t L = std::max<index_t>(max_len - min_len + 1, 1);
+    const index_t k = std::max<index_t>(opts.top_k, 1);
+    std::vector<int64_t> counts((size_t)L), retries((size_t)L);
+    std::vector<tsd_record> recs((size_t)(L * k));
+    std::vector<double> final_r((size_t)L);
+    std::vector<uint8_t> failed((size_t)L);
+    tsd_merlin_opts o{opts.top_k, opts.seglen, opts.workers, opts.max_retries, opts.reuse_stats ? 1 : 0};
+    c.check(tsd_merlin(c.c, min_len, max_len, &o, counts.data(), recs.data(), final_r.data(),
+                       retries.data(), failed.data()));
+    MerlinReport rep;
+    rep.discords.min_len = min_len;
+    rep.discords.max_len = max_len;
+    for (index_t i = 0; i < L; ++i) {
+        const index_t m = min_len + i;
+        rep.final_r.push_back(final_r[(size_t)i]);
+        rep.retries.push_back((index_t)retries[(size_t)i]);
+        if (failed[(size_t)i]) {
+            rep.discords.failed_lengths.push_back(m);
+            continue;
+        }
+        std::vector<DiscordRecord> lst;
+        for (int64_t j = 0; j < counts[(size_t)i]; ++j) {
+            const tsd_record& r = recs[(size_t)(i * k + j)];
+            lst.push_back({(index_t)r.index, r.nn_dist_sq, r.nn_dist});
+        }
+        rep.discords.per_length[m] = std::move(lst);
+    }
+    return rep;
+}
+
+MultiLengthDiscordSet merlin(const TimeSeries& series, index_t min_len, index_t max_len,
+                             const MerlinOptions& opts) {
+    return merlin_full(series, min_len, max_len, opts).discords;
+}
+
+// ---- io -------------------------------------------------------------------------
+std::string format_double(double value) {
+    char buf[40];
+    auto res = std::to_chars(buf, buf + sizeof(buf), value);
+    return std::string(buf, res.ptr);
+}
+
+TimeSeries gen_randomwalk(index_t n, std::uint64_t seed) {
+    if (n < 3) throw std::invalid_argument("gen_randomwalk: n must be at least 3");
+    std::vector<double> v((size_t)n);
+    const int rc = tsd_gen_randomwalk(n, seed, v.data());
+    if (rc != TSD_OK) rethrow(rc, tsd_last_error(nullptr));
+    return TimeSeries(std::move(v));
+}
+
+void write_series(const TimeSeries& series, std::ostream& out) {
+    for (double v : series.values()) out << format_double(v) << '\n';
+}
+
+void write_discords_csv(const MultiLengthDiscordSet& d, std::ostream& out) {
+    out << "length,index,nn_dist,nn_dist_sq,score\n";
+    for (const auto& [m, lst] : d.per_length)
+        for (const auto& r : lst)
+            out << m << ',' << r.index << ',' << format_double(r.nn_dist) << ','
+                << format_double(r.nn_dist_sq) << ','
+                << format_double(r.nn_dist_sq / (2.0 * static_cast<double>(m))) << '\n';
+}
+
+namespace {
+std::string strip(const std::string& s) {
+    size_t a = 0, b = s.size();
+    while (a < b && std::isspace((unsigned char)s[a])) ++a;
+    while (b > a && std::isspace((unsigned char)s[b - 1])) --b;
+    return s.substr(a, b - a);
+}
+bool to_double(const std::string& tok, double& out) {
+    const std::string t = strip(tok);
+    if (t.empty()) return false;
+    auto res = std::from_chars(t.data(), t.data() + t.size(), out);
+    return res.ec == std::errc() && res.ptr == t.data() + t.size();
+}
+std::vector<std::string> split_csv(const std::string& line) {
+    std::vector<std::string> f;
+    std::string cur;
+    std::istringstream is(line);
+    while (std::getline(is, cur, ',')) f.push_back(cur);
+    if (!line.empty() && line.back() == ',') f.emplace_back();
+    return f;
+}
+}  // namespace
+
+TimeSeries load_series(const std::string& path, const std::string& column) {
+    std::ifstream in(path);
+    if (!in) throw std::runtime_error("cannot open input file: " + path);
+    std::vector<double> values;
+    std::string line;
+    long lineno = 0;
+    long col = -1;
+    bool header_seen = false;
+    while (std::getline(in, line)) {
+        ++lineno;
+        if (!line.empty() && line.back() == '\r') line.pop_back();
+        if (strip(line).empty()) continue;
+        const auto fields = split_csv(line);
+        if (col < 0) {
+            // column selection: empty -> first, digits -> position, else header name
+            if (column.empty()) col = 0;
+            else if (std::all_of(column.begin(), column.end(), ::isdigit)) col = std::atol(column.c_str());
+            else {
+                for (size_t i = 0; i < fields.size(); ++i)
+                    if (strip(fields[i]) == column) col = (long)i;
+                if (col < 0) throw std::runtime_error("column not found: " + column);
+                header_seen = true;
+                continue;
+            }
+        }
+        if ((size_t)col >= fields.size())
+            throw std::runtime_error("line " + std::to_string(lineno) + ": missing column");
+        double v;
+        if (!to_double(fields[(size_t)col], v)) {
+            if (!header_seen && values.empty()) {
+                header_seen = true;  // a leading header line
+                continue;
+            }
+            throw std::runtime_error("line " + std::to_string(lineno) + ": not a number: " +
+                                     strip(fields[(size_t)col]));
+        }
+        values.push_back(v);
+    }
+    if (values.size() < 3)
+        throw std::runtime_error("series too short: need at least 3 values, got " +
+                                 std::to_string(values.size()));
+    return TimeSeries(std::move(values));
+}
+
+}  // namespace tsdiscord

@@ -1,0 +1,71 @@
+// Shared device-side definitions for the PALMAD engine (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tsd {
+
+// include/tsdiscord/stats.hpp:11 — a subsequence with sigma below this is constant.
+constexpr double kSigmaEps = 1e-12;
+
+// ---- tile-scan geometry ----------------------------------------------------
+// One CTA sweeps a parallelogram of the distance matrix: `rows` consecutive
+// candidates c (walk order given by dir) x W consecutive diagonals k = q - c.
+// Each thread owns D adjacent diagonals and walks them down (dir=+1, k >= m)
+// or up (dir=-1, k <= -m) with the FP32 centered-covariance recurrence, so
+// every invalid cell (q outside [0,N)) lies at the far end of its walk.
+constexpr int kThreads = 128;            // threads per scan CTA
+constexpr int kDiag = 9;                 // diagonals per thread (odd: conflict-free strided smem)
+constexpr int kW = kThreads * kDiag;     // 1152 diagonals per tile
+constexpr int kMaxRows = 1024;           // max rows per tile
+constexpr int kSeedChunk = 512;          // seed dot products are staged m in chunks of this
+
+struct TileDesc {
+    int r0;    // first row (0-based candidate index)
+    int rows;  // number of rows (<= kMaxRows), all < N
+    int k0;    // lowest diagonal of the tile; the tile covers [k0, k0 + kW)
+    int dir;   // +1: positive side walked downward; -1: negative side walked upward
+};
+
+enum ScanMode : int {
+    kPrune = 0,       // dense band: kill both ends of any pair with d^2 < r^2
+    kPruneTrack = 1,  // sparse rows: prune + track a lower bound of each live row's max corr
+    kCollect = 2      // survivors: push every pair that may attain the row's exact minimum
+};
+
+struct ScanParams {
+    const double* t;     // series (n)
+    const double* mu;    // FP64 rolling mean, length m (N)
+    const double* sig;   // FP64 rolling std (N)
+    const float* df;     // FP32 (t[i+m-1]-t[i-1])/2             (N; [0] unused)
+    const float* dg;     // FP32 (t[i+m-1]-mu_i)+(t[i-1]-mu_{i-1}) (N; [0] unused)
+    const float* nrm;    // FP32 1/(sqrt(m)*sigma_i), 0 if constant (N)
+    int n, m, N;
+    double r_sq;         // squared threshold
+    double thr0;         // 1 - r_sq/(2m): corr > thr0  <=>  d^2 < r^2
+    double err_k;        // error model: |cov_fp32 - cov| <= err_k*eps*m*smax_c*smax_q*(rows+8)
+    uint8_t* alive;      // candidate flags (N); 1 = may still be a range discord
+    int2* queue;         // knife-edge pairs for the exact FP64 recheck
+    int* queue_count;
+    int queue_cap;
+    unsigned* ymax;      // kPruneTrack: ordered-float key of max lower-bound (x - E*qn) per row
+    const float* ythr;   // kCollect: per-row collection threshold (decoded ymax)
+    int2* coll;          // kCollect output pairs
+    int* coll_count;
+    int coll_cap;
+    const TileDesc* tiles;
+    unsigned long long* cells;  // accounting
+    unsigned long long* seeds;
+};
+
+// Order-preserving float <-> uint32 map (for atomicMax on floats of any sign).
+__device__ __forceinline__ unsigned f2key(float f) {
+    const unsigned b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(unsigned k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+}  // namespace tsd

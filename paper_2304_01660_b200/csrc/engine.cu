@@ -1,0 +1,842 @@
+// Host engine + C-ABI of libtsdiscord_b200.so.
+//
+// The control flow mirrors the reference exactly where it is observable
+// (validation, MERLIN's length loop and threshold schedule, record order,
+// error kinds); the scan itself is re-designed for B200:
+//
+//   pardrag(m, r^2)  (reference: src/pardrag.cpp:421-434)
+//     dense  : band tiles k in [m, m + b*kW) over all rows, both ends of every
+//              certain pair are killed (select + neighbour clearing, Alg. 3)
+//     sparse : full rows (both sides) for the remaining candidates, with kills,
+//              plus a lower bound of every live row's max correlation (Alg. 4)
+//     exact  : survivors' near-minimum pairs re-evaluated with the reference's
+//              FP64 znormalize + sq_ed (pardrag.cpp:378-416)
+//   merlin (src/merlin.cpp:57-132): sequential lengths, Eq. 7-8 stats on the
+//   device, adaptive r; only (count, survivors) cross to the host per try.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/tsdiscord_b200.h"
+#include "common.cuh"
+#include "engine_internal.h"
+#include "nccl_shim.h"
+
+using namespace tsd;
+
+namespace {
+
+thread_local std::string g_create_err;
+
+struct Fail {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Fail{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(TSD_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    void ensure(size_t n) {
+        if (n <= cap) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        ck(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMalloc");
+        cap = n;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+template <typename T>
+struct HBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    void ensure(size_t n) {
+        if (n <= cap) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        ck(cudaMallocHost(&p, std::max<size_t>(n, 1) * sizeof(T)), "cudaMallocHost");
+        cap = n;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+constexpr int kQueueCap = 1 << 22;
+constexpr int kCollCap = 1 << 23;
+
+}  // namespace
+
+struct tsd_ctx {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    std::string err;
+
+    // series
+    int64_t n = 0;
+    std::vector<double> h_t;
+    DBuf<double> t;
+
+    // per-length state
+    int64_t stats_m = -1;  // length the device mu/sig currently hold (-1: none)
+    DBuf<double> mu, sig, scr_a, scr_b;
+    int64_t derived_m = -1;
+    DBuf<float> df, dg, nrm;
+
+    // scan state
+    DBuf<uint8_t> alive;
+    DBuf<int2> queue, coll;
+    DBuf<int> counters;  // [0] queue, [1] coll, [2..3] const range
+    DBuf<unsigned> ymax;
+    DBuf<float> ythr;
+    DBuf<unsigned long long> nnkey, acc;  // acc: [0] cells, [1] seeds
+    DBuf<int> blk, list;
+    DBuf<double> nnout;
+    DBuf<TileDesc> tiles;
+    HBuf<TileDesc> h_tiles;
+    HBuf<int> h_int;
+    HBuf<double> h_dbl;
+    std::vector<int> h_list;
+
+    // tuning
+    int dense_rows = 512;
+    int sparse_rows = 0;  // 0: choose by cost model
+    double err_k = 4.0;
+
+    // accounting
+    tsd_counters ctr{};
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+
+    // multi-GPU (segment-sharded tiles; flags / maxima / minima all-reduced)
+    int rank = 0, world = 1;
+    void* comm = nullptr;
+
+    // ------------------------------------------------------------------
+    void sync() { ck(cudaStreamSynchronize(st), "stream sync"); }
+
+    void allreduce_min_u8(uint8_t* p, size_t cnt) {
+        if (world > 1) nccl_allreduce(comm, p, cnt, 0 /*u8 min*/, st);
+    }
+    void allreduce_max_u32(unsigned* p, size_t cnt) {
+        if (world > 1) nccl_allreduce(comm, p, cnt, 1 /*u32 max*/, st);
+    }
+    void allreduce_min_u64(unsigned long long* p, size_t cnt) {
+        if (world > 1) nccl_allreduce(comm, p, cnt, 2 /*u64 min*/, st);
+    }
+    void allreduce_sum_i32(int* p, size_t cnt) {
+        if (world > 1) nccl_allreduce(comm, p, cnt, 3 /*i32 sum*/, st);
+    }
+
+    // ---- statistics --------------------------------------------------
+    void init_stats_dev(int64_t m) {
+        mu.ensure(n);
+        sig.ensure(n);
+        scr_a.ensure(n);
+        scr_b.ensure(n);
+        launch_init_stats(t.p, (int)n, (int)m, mu.p, sig.p, scr_a.p, scr_b.p, st);
+        ctr.kernel_launches += 2;
+        ck(cudaGetLastError(), "init_stats");
+        stats_m = m;
+        derived_m = -1;
+    }
+    void advance_stats_dev() {
+        launch_advance_stats(t.p, (int)n, (int)stats_m, mu.p, sig.p, st);
+        ctr.kernel_launches += 1;
+        ck(cudaGetLastError(), "advance_stats");
+        ++stats_m;
+        derived_m = -1;
+    }
+    void derive(int64_t m) {
+        if (derived_m == m) return;
+        const int64_t N = n - m + 1;
+        df.ensure(N);
+        dg.ensure(N);
+        nrm.ensure(N);
+        launch_derive(t.p, (int)m, (int)N, mu.p, sig.p, df.p, dg.p, nrm.p, st);
+        ctr.kernel_launches += 1;
+        ck(cudaGetLastError(), "derive");
+        derived_m = m;
+    }
+
+    // ---- scan helpers ---------------------------------------------------
+    ScanParams params(int64_t m, double r_sq) {
+        ScanParams p{};
+        p.t = t.p;
+        p.mu = mu.p;
+        p.sig = sig.p;
+        p.df = df.p;
+        p.dg = dg.p;
+        p.nrm = nrm.p;
+        p.n = (int)n;
+        p.m = (int)m;
+        p.N = (int)(n - m + 1);
+        p.r_sq = r_sq;
+        p.thr0 = 1.0 - r_sq / (2.0 * (double)m);
+        p.err_k = err_k;
+        p.alive = alive.p;
+        p.queue = queue.p;
+        p.queue_count = counters.p + 0;
+        p.queue_cap = kQueueCap;
+        p.ymax = ymax.p;
+        p.ythr = ythr.p;
+        p.coll = coll.p;
+        p.coll_count = counters.p + 1;
+        p.coll_cap = kCollCap;
+        p.tiles = tiles.p;
+        p.cells = acc.p + 0;
+        p.seeds = acc.p + 1;
+        return p;
+    }
+
+    void run_scan(int mode, const std::vector<TileDesc>& tl, ScanParams p) {
+        // shard tiles cyclically across ranks: every rank sweeps a disjoint set
+        std::vector<TileDesc> mine;
+        const std::vector<TileDesc>* use = &tl;
+        if (world > 1) {
+            for (size_t i = rank; i < tl.size(); i += world) mine.push_back(tl[i]);
+            use = &mine;
+        }
+        const size_t nt = use->size();
+        if (nt == 0) return;
+        h_tiles.ensure(nt);
+        tiles.ensure(nt);
+        // the previous scan (if any) must have consumed the pinned staging buffer
+        sync();
+        std::memcpy(h_tiles.p, use->data(), nt * sizeof(TileDesc));
+        ck(cudaMemcpyAsync(tiles.p, h_tiles.p, nt * sizeof(TileDesc), cudaMemcpyHostToDevice, st),
+           "tiles H2D");
+        p.tiles = tiles.p;
+        ck(cudaEventRecord(ev_a, st), "event");
+        launch_scan(mode, (int)nt, p, st);
+        ck(cudaGetLastError(), "scan launch");
+        ck(cudaEventRecord(ev_b, st), "event");
+        ck(cudaEventSynchronize(ev_b), "scan sync");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev_a, ev_b);
+        ctr.scan_ms += ms;
+        ctr.scan_launches += 1;
+        ctr.kernel_launches += 1;
+    }
+
+    void recheck(int64_t m, double r_sq) {
+        launch_ref_pairs(0, t.p, (int)m, queue.p, counters.p + 0, kQueueCap, r_sq, alive.p, nnkey.p,
+                         kQueueCap, st);
+        ck(cudaGetLastError(), "recheck");
+        ctr.kernel_launches += 1;
+    }
+
+    // returns count of set flags in alive[0..N) and (optionally) the ordered list on host
+    int compact_alive(int N, bool want_list) {
+        const int nb = compact_blocks(N);
+        blk.ensure(nb + 1);
+        list.ensure(N);
+        launch_compact(alive.p, N, blk.p, list.p, st);
+        ctr.kernel_launches += 3;
+        ck(cudaGetLastError(), "compact");
+        h_int.ensure(4);
+        ck(cudaMemcpyAsync(h_int.p, blk.p + nb, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+        sync();
+        const int cnt = h_int.p[0];
+        if (want_list) {
+            h_list.resize(cnt);
+            if (cnt > 0) {
+                ck(cudaMemcpy(h_list.data(), list.p, cnt * sizeof(int), cudaMemcpyDeviceToHost),
+                   "list D2H");
+            }
+        }
+        return cnt;
+    }
+
+    int read_counter(int idx) {
+        h_int.ensure(4);
+        ck(cudaMemcpyAsync(h_int.p, counters.p + idx, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+        sync();
+        return h_int.p[0];
+    }
+
+    // group sorted row indices into spans of at most `span` rows
+    static void group_rows(const std::vector<int>& lst, int span, std::vector<int2>& groups) {
+        groups.clear();
+        size_t i = 0;
+        while (i < lst.size()) {
+            const int a = lst[i];
+            size_t j = i;
+            while (j + 1 < lst.size() && lst[j + 1] - a < span) ++j;
+            groups.push_back(make_int2(a, lst[j]));
+            i = j + 1;
+        }
+    }
+
+    int choose_span(const std::vector<int>& lst, int64_t m) {
+        if (sparse_rows > 0) return sparse_rows;
+        // cost per q of one group ~ seeds (2*m FP32-equivalent FMAs per FP64 seed) + 3 per row
+        double best = 1e300;
+        int best_span = 64;
+        std::vector<int2> g;
+        for (int span : {16, 32, 64, 128, 256, 512, 1024}) {
+            group_rows(lst, span, g);
+            double cost = 0.0;
+            for (const auto& x : g) cost += 2.0 * (double)m + 3.0 * (double)(x.y - x.x + 1 + kDiag);
+            if (cost < best) {
+                best = cost;
+                best_span = span;
+            }
+        }
+        return best_span;
+    }
+
+    void full_row_tiles(const std::vector<int2>& groups, int64_t m, int N, std::vector<TileDesc>& out) {
+        out.clear();
+        std::vector<int> npos(groups.size()), nneg(groups.size());
+        int maxc = 0;
+        for (size_t g = 0; g < groups.size(); ++g) {
+            const int a = groups[g].x, b = groups[g].y;
+            const long long pos_span = (long long)N - a - m;  // k in [m, N-1-a]
+            npos[g] = pos_span > 0 ? (int)((pos_span + kW - 1) / kW) : 0;
+            const long long neg_span = (long long)b - m + 1;  // k in [-b, -m]
+            nneg[g] = neg_span > 0 ? (int)((neg_span + kW - 1) / kW) : 0;
+            maxc = std::max(maxc, std::max(npos[g], nneg[g]));
+        }
+        for (int i = 0; i < maxc; ++i) {
+            for (size_t g = 0; g < groups.size(); ++g) {
+                const int a = groups[g].x, b = groups[g].y;
+                const int rows = b - a + 1;
+                if (i < npos[g]) out.push_back(TileDesc{a, rows, (int)m + i * kW, +1});
+                if (i < nneg[g]) out.push_back(TileDesc{a, rows, -(int)m - (i + 1) * kW + 1, -1});
+            }
+        }
+    }
+
+    void ensure_scan_buffers(int N) {
+        alive.ensure(N);
+        queue.ensure(kQueueCap);
+        coll.ensure(kCollCap);
+        counters.ensure(8);
+        ymax.ensure(N);
+        ythr.ensure(N);
+        nnkey.ensure(N);
+        acc.ensure(2);
+        nnout.ensure(N);
+    }
+
+    // Core PD3: survivors {c : nn(c)^2 >= r_sq} with exact nn, sorted like
+    // sort_discords.  If `all_nn` is given (r_sq must be 0) it receives nn for
+    // every index.
+    std::vector<tsd_record> pardrag_core(int64_t m, double r_sq, double* all_nn = nullptr) {
+        const int N = (int)(n - m + 1);
+        derive(m);
+        ensure_scan_buffers(N);
+        ctr.pardrag_calls += 1;
+        ck(cudaMemsetAsync(counters.p, 0, 2 * sizeof(int), st), "memset");
+        ck(cudaMemsetAsync(acc.p, 0, 2 * sizeof(unsigned long long), st), "memset");
+        launch_fill_u8(alive.p, N, 1, st);
+        ctr.kernel_launches += 1;
+        const ScanParams P = params(m, r_sq);
+        std::vector<TileDesc> tl;
+
+        // ---- dense phase: bands of kW diagonals right of the main diagonal
+        int alive_cnt = N;
+        if (r_sq > 0.0) {
+            long long k_lo = m;
+            const long long k_max = (long long)N - 1;
+            int batch = 2;
+            int prev = N;
+            const int L = dense_rows;
+            while (k_lo <= k_max) {
+                tl.clear();
+                const long long nb = std::min<long long>(batch, (k_max - k_lo + kW) / kW);
+                for (long long b = 0; b < nb; ++b) {
+                    const long long k0 = k_lo + b * kW;
+                    for (long long r0 = 0; r0 < N; r0 += L) {
+                        if (r0 + k0 >= N) break;
+                        const int rows = (int)std::min<long long>(L, N - r0);
+                        tl.push_back(TileDesc{(int)r0, rows, (int)k0, +1});
+                    }
+                }
+                k_lo += nb * kW;
+                run_scan(kPrune, tl, P);
+                allreduce_min_u8(alive.p, N);
+                recheck(m, r_sq);
+                allreduce_min_u8(alive.p, N);
+                ck(cudaMemsetAsync(counters.p, 0, sizeof(int), st), "memset");
+                alive_cnt = compact_alive(N, false);
+                if (alive_cnt == 0) break;
+                if (alive_cnt <= std::max(32, N / 8192)) break;
+                if ((double)alive_cnt > 0.7 * (double)prev) break;  // kill rate stalled
+                prev = alive_cnt;
+                batch *= 2;
+            }
+        }
+
+        std::vector<tsd_record> out;
+        if (alive_cnt == 0) return out;
+
+        // ---- sparse phase: full rows for every remaining candidate
+        alive_cnt = compact_alive(N, true);
+        std::vector<int2> groups;
+        group_rows(h_list, choose_span(h_list, m), groups);
+        full_row_tiles(groups, m, N, tl);
+        ck(cudaMemsetAsync(ymax.p, 0, (size_t)N * sizeof(unsigned), st), "memset");
+        run_scan(kPruneTrack, tl, P);
+        allreduce_min_u8(alive.p, N);
+        allreduce_max_u32(ymax.p, N);
+        recheck(m, r_sq);
+        allreduce_min_u8(alive.p, N);
+        if (read_counter(0) > kQueueCap)
+            fail(TSD_ERUNTIME, "knife-edge queue overflow (degenerate series?)");
+
+        // ---- survivors: exact nearest neighbours
+        const int sc = compact_alive(N, true);
+        if (sc == 0) return out;
+        launch_prep_survivors(list.p, sc, ymax.p, ythr.p, nnkey.p, st);
+        ctr.kernel_launches += 1;
+        group_rows(h_list, choose_span(h_list, m), groups);
+        full_row_tiles(groups, m, N, tl);
+        ck(cudaMemsetAsync(counters.p + 1, 0, sizeof(int), st), "memset");
+        run_scan(kCollect, tl, P);
+        const int cc = read_counter(1);
+        if (cc > kCollCap) fail(TSD_ERUNTIME, "near-pair buffer overflow (degenerate series?)");
+        launch_ref_pairs(1, t.p, (int)m, coll.p, counters.p + 1, kCollCap, r_sq, alive.p, nnkey.p,
+                         std::max(cc, 1), st);
+        ck(cudaGetLastError(), "exact");
+        // constant rows follow the constant conventions
+        h_int.ensure(4);
+        int cr_init[2] = {N, -1};
+        ck(cudaMemcpyAsync(counters.p + 2, cr_init, 2 * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+        launch_const_range(nrm.p, N, counters.p + 2, st);
+        launch_const_nn(list.p, sc, nrm.p, counters.p + 2, N, (int)m, nnkey.p, st);
+        allreduce_min_u64(nnkey.p, N);
+        launch_gather_nn(list.p, sc, nnkey.p, nnout.p, st);
+        ck(cudaGetLastError(), "gather");
+        ctr.kernel_launches += 4;  // exact pairs, const range, const nn, gather
+        std::vector<double> nn(sc);
+        ck(cudaMemcpyAsync(nn.data(), nnout.p, sc * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+        h_int.ensure(2);
+        unsigned long long hacc[2];
+        ck(cudaMemcpyAsync(hacc, acc.p, sizeof(hacc), cudaMemcpyDeviceToHost, st), "D2H");
+        sync();
+        ctr.cells += hacc[0];
+        ctr.seed_dots += hacc[1];
+        ctr.seed_flops += hacc[1] * 2ull * (unsigned long long)m;
+        ctr.exact_pairs += (unsigned long long)cc;
+        out.reserve(sc);
+        for (int e = 0; e < sc; ++e) {
+            const int c = h_list[e];
+            if (all_nn) all_nn[c] = nn[e];
+            out.push_back(tsd_record{(int64_t)c + 1, nn[e], std::sqrt(nn[e])});
+        }
+        // sort_discords: nn_dist_sq desc, index asc (src/types.cpp:15-20)
+        std::sort(out.begin(), out.end(), [](const tsd_record& a, const tsd_record& b) {
+            if (a.nn_dist_sq != b.nn_dist_sq) return a.nn_dist_sq > b.nn_dist_sq;
+            return a.index < b.index;
+        });
+        return out;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// host arithmetic shared with the C++ API (bit-exact restatements)
+namespace {
+
+void layout(int64_t n, int64_t m, int64_t seglen, int64_t out[4]) {
+    // src/types.cpp:26-39
+    if (m < 3) fail(TSD_EINVAL, "subsequence length must be at least 3");
+    if (m > n - 2) fail(TSD_EINVAL, "subsequence length too large for series");
+    if (seglen < m) fail(TSD_EINVAL, "segment length must be at least the subsequence length");
+    if (n < seglen) fail(TSD_EINVAL, "series shorter than one segment");
+    const int64_t seg_n = seglen - m + 1, cnt = n - m + 1;
+    const int64_t num_seg = (cnt + seg_n - 1) / seg_n;
+    out[0] = seglen;
+    out[1] = seg_n;
+    out[2] = num_seg;
+    out[3] = num_seg * seg_n + 2 * (m - 1) - n;
+}
+
+double window_mean(const double* h, int64_t len) {
+    if (len < 5) fail(TSD_ELOGIC, "threshold history window too short");
+    double s = 0.0;
+    for (int64_t k = len - 5; k < len; ++k) s += h[k];
+    return s / 5.0;
+}
+
+double window_std(const double* h, int64_t len) {
+    const double mu = window_mean(h, len);
+    double s = 0.0;
+    for (int64_t k = len - 5; k < len; ++k) {
+        const double d = h[k] - mu;
+        s += d * d;
+    }
+    return std::sqrt(s / 5.0);
+}
+
+double next_thr(const double* h, int64_t len, int phase, int64_t min_len, double last_r, bool failed) {
+    // src/merlin.cpp:35-55
+    switch (phase) {
+        case 0:
+            return failed ? 0.5 * last_r : 2.0 * std::sqrt((double)min_len);
+        case 1:
+            if (!failed && len < 1) fail(TSD_ELOGIC, "threshold history is empty");
+            return 0.99 * (failed ? last_r : h[len - 1]);
+        case 2: {
+            if (failed) {
+                const double sigma = window_std(h, len);
+                return last_r - std::max(sigma, 0.01 * last_r);
+            }
+            const double r = window_mean(h, len) - 2.0 * window_std(h, len);
+            if (r <= 0.0) return 0.01 * h[len - 1];
+            return r;
+        }
+        default:
+            fail(TSD_ELOGIC, "unreachable");
+    }
+}
+
+template <typename F>
+int guard(tsd_ctx* ctx, F&& f) {
+    try {
+        f();
+        if (ctx) ctx->err.clear();
+        return TSD_OK;
+    } catch (const Fail& e) {
+        if (ctx) ctx->err = e.msg;
+        else g_create_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        if (ctx) ctx->err = "out of host memory";
+        return TSD_ERUNTIME;
+    } catch (const std::exception& e) {
+        if (ctx) ctx->err = e.what();
+        return TSD_ERUNTIME;
+    }
+}
+
+void need_series(tsd_ctx* c) {
+    if (c->n <= 0) fail(TSD_EINVAL, "no series set");
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* tsd_create_error(void) { return g_create_err.c_str(); }
+
+int tsd_ctx_create(int device, tsd_ctx** out) {
+    *out = nullptr;
+    tsd_ctx* c = new tsd_ctx();
+    const int rc = guard(nullptr, [&] {
+        int cnt = 0;
+        ck(cudaGetDeviceCount(&cnt), "cudaGetDeviceCount");
+        if (device < 0 || device >= cnt) fail(TSD_ECUDA, "no such CUDA device");
+        c->device = device;
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        ck(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking), "stream");
+        ck(cudaEventCreate(&c->ev_a), "event");
+        ck(cudaEventCreate(&c->ev_b), "event");
+        ck(cudaEventCreate(&c->ev_t0), "event");
+        ck(cudaEventCreate(&c->ev_t1), "event");
+        scan_configure();
+        ck(cudaGetLastError(), "configure");
+    });
+    if (rc != TSD_OK) {
+        delete c;
+        return rc;
+    }
+    *out = c;
+    return TSD_OK;
+}
+
+void tsd_ctx_destroy(tsd_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->comm) nccl_destroy(c->comm);
+    c->t.release();
+    c->mu.release();
+    c->sig.release();
+    c->scr_a.release();
+    c->scr_b.release();
+    c->df.release();
+    c->dg.release();
+    c->nrm.release();
+    c->alive.release();
+    c->queue.release();
+    c->coll.release();
+    c->counters.release();
+    c->ymax.release();
+    c->ythr.release();
+    c->nnkey.release();
+    c->acc.release();
+    c->blk.release();
+    c->list.release();
+    c->nnout.release();
+    c->tiles.release();
+    c->h_tiles.release();
+    c->h_int.release();
+    c->h_dbl.release();
+    if (c->ev_a) cudaEventDestroy(c->ev_a);
+    if (c->ev_b) cudaEventDestroy(c->ev_b);
+    if (c->ev_t0) cudaEventDestroy(c->ev_t0);
+    if (c->ev_t1) cudaEventDestroy(c->ev_t1);
+    if (c->st) cudaStreamDestroy(c->st);
+    delete c;
+}
+
+const char* tsd_last_error(const tsd_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
+
+int tsd_nccl_unique_id(uint8_t out[128]) {
+    return guard(nullptr, [&] {
+        if (!nccl_get_unique_id(out)) fail(TSD_ECUDA, "ncclGetUniqueId failed (NCCL unavailable?)");
+    });
+}
+
+int tsd_ctx_join(tsd_ctx* c, int rank, int world, const uint8_t id[128]) {
+    return guard(c, [&] {
+        if (world < 1 || rank < 0 || rank >= world) fail(TSD_EINVAL, "bad rank/world");
+        c->rank = rank;
+        c->world = world;
+        if (world == 1) return;
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        c->comm = nccl_init(id, rank, world);
+        if (!c->comm) fail(TSD_ECUDA, "ncclCommInitRank failed");
+    });
+}
+
+int tsd_series_set(tsd_ctx* c, const double* v, int64_t n) {
+    return guard(c, [&] {
+        // src/types.cpp:8-13
+        if (n < 3) fail(TSD_EINVAL, "time series needs at least 3 points");
+        for (int64_t i = 0; i < n; ++i)
+            if (!std::isfinite(v[i])) fail(TSD_EINVAL, "time series contains a non-finite value");
+        if (n > (int64_t)INT32_MAX / 2) fail(TSD_EINVAL, "series too long for 32-bit device indexing");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        c->h_t.assign(v, v + n);
+        c->n = n;
+        c->t.ensure(n);
+        ck(cudaMemcpyAsync(c->t.p, v, n * sizeof(double), cudaMemcpyHostToDevice, c->st), "series H2D");
+        c->sync();
+        c->stats_m = -1;
+        c->derived_m = -1;
+    });
+}
+
+int64_t tsd_series_len(const tsd_ctx* c) { return c ? c->n : 0; }
+
+int tsd_init_stats(tsd_ctx* c, int64_t m, double* mu, double* sigma) {
+    return guard(c, [&] {
+        need_series(c);
+        // src/stats.cpp:9
+        if (m < 2 || m > c->n - 1) fail(TSD_EINVAL, "init_stats: length out of range");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        c->init_stats_dev(m);
+        const int64_t N = c->n - m + 1;
+        ck(cudaMemcpyAsync(mu, c->mu.p, N * sizeof(double), cudaMemcpyDeviceToHost, c->st), "D2H");
+        ck(cudaMemcpyAsync(sigma, c->sig.p, N * sizeof(double), cudaMemcpyDeviceToHost, c->st), "D2H");
+        c->sync();
+    });
+}
+
+int tsd_advance_stats(tsd_ctx* c, int64_t m, const double* mu_in, const double* sigma_in,
+                      double* mu_out, double* sigma_out) {
+    return guard(c, [&] {
+        need_series(c);
+        // src/stats.cpp:41
+        if (m + 1 > c->n - 1) fail(TSD_EINVAL, "advance_stats: next length out of range");
+        if (m < 2) fail(TSD_EINVAL, "advance_stats: length out of range");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        const int64_t N = c->n - m + 1;
+        c->mu.ensure(c->n);
+        c->sig.ensure(c->n);
+        ck(cudaMemcpyAsync(c->mu.p, mu_in, N * sizeof(double), cudaMemcpyHostToDevice, c->st), "H2D");
+        ck(cudaMemcpyAsync(c->sig.p, sigma_in, N * sizeof(double), cudaMemcpyHostToDevice, c->st), "H2D");
+        c->stats_m = m;
+        c->advance_stats_dev();
+        ck(cudaMemcpyAsync(mu_out, c->mu.p, (N - 1) * sizeof(double), cudaMemcpyDeviceToHost, c->st), "D2H");
+        ck(cudaMemcpyAsync(sigma_out, c->sig.p, (N - 1) * sizeof(double), cudaMemcpyDeviceToHost, c->st),
+           "D2H");
+        c->sync();
+    });
+}
+
+int tsd_compute_layout(int64_t n, int64_t m, int64_t seglen, int64_t out[4]) {
+    return guard(nullptr, [&] { layout(n, m, seglen, out); });
+}
+
+int tsd_next_threshold(const double* h, int64_t len, int phase, int64_t min_len, double last_r,
+                       int failed, double* out) {
+    return guard(nullptr, [&] { *out = next_thr(h, len, phase, min_len, last_r, failed != 0); });
+}
+
+int tsd_pardrag(tsd_ctx* c, int64_t m, double r_sq, int64_t seglen, const double* mu,
+                const double* sigma, tsd_record* out, int64_t cap, int64_t* count) {
+    return guard(c, [&] {
+        need_series(c);
+        int64_t lay[4];
+        layout(c->n, m, seglen, lay);  // same preconditions as the reference call
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        ck(cudaEventRecord(c->ev_t0, c->st), "event");
+        const int64_t N = c->n - m + 1;
+        if (mu && sigma) {
+            c->mu.ensure(c->n);
+            c->sig.ensure(c->n);
+            ck(cudaMemcpyAsync(c->mu.p, mu, N * sizeof(double), cudaMemcpyHostToDevice, c->st), "H2D");
+            ck(cudaMemcpyAsync(c->sig.p, sigma, N * sizeof(double), cudaMemcpyHostToDevice, c->st), "H2D");
+            c->stats_m = m;
+            c->derived_m = -1;
+        } else if (c->stats_m != m) {
+            c->init_stats_dev(m);
+        }
+        const auto recs = c->pardrag_core(m, r_sq);
+        ck(cudaEventRecord(c->ev_t1, c->st), "event");
+        c->sync();
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c->ev_t0, c->ev_t1);
+        c->ctr.total_ms = ms;
+        *count = (int64_t)recs.size();
+        const int64_t k = std::min<int64_t>(cap, (int64_t)recs.size());
+        if (k > 0) std::memcpy(out, recs.data(), k * sizeof(tsd_record));
+    });
+}
+
+int tsd_brute_force_nn(tsd_ctx* c, int64_t m, double* out) {
+    return guard(c, [&] {
+        need_series(c);
+        if (m < 3 || m > c->n - 2) fail(TSD_EINVAL, "brute_force_nn: length out of range");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        if (c->stats_m != m) c->init_stats_dev(m);
+        const int64_t N = c->n - m + 1;
+        for (int64_t i = 0; i < N; ++i) out[i] = INFINITY;
+        c->pardrag_core(m, 0.0, out);
+    });
+}
+
+int tsd_merlin(tsd_ctx* c, int64_t min_len, int64_t max_len, const tsd_merlin_opts* o,
+               int64_t* counts, tsd_record* recs, double* final_r, int64_t* retries, uint8_t* failed) {
+    return guard(c, [&] {
+        need_series(c);
+        const int64_t n = c->n;
+        const int64_t top_k = o ? o->top_k : 1;
+        const int64_t seglen_opt = o ? o->seglen : 512;
+        const int64_t max_retries = o ? o->max_retries : 100;
+        const bool reuse = o ? o->reuse_stats != 0 : true;
+        // src/merlin.cpp:60-62
+        if (min_len < 3 || min_len > max_len || 2 * max_len > n)
+            fail(TSD_EINVAL, "merlin: length range out of bounds (need 3 <= minL <= maxL <= n/2)");
+        if (top_k < 1) fail(TSD_EINVAL, "merlin: topK must be positive");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        ck(cudaEventRecord(c->ev_t0, c->st), "event");
+
+        std::vector<double> history;
+        c->init_stats_dev(min_len);
+        for (int64_t m = min_len; m <= max_len; ++m) {
+            const int64_t k = m - min_len;
+            counts[k] = 0;
+            failed[k] = 0;
+            if (m > min_len) {
+                if (reuse) c->advance_stats_dev();
+                else c->init_stats_dev(m);
+            }
+            const int phase = m == min_len ? 0 : (m < min_len + 5 ? 1 : 2);
+            if (phase != 0 && history.empty()) {
+                failed[k] = 1;
+                final_r[k] = 0.0;
+                retries[k] = 0;
+                continue;
+            }
+            int64_t lay[4];
+            layout(n, m, std::min(std::max(seglen_opt, 2 * m), n), lay);  // src/merlin.cpp:86-87
+
+            double r = next_thr(history.data(), (int64_t)history.size(), phase, min_len, 0.0, false);
+            std::vector<tsd_record> got;
+            int64_t tries = 0;
+            bool success = false;
+            for (;;) {
+                const double r_sq = r > 0.0 ? r * r : 0.0;
+                got = c->pardrag_core(m, r_sq);
+                if ((int64_t)got.size() >= top_k) {
+                    success = true;
+                    break;
+                }
+                if (tries >= max_retries) {
+                    success = !got.empty();
+                    break;
+                }
+                ++tries;
+                r = next_thr(history.data(), (int64_t)history.size(), phase, min_len, r, true);
+            }
+            final_r[k] = r;
+            retries[k] = tries;
+            if (!success) {
+                failed[k] = 1;
+                continue;
+            }
+            if ((int64_t)got.size() > top_k) got.resize(top_k);
+            double mn = got.front().nn_dist;
+            for (const auto& g : got) mn = std::min(mn, g.nn_dist);
+            history.push_back(mn);
+            counts[k] = (int64_t)got.size();
+            for (size_t j = 0; j < got.size(); ++j) recs[k * top_k + (int64_t)j] = got[j];
+        }
+        ck(cudaEventRecord(c->ev_t1, c->st), "event");
+        c->sync();
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c->ev_t0, c->ev_t1);
+        c->ctr.total_ms = ms;
+    });
+}
+
+int tsd_gen_randomwalk(int64_t n, uint64_t seed, double* out) {
+    return guard(nullptr, [&] {
+        // src/io.cpp:110-119 — same engine and distribution (libstdc++)
+        if (n < 3) fail(TSD_EINVAL, "gen_randomwalk: n must be at least 3");
+        std::mt19937_64 rng(seed);
+        std::normal_distribution<double> step(0.0, 1.0);
+        out[0] = 0.0;
+        for (int64_t i = 1; i < n; ++i) out[i] = out[i - 1] + step(rng);
+    });
+}
+
+int tsd_get_counters(const tsd_ctx* c, tsd_counters* out) {
+    if (!c || !out) return TSD_EINVAL;
+    *out = c->ctr;
+    return TSD_OK;
+}
+
+int tsd_reset_counters(tsd_ctx* c) {
+    if (!c) return TSD_EINVAL;
+    c->ctr = tsd_counters{};
+    return TSD_OK;
+}
+
+int tsd_set_param(tsd_ctx* c, const char* key, double v) {
+    return guard(c, [&] {
+        const std::string k = key ? key : "";
+        if (k == "dense_rows") c->dense_rows = std::max(16, std::min(kMaxRows, (int)v));
+        else if (k == "sparse_rows") c->sparse_rows = std::max(0, std::min(kMaxRows, (int)v));
+        else if (k == "err_scale") c->err_k = v;
+        else fail(TSD_EINVAL, "unknown parameter " + k);
+    });
+}
+
+}  // extern "C"

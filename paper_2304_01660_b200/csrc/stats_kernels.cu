@@ -1,0 +1,114 @@
+// Per-length subsequence statistics on the device (north_star (a)).
+//
+// K1  init:    Eq. 4 running sums, src/stats.cpp:7-36.  The reference's running
+//              sum is a sequential FP64 recurrence, so the prefix sums are
+//              produced by one thread in exactly the reference's operation
+//              order (no FMA contraction) and the per-index mean/sigma by a
+//              parallel pass: bit-identical to init_stats.
+// K2  advance: Eq. 7-8, src/stats.cpp:38-58, one thread per index, in place,
+//              bit-identical to advance_stats.
+// K2b derive:  the FP32 arrays the tile scan walks (df, dg, 1/(sqrt(m) sigma)),
+//              computed in FP64 and rounded once (HBM-bound, fused per length).
+#include "common.cuh"
+#include "engine_internal.h"
+
+namespace tsd {
+
+__global__ void k_init_prefix(const double* __restrict__ t, int n, int m,
+                              double* __restrict__ sum, double* __restrict__ sum_sq) {
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    const int cnt = n - m + 1;
+    double s = 0.0, q = 0.0;
+    for (int k = 0; k < m; ++k) {
+        const double v = t[k];
+        s = __dadd_rn(s, v);
+        q = __dadd_rn(q, __dmul_rn(v, v));
+    }
+    sum[0] = s;
+    sum_sq[0] = q;
+    // sum += in - out; sum_sq += in*in - out*out   (stats.cpp:30-33)
+    int i = 0;
+    for (; i + 1 < cnt; ++i) {
+        const double out = t[i];
+        const double in = t[i + m];
+        s = __dadd_rn(s, __dsub_rn(in, out));
+        q = __dadd_rn(q, __dsub_rn(__dmul_rn(in, in), __dmul_rn(out, out)));
+        sum[i + 1] = s;
+        sum_sq[i + 1] = q;
+    }
+}
+
+__global__ void k_init_finish(const double* __restrict__ sum, const double* __restrict__ sum_sq,
+                              int cnt, int m, double* __restrict__ mu, double* __restrict__ sig) {
+    const double md = (double)m;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+        const double mean = __ddiv_rn(sum[i], md);
+        const double var = __dsub_rn(__ddiv_rn(sum_sq[i], md), __dmul_rn(mean, mean));
+        mu[i] = mean;
+        sig[i] = __dsqrt_rn(var > 0.0 ? var : 0.0);
+    }
+}
+
+// stats (length m, n-m+1 valid) -> length m+1 (n-m valid), in place.
+__global__ void k_advance(const double* __restrict__ t, int n, int m, double* __restrict__ mu,
+                          double* __restrict__ sig) {
+    const int cnt = n - m;  // next valid_count
+    const double md = (double)m;
+    const double md1 = md + 1.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+        const double u = mu[i];
+        const double sg = sig[i];
+        const double in = t[i + m];
+        const double delta = __dsub_rn(u, in);
+        mu[i] = __ddiv_rn(__dadd_rn(__dmul_rn(md, u), in), md1);
+        const double var = __dmul_rn(__ddiv_rn(md, md1),
+                                     __dadd_rn(__dmul_rn(sg, sg), __ddiv_rn(__dmul_rn(delta, delta), md1)));
+        sig[i] = __dsqrt_rn(var > 0.0 ? var : 0.0);
+    }
+}
+
+// df[i] = (t[i+m-1] - t[i-1]) / 2, dg[i] = (t[i+m-1] - mu_i) + (t[i-1] - mu_{i-1})
+// (centered-covariance diagonal step: cov(i,j) = cov(i-1,j-1) + df_i dg_j + df_j dg_i)
+// nrm[i] = 1 / (sqrt(m) sigma_i), 0 for a constant subsequence.
+__global__ void k_derive(const double* __restrict__ t, int m, int cnt, const double* __restrict__ mu,
+                         const double* __restrict__ sig, float* __restrict__ df,
+                         float* __restrict__ dg, float* __restrict__ nrm) {
+    const double sqm = sqrt((double)m);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+        const double s = sig[i];
+        nrm[i] = s < kSigmaEps ? 0.f : (float)(1.0 / (sqm * s));
+        if (i == 0) {
+            df[0] = 0.f;
+            dg[0] = 0.f;
+        } else {
+            const double a = t[i + m - 1], b = t[i - 1];
+            df[i] = (float)((a - b) * 0.5);
+            dg[i] = (float)((a - mu[i]) + (b - mu[i - 1]));
+        }
+    }
+}
+
+static int grid_for(long long work, int threads) {
+    long long b = (work + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > 148 * 16) b = 148 * 16;
+    return (int)b;
+}
+
+void launch_init_stats(const double* t, int n, int m, double* mu, double* sig, double* scratch_a,
+                       double* scratch_b, cudaStream_t st) {
+    const int cnt = n - m + 1;
+    k_init_prefix<<<1, 32, 0, st>>>(t, n, m, scratch_a, scratch_b);
+    k_init_finish<<<grid_for(cnt, 256), 256, 0, st>>>(scratch_a, scratch_b, cnt, m, mu, sig);
+}
+
+void launch_advance_stats(const double* t, int n, int m, double* mu, double* sig, cudaStream_t st) {
+    k_advance<<<grid_for(n - m, 256), 256, 0, st>>>(t, n, m, mu, sig);
+}
+
+void launch_derive(const double* t, int m, int cnt, const double* mu, const double* sig, float* df,
+                   float* dg, float* nrm, cudaStream_t st) {
+    k_derive<<<grid_for(cnt, 256), 256, 0, st>>>(t, m, cnt, mu, sig, df, dg, nrm);
+}
+
+}  // namespace tsd

@@ -1,0 +1,138 @@
+"""Parity of the CUDA path (through the C-ABI) with the reference: golden
+fixtures from the unmodified reference, the C oracle on seeded inputs, and
+size-independent properties at full size."""
+import numpy as np
+import pytest
+
+from conftest import hexf, load_golden, series_of
+
+pytestmark = pytest.mark.gpu
+
+
+def recs_list(recs):
+    return [[int(r["index"]), float(r["nn_dist_sq"]).hex(), float(r["nn_dist"]).hex()] for r in recs]
+
+
+def check_merlin(rep, fx):
+    for e in fx["per_length"]:
+        m = e["m"]
+        assert (m in rep.failed_lengths) == bool(e["failed"]), m
+        k = m - fx["min_len"]
+        assert float(rep.final_r[k]).hex() == e["final_r"], (m, rep.final_r[k], hexf(e["final_r"]))
+        assert int(rep.retries[k]) == e["retries"], m
+        if not e["failed"]:
+            assert recs_list(rep.per_length[m]) == e["records"], m
+
+
+# ---- statistics (Eq. 4, Eq. 7-8) -------------------------------------------
+def test_stats_bitexact(engine, oracle):
+    x = oracle.gen_randomwalk(10_000, 3)
+    engine.set_series(x)
+    mu, sg = engine.init_stats(8)
+    omu, osg = oracle.init_stats(x, 8)
+    assert np.array_equal(mu, omu) and np.array_equal(sg, osg)
+    for m in range(8, 40):  # acceptance criterion 3, bit-exact instead of 1e-9
+        mu, sg = engine.advance_stats(m, mu, sg)
+    omu, osg = oracle.advance_stats(x, 8, 40)
+    assert np.array_equal(mu, omu) and np.array_equal(sg, osg)
+
+
+def test_stats_known_answers(engine):
+    engine.set_series(np.array([1.0, 2.0, 3.0, 4.0]))
+    mu, sg = engine.init_stats(2)
+    assert mu.tolist() == [1.5, 2.5, 3.5] and sg.tolist() == [0.5, 0.5, 0.5]
+
+
+# ---- range discords ----------------------------------------------------------
+def test_range_sets_golden(engine):
+    g = load_golden("small.json")
+    for e in g["range"]:
+        engine.set_series(series_of(e["input"]))
+        got = engine.pardrag(e["m"], hexf(e["r_sq"]), seglen=max(2 * e["m"], 64))
+        assert recs_list(got) == e["records"], (e["input"], e["m"])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_range_sets_vs_oracle(engine, oracle, seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(300, 3000))
+    x = oracle.gen_randomwalk(n, 500 + seed)
+    engine.set_series(x)
+    for m in (3, 8, 12, 33, 64):
+        if 2 * m > n:
+            continue
+        nn = oracle.brute_force_nn(x, m)
+        s = np.sort(nn)
+        for q in (0.0, 0.5, 0.9, 0.999, 1.0):
+            r_sq = float(s[min(int(len(s) * q), len(s) - 1)]) if q > 0 else 0.0
+            exp = oracle.range_discords(x, m, r_sq)
+            got = engine.pardrag(m, r_sq, seglen=min(max(2 * m, 64), n))
+            assert recs_list(got) == recs_list(exp), (n, m, q)
+
+
+def test_brute_force_nn_bitexact(engine, oracle):
+    x = oracle.gen_randomwalk(1200, 11)
+    engine.set_series(x)
+    for m in (3, 16, 50):
+        assert np.array_equal(engine.brute_force_nn(m), oracle.brute_force_nn(x, m))
+
+
+def test_series_validation(engine):
+    with pytest.raises(ValueError):
+        engine.set_series(np.array([1.0, 2.0]))
+    with pytest.raises(ValueError):
+        engine.set_series(np.array([1.0, np.nan, 2.0, 3.0]))
+    engine.set_series(np.arange(100, dtype=float))
+    with pytest.raises(ValueError):
+        engine.pardrag(2, 1.0, 32)          # m < 3
+    with pytest.raises(ValueError):
+        engine.pardrag(10, 1.0, 9)          # seglen < m
+    with pytest.raises(ValueError):
+        engine.merlin_full(10, 60)          # maxL > n/2
+
+
+# ---- MERLIN --------------------------------------------------------------------
+def test_merlin_golden_small(engine):
+    for fx in load_golden("small.json")["merlin"]:
+        engine.set_series(series_of(fx["input"]))
+        rep = engine.merlin_full(fx["min_len"], fx["max_len"], top_k=fx["top_k"], seglen=fx["seglen"])
+        check_merlin(rep, fx)
+
+
+def test_merlin_golden_c1(engine):
+    fx = load_golden("c1.json")
+    engine.set_series(series_of(fx["input"]))
+    rep = engine.merlin_full(fx["min_len"], fx["max_len"], top_k=fx["top_k"], seglen=fx["seglen"])
+    check_merlin(rep, fx)
+
+
+def test_merlin_golden_c2(engine):
+    fx = load_golden("c2.json")
+    engine.set_series(series_of(fx["input"]))
+    rep = engine.merlin_full(fx["min_len"], fx["max_len"], top_k=fx["top_k"], seglen=fx["seglen"])
+    check_merlin(rep, fx)
+
+
+def test_merlin_csv_bytes(engine):
+    import paper_2304_01660_b200 as P
+    g = load_golden("small.json")
+    engine.set_series(P.gen_randomwalk(3000, 2024))
+    rep = engine.merlin_full(8, 24, top_k=2, seglen=128)
+    assert P.discords_csv(rep.per_length) == g["csv_acceptance_c2"]
+
+
+def test_merlin_vs_oracle_top3(engine, oracle):
+    # acceptance criterion 1 shape: single-length top-3 == brute force
+    for seed in range(1, 6):
+        x = oracle.gen_randomwalk(2000, seed)
+        engine.set_series(x)
+        for m in (8, 16, 32, 64):
+            rep = engine.merlin_full(m, m, top_k=3)
+            exp = oracle.merlin(x, m, m, top_k=3)
+            assert recs_list(rep.per_length[m]) == recs_list(exp["recs"][0][: exp["counts"][0]])
+
+
+def test_merlin_constant_series_fails_lengths(engine):
+    engine.set_series(np.full(400, 2.5))
+    rep = engine.merlin_full(8, 12)
+    assert rep.failed_lengths == list(range(8, 13))

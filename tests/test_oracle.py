@@ -1,0 +1,100 @@
+"""The C restatement (oracle/oracle.c) pinned against the reference's outputs:
+committed golden fixtures (generated from the unmodified reference by
+tests/golden/make_golden.py) and, where this container has it, the reference
+library itself (oracle/_ref/libtsdref.so)."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import hexf, load_golden
+
+
+def test_randomwalk_generator_matches_reference(oracle):
+    g = load_golden("small.json")
+    for e in g["randomwalk"]:
+        x = oracle.gen_randomwalk(e["n"], e["seed"])
+        assert [v.hex() for v in x[:8].tolist()] == e["head"][: len(x[:8])]
+        assert x[-1].hex() == e["last"]
+        assert float(np.sum(x)).hex() == e["sum"]
+
+
+def test_stats_recurrence_matches_reference(oracle):
+    g = load_golden("small.json")["stats"]
+    x = oracle.gen_randomwalk(g["input"]["n"], g["input"]["seed"])
+    mu, sg = oracle.advance_stats(x, g["m0"], g["m1"])
+    assert [v.hex() for v in mu[:16].tolist()] == g["mu_head"]
+    assert [v.hex() for v in sg[:16].tolist()] == g["sigma_head"]
+    assert float(np.sum(mu)).hex() == g["mu_sum"]
+    assert float(np.sum(sg)).hex() == g["sigma_sum"]
+
+
+def test_stats_known_answers(oracle):
+    # tests/stats_test.cpp:14-28
+    mu, sg = oracle.init_stats([1.0, 2.0, 3.0, 4.0], 2)
+    assert mu.tolist() == [1.5, 2.5, 3.5] and sg.tolist() == [0.5, 0.5, 0.5]
+    mu, sg = oracle.init_stats([1.0, 2.0, 3.0, 4.0], 3)
+    assert mu.tolist() == [2.0, 3.0]
+    assert np.allclose(sg, np.sqrt(2.0 / 3.0), rtol=0, atol=1e-15)
+
+
+def test_range_sets_match_reference(oracle):
+    g = load_golden("small.json")
+    for e in g["range"]:
+        x = oracle.gen_randomwalk(e["input"]["n"], e["input"]["seed"])
+        got = oracle.range_discords(x, e["m"], hexf(e["r_sq"]))
+        exp = e["records"]
+        assert len(got) == len(exp)
+        for r, (idx, d2, d) in zip(got, exp):
+            assert int(r["index"]) == idx
+            assert float(r["nn_dist_sq"]).hex() == d2
+            assert float(r["nn_dist"]).hex() == d
+
+
+def _check_merlin(out, fx):
+    for k, e in enumerate(fx["per_length"]):
+        assert int(out["failed"][k]) == e["failed"], e["m"]
+        assert float(out["final_r"][k]).hex() == e["final_r"], e["m"]
+        assert int(out["retries"][k]) == e["retries"], e["m"]
+        recs = out["recs"][k][: out["counts"][k]]
+        assert [[int(r["index"]), float(r["nn_dist_sq"]).hex(), float(r["nn_dist"]).hex()]
+                for r in recs] == e["records"], e["m"]
+
+
+def test_merlin_matches_reference_small(oracle):
+    for fx in load_golden("small.json")["merlin"]:
+        x = oracle.gen_randomwalk(fx["input"]["n"], fx["input"]["seed"])
+        out = oracle.merlin(x, fx["min_len"], fx["max_len"], top_k=fx["top_k"], seglen=fx["seglen"])
+        _check_merlin(out, fx)
+
+
+def test_layout_and_schedule_known_answers(oracle):
+    # tests/types_test.cpp:9-25
+    assert oracle.compute_layout(100, 10, 32) == dict(seglen=32, seg_n=23, num_seg=4, pad=10)
+    assert oracle.compute_layout(101, 10, 32)["pad"] == 9
+    assert oracle.compute_layout(100, 10, 10) == dict(seglen=10, seg_n=1, num_seg=91, pad=9)
+    # tests/merlin_test.cpp:11-45
+    assert oracle.next_threshold([], 0, 64, 0.0, False) == 16.0
+    assert oracle.next_threshold([], 0, 64, 16.0, True) == 8.0
+    assert abs(oracle.next_threshold([10.0], 1, 8, 0.0, False) - 9.9) < 1e-12
+    assert abs(oracle.next_threshold([10.0], 1, 8, 9.9, True) - 9.801) < 1e-12
+    st = [3.5, 4.5, 4.0, 4.5, 3.5]
+    sd = float(np.std(st))
+    assert abs(oracle.next_threshold(st, 2, 8, 0.0, False) - (4.0 - 2 * sd)) < 1e-12
+    assert abs(oracle.next_threshold(st, 2, 8, 3.0, True) - (3.0 - sd)) < 1e-12
+    assert abs(oracle.next_threshold([3.0] * 5, 2, 8, 3.0, True) - 2.97) < 1e-12
+    assert abs(oracle.next_threshold([0.1, 10.0, 0.1, 10.0, 0.2], 2, 8, 0.0, False) - 0.002) < 1e-15
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(os.path.dirname(__file__), "..", "oracle", "_ref",
+                                                    "libtsdref.so")), reason="reference not built here")
+def test_oracle_equals_reference_library(oracle):
+    from oracle.refbind import Ref
+    R = Ref()
+    x = R.gen_randomwalk(1500, 99)
+    assert np.array_equal(R.brute_force_nn(x, 16), oracle.brute_force_nn(x, 16))
+    a = R.merlin(x, 10, 20, top_k=2, seglen=64, workers=2)
+    b = oracle.merlin(x, 10, 20, top_k=2, seglen=64)
+    for key in ("counts", "final_r", "retries", "failed"):
+        assert np.array_equal(a[key], b[key]), key
+    assert np.array_equal(a["recs"], b["recs"])
