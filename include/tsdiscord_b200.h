@@ -57,7 +57,8 @@ typedef struct {
 
 /* Per-run counters (device-side work accounting, for the roofline). */
 typedef struct {
-    uint64_t cells;         /* (candidate, subsequence) correlations updated by the FP32 scan */
+    uint64_t cells;         /* (candidate, subsequence) cells walked by the FP32 recurrence (2 FFMA) */
+    uint64_t cells_eval;    /* of which evaluated against the threshold (+1 FMUL, +1 FMNMX) */
     uint64_t seed_dots;     /* directly seeded dot products (m FMAs each, FP64) */
     uint64_t seed_flops;    /* sum over seeds of 2*m */
     uint64_t rechecks;      /* knife-edge pairs resolved with the exact FP64 distance */
@@ -65,7 +66,11 @@ typedef struct {
     uint64_t pardrag_calls; /* DRAG tries */
     uint64_t scan_launches; /* launches of the tile scan kernel */
     uint64_t kernel_launches; /* all kernel launches issued by the library */
+    uint64_t host_syncs;    /* stream synchronisations (host round trips) */
     double scan_ms;         /* device time inside the scan kernel (CUDA events) */
+    double dense_ms;        /* ... of which dense band phase */
+    double sparse_ms;       /* ... of which sparse full-row phase */
+    double collect_ms;      /* ... of which survivor near-pair collection */
     double total_ms;        /* device time of the last merlin/pardrag call (CUDA events) */
 } tsd_counters;
 

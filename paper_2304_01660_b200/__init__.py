@@ -44,11 +44,12 @@ class _Opts(C.Structure):
 
 
 class Counters(C.Structure):
-    _fields_ = [("cells", C.c_uint64), ("seed_dots", C.c_uint64), ("seed_flops", C.c_uint64),
-                ("rechecks", C.c_uint64), ("exact_pairs", C.c_uint64),
+    _fields_ = [("cells", C.c_uint64), ("cells_eval", C.c_uint64), ("seed_dots", C.c_uint64),
+                ("seed_flops", C.c_uint64), ("rechecks", C.c_uint64), ("exact_pairs", C.c_uint64),
                 ("pardrag_calls", C.c_uint64), ("scan_launches", C.c_uint64),
-                ("kernel_launches", C.c_uint64),
-                ("scan_ms", C.c_double), ("total_ms", C.c_double)]
+                ("kernel_launches", C.c_uint64), ("host_syncs", C.c_uint64),
+                ("scan_ms", C.c_double), ("dense_ms", C.c_double), ("sparse_ms", C.c_double),
+                ("collect_ms", C.c_double), ("total_ms", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -55,8 +55,7 @@ struct ScanParams {
     int* coll_count;
     int coll_cap;
     const TileDesc* tiles;
-    unsigned long long* cells;  // accounting
-    unsigned long long* seeds;
+    unsigned long long* acc;  // accounting: [0] cells walked, [1] cells evaluated, [2] seed dots
 };
 
 // Order-preserving float <-> uint32 map (for atomicMax on floats of any sign).

@@ -119,6 +119,7 @@ struct tsd_ctx {
     HBuf<int> h_int;
     HBuf<double> h_dbl;
     std::vector<int> h_list;
+    int last_queue = 0;
 
     // tuning
     int dense_rows = 512;
@@ -134,7 +135,10 @@ struct tsd_ctx {
     void* comm = nullptr;
 
     // ------------------------------------------------------------------
-    void sync() { ck(cudaStreamSynchronize(st), "stream sync"); }
+    void sync() {
+        ck(cudaStreamSynchronize(st), "stream sync");
+        ctr.host_syncs += 1;
+    }
 
     void allreduce_min_u8(uint8_t* p, size_t cnt) {
         if (world > 1) nccl_allreduce(comm, p, cnt, 0 /*u8 min*/, st);
@@ -205,8 +209,7 @@ struct tsd_ctx {
         p.coll_count = counters.p + 1;
         p.coll_cap = kCollCap;
         p.tiles = tiles.p;
-        p.cells = acc.p + 0;
-        p.seeds = acc.p + 1;
+        p.acc = acc.p;
         return p;
     }
 
@@ -236,6 +239,9 @@ struct tsd_ctx {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, ev_a, ev_b);
         ctr.scan_ms += ms;
+        if (mode == kPrune) ctr.dense_ms += ms;
+        else if (mode == kPruneTrack) ctr.sparse_ms += ms;
+        else ctr.collect_ms += ms;
         ctr.scan_launches += 1;
         ctr.kernel_launches += 1;
     }
@@ -257,8 +263,10 @@ struct tsd_ctx {
         ck(cudaGetLastError(), "compact");
         h_int.ensure(4);
         ck(cudaMemcpyAsync(h_int.p, blk.p + nb, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaMemcpyAsync(h_int.p + 1, counters.p, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
         sync();
         const int cnt = h_int.p[0];
+        last_queue = h_int.p[1];
         if (want_list) {
             h_list.resize(cnt);
             if (cnt > 0) {
@@ -337,8 +345,18 @@ struct tsd_ctx {
         ymax.ensure(N);
         ythr.ensure(N);
         nnkey.ensure(N);
-        acc.ensure(2);
+        acc.ensure(3);
         nnout.ensure(N);
+    }
+
+    // fold the device work counters of the current call into ctr
+    void harvest(int64_t m) {
+        unsigned long long hacc[3];
+        ck(cudaMemcpy(hacc, acc.p, sizeof(hacc), cudaMemcpyDeviceToHost), "acc D2H");
+        ctr.cells += hacc[0];
+        ctr.cells_eval += hacc[1];
+        ctr.seed_dots += hacc[2];
+        ctr.seed_flops += hacc[2] * 2ull * (unsigned long long)m;
     }
 
     // Core PD3: survivors {c : nn(c)^2 >= r_sq} with exact nn, sorted like
@@ -350,7 +368,7 @@ struct tsd_ctx {
         ensure_scan_buffers(N);
         ctr.pardrag_calls += 1;
         ck(cudaMemsetAsync(counters.p, 0, 2 * sizeof(int), st), "memset");
-        ck(cudaMemsetAsync(acc.p, 0, 2 * sizeof(unsigned long long), st), "memset");
+        ck(cudaMemsetAsync(acc.p, 0, 3 * sizeof(unsigned long long), st), "memset");
         launch_fill_u8(alive.p, N, 1, st);
         ctr.kernel_launches += 1;
         const ScanParams P = params(m, r_sq);
@@ -367,12 +385,16 @@ struct tsd_ctx {
             while (k_lo <= k_max) {
                 tl.clear();
                 const long long nb = std::min<long long>(batch, (k_max - k_lo + kW) / kW);
+                // band b: diagonals k in [k_lo + b*kW, +kW) right of every row and the
+                // mirror band left of it; each row is decided by its own cells only
                 for (long long b = 0; b < nb; ++b) {
                     const long long k0 = k_lo + b * kW;
                     for (long long r0 = 0; r0 < N; r0 += L) {
-                        if (r0 + k0 >= N) break;
                         const int rows = (int)std::min<long long>(L, N - r0);
-                        tl.push_back(TileDesc{(int)r0, rows, (int)k0, +1});
+                        if (r0 + k0 < N) tl.push_back(TileDesc{(int)r0, rows, (int)k0, +1});
+                        const long long khi = -k0;  // tile covers [khi - kW + 1, khi]
+                        if (r0 + rows - 1 + khi >= 0)
+                            tl.push_back(TileDesc{(int)r0, rows, (int)(khi - kW + 1), -1});
                     }
                 }
                 k_lo += nb * kW;
@@ -380,8 +402,10 @@ struct tsd_ctx {
                 allreduce_min_u8(alive.p, N);
                 recheck(m, r_sq);
                 allreduce_min_u8(alive.p, N);
-                ck(cudaMemsetAsync(counters.p, 0, sizeof(int), st), "memset");
                 alive_cnt = compact_alive(N, false);
+                ctr.rechecks += (unsigned long long)std::min(last_queue, kQueueCap);
+                if (last_queue > kQueueCap) fail(TSD_ERUNTIME, "knife-edge queue overflow (degenerate series?)");
+                ck(cudaMemsetAsync(counters.p, 0, sizeof(int), st), "memset");
                 if (alive_cnt == 0) break;
                 if (alive_cnt <= std::max(32, N / 8192)) break;
                 if ((double)alive_cnt > 0.7 * (double)prev) break;  // kill rate stalled
@@ -391,7 +415,10 @@ struct tsd_ctx {
         }
 
         std::vector<tsd_record> out;
-        if (alive_cnt == 0) return out;
+        if (alive_cnt == 0) {
+            harvest(m);
+            return out;
+        }
 
         // ---- sparse phase: full rows for every remaining candidate
         alive_cnt = compact_alive(N, true);
@@ -404,12 +431,15 @@ struct tsd_ctx {
         allreduce_max_u32(ymax.p, N);
         recheck(m, r_sq);
         allreduce_min_u8(alive.p, N);
-        if (read_counter(0) > kQueueCap)
-            fail(TSD_ERUNTIME, "knife-edge queue overflow (degenerate series?)");
 
         // ---- survivors: exact nearest neighbours
         const int sc = compact_alive(N, true);
-        if (sc == 0) return out;
+        ctr.rechecks += (unsigned long long)std::min(last_queue, kQueueCap);
+        if (last_queue > kQueueCap) fail(TSD_ERUNTIME, "knife-edge queue overflow (degenerate series?)");
+        if (sc == 0) {
+            harvest(m);
+            return out;
+        }
         launch_prep_survivors(list.p, sc, ymax.p, ythr.p, nnkey.p, st);
         ctr.kernel_launches += 1;
         group_rows(h_list, choose_span(h_list, m), groups);
@@ -434,12 +464,8 @@ struct tsd_ctx {
         std::vector<double> nn(sc);
         ck(cudaMemcpyAsync(nn.data(), nnout.p, sc * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
         h_int.ensure(2);
-        unsigned long long hacc[2];
-        ck(cudaMemcpyAsync(hacc, acc.p, sizeof(hacc), cudaMemcpyDeviceToHost, st), "D2H");
         sync();
-        ctr.cells += hacc[0];
-        ctr.seed_dots += hacc[1];
-        ctr.seed_flops += hacc[1] * 2ull * (unsigned long long)m;
+        harvest(m);
         ctr.exact_pairs += (unsigned long long)cc;
         out.reserve(sc);
         for (int e = 0; e < sc; ++e) {

@@ -74,16 +74,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_scan(const ScanParams p) {
     const int qbase = dir > 0 ? td.r0 + td.k0 : r_end + td.k0 + kW - 1;
     const int nq = rows - 1 + kW;
 
-    // ---- 0. skip tiles with nothing left to decide ----------------------
+    // ---- 0. skip tiles whose rows are all decided -------------------------
     {
         int any = 0;
         for (int s = tid; s < rows; s += kThreads) any |= p.alive[td.r0 + s];
-        if (MODE == kPrune && !any) {
-            for (int u = tid; u < nq; u += kThreads) {
-                const int q = dir > 0 ? qbase + u : qbase - u;
-                if (q >= 0 && q < N) any |= p.alive[q];
-            }
-        }
         if (!__syncthreads_or(any)) return;
     }
 
@@ -203,16 +197,21 @@ __global__ void __launch_bounds__(kThreads, 3) k_scan(const ScanParams p) {
     const double E = p.err_k * (double)kEps32 * (double)m * (double)smax_c * (double)smax_q *
                      (double)(rows + 8);
     const float Ef = (float)E;
+    // Row thresholds.  crow.z = tc: a live row's cells with x = cov*qn > tc may be
+    // within the error band of d^2 = r^2 (slow path); kNoEval marks rows whose
+    // cells are only walked (already decided, or not a survivor in kCollect).
+    constexpr float kNoEval = FLT_MAX;
+    int evals = 0;
     for (int s = tid; s < rows; s += kThreads) {
         const int c = dir > 0 ? td.r0 + s : r_end - s;
         const float cn = S.crow[s].w;
         const bool live = p.alive[c] != 0;
         float tc;
         if (MODE == kCollect) {
-            tc = FLT_MAX;  // no pruning in the collect pass
             S.cy[s] = (live && cn != 0.f) ? p.ythr[c] : FLT_MAX;
-        } else if (MODE == kPruneTrack && !live) {
-            tc = FLT_MAX;
+            tc = S.cy[s] < FLT_MAX ? 0.f : kNoEval;
+        } else if (!live) {
+            tc = kNoEval;
         } else if (cn == 0.f) {
             tc = -FLT_MAX;  // constant row: always take the exact-convention slow path
         } else {
@@ -221,9 +220,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_scan(const ScanParams p) {
             tc = tc - fabsf(tc) * 2.4e-7f;  // round toward -inf (conservative)
         }
         S.crow[s].z = tc;
+        evals += tc != kNoEval;
         if (MODE == kPruneTrack) S.ykey[s] = (live && cn != 0.f) ? 1u : 0u;  // 0 = untracked
     }
-    __syncthreads();
+    evals = __syncthreads_count(evals);
 
     // ---- 3. walk ----------------------------------------------------------
     float ra[kDiag], rb[kDiag], rc[kDiag];  // ring of q-side operands
@@ -242,72 +242,71 @@ __global__ void __launch_bounds__(kThreads, 3) k_scan(const ScanParams p) {
             const int ss = s0 + uu;
             if (ss < rows) {
                 const float4 cr = S.crow[ss];
-                float x[kDiag];
-                float mx = -FLT_MAX;
-#pragma unroll
-                for (int j = 0; j < kDiag; ++j) {
-                    const int rj = (j + uu) % kDiag;
-                    if (uu > 0 || s0 > 0) {
-                        cov[j] = fmaf(cr.x, rb[rj], cov[j]);
-                        cov[j] = fmaf(ra[rj], cr.y, cov[j]);
-                    }
-                    x[j] = cov[j] * rc[rj];
-                    mx = fmaxf(mx, x[j]);
-                }
-                if (MODE != kCollect && mx > cr.z) {
-                    // ---- slow path: exact conventions, certain kills, knife edges
-                    const int c = dir > 0 ? td.r0 + ss : r_end - ss;
+                if (uu > 0 || s0 > 0) {
 #pragma unroll
                     for (int j = 0; j < kDiag; ++j) {
                         const int rj = (j + uu) % kDiag;
-                        if (!(x[j] > cr.z)) continue;
-                        const int u = ss + ub + j;
-                        const int q = dir > 0 ? qbase + u : qbase - u;
-                        if (q < 0 || q >= N) continue;
-                        const float qn = rc[rj];
-                        if (cr.w == 0.f || qn == 0.f) {
-                            const double d = (cr.w == 0.f && qn == 0.f) ? 0.0 : 2.0 * (double)m;
-                            if (d < p.r_sq) {
-                                p.alive[c] = 0;
-                                p.alive[q] = 0;
-                            }
-                            continue;
-                        }
-                        const double corr = (double)x[j] * (double)cr.w;
-                        const double ec = E * (double)cr.w * (double)qn + kSlack;
-                        if (corr - ec > p.thr0) {
-                            p.alive[c] = 0;
-                            p.alive[q] = 0;
-                        } else if (corr + ec >= p.thr0) {
-                            const int at = atomicAdd(p.queue_count, 1);
-                            if (at < p.queue_cap) p.queue[at] = make_int2(c, q);
-                        }
+                        cov[j] = fmaf(cr.x, rb[rj], cov[j]);
+                        cov[j] = fmaf(ra[rj], cr.y, cov[j]);
                     }
                 }
-                if (MODE == kPruneTrack && S.ykey[ss] != 0u) {
-                    // lower bound of the row's max corr / cn: max_j (cov - E) * qn
-                    // (a constant q contributes corr 0 exactly: x = 0, rc = 0)
-                    float y = -FLT_MAX;
+                if (cr.z != kNoEval) {  // CTA-uniform branch: the row is undecided
+                    float x[kDiag];
+                    float mx = -FLT_MAX;
 #pragma unroll
                     for (int j = 0; j < kDiag; ++j) {
-                        const int u = ss + ub + j;
-                        const int q = dir > 0 ? qbase + u : qbase - u;
-                        if (q >= 0 && q < N) y = fmaxf(y, fmaf(-Ef, rc[(j + uu) % kDiag], x[j]));
+                        x[j] = cov[j] * rc[(j + uu) % kDiag];
+                        mx = fmaxf(mx, x[j]);
                     }
-                    y = warp_max(y);
-                    if (lane == 0 && y > -FLT_MAX) atomicMax(&S.ykey[ss], f2key(y));
-                }
-                if (MODE == kCollect) {
-                    const float th = S.cy[ss];
-                    if (th < FLT_MAX) {
+                    if (MODE != kCollect && mx > cr.z) {
+                        // ---- slow path: exact conventions, certain kill, knife edges.
+                        // Only the row candidate is killed (the pair's other end is
+                        // decided by its own row), so a decided row never re-enters.
                         const int c = dir > 0 ? td.r0 + ss : r_end - ss;
 #pragma unroll
                         for (int j = 0; j < kDiag; ++j) {
-                            const int rj = (j + uu) % kDiag;
+                            if (!(x[j] > cr.z)) continue;
+                            const int u = ss + ub + j;
+                            const int q = dir > 0 ? qbase + u : qbase - u;
+                            if (q < 0 || q >= N) continue;
+                            const float qn = rc[(j + uu) % kDiag];
+                            if (cr.w == 0.f || qn == 0.f) {
+                                const double d = (cr.w == 0.f && qn == 0.f) ? 0.0 : 2.0 * (double)m;
+                                if (d < p.r_sq) p.alive[c] = 0;
+                                continue;
+                            }
+                            const double corr = (double)x[j] * (double)cr.w;
+                            const double ec = E * (double)cr.w * (double)qn + kSlack;
+                            if (corr - ec > p.thr0) {
+                                p.alive[c] = 0;
+                            } else if (corr + ec >= p.thr0) {
+                                const int at = atomicAdd(p.queue_count, 1);
+                                if (at < p.queue_cap) p.queue[at] = make_int2(c, q);
+                            }
+                        }
+                    }
+                    if (MODE == kPruneTrack && S.ykey[ss] != 0u) {
+                        // lower bound of the row's max corr / cn: max_j (cov - E) * qn
+                        // (a constant q contributes corr 0 exactly: x = 0, rc = 0)
+                        float y = -FLT_MAX;
+#pragma unroll
+                        for (int j = 0; j < kDiag; ++j) {
+                            const int u = ss + ub + j;
+                            const int q = dir > 0 ? qbase + u : qbase - u;
+                            if (q >= 0 && q < N) y = fmaxf(y, fmaf(-Ef, rc[(j + uu) % kDiag], x[j]));
+                        }
+                        y = warp_max(y);
+                        if (lane == 0 && y > -FLT_MAX) atomicMax(&S.ykey[ss], f2key(y));
+                    }
+                    if (MODE == kCollect) {
+                        const float th = S.cy[ss];
+                        const int c = dir > 0 ? td.r0 + ss : r_end - ss;
+#pragma unroll
+                        for (int j = 0; j < kDiag; ++j) {
                             const int u = ss + ub + j;
                             const int q = dir > 0 ? qbase + u : qbase - u;
                             // upper bound (cov + E) * qn reaches the row's best lower bound
-                            if (q >= 0 && q < N && fmaf(Ef, rc[rj], x[j]) >= th) {
+                            if (q >= 0 && q < N && fmaf(Ef, rc[(j + uu) % kDiag], x[j]) >= th) {
                                 const int at = atomicAdd(p.coll_count, 1);
                                 if (at < p.coll_cap) p.coll[at] = make_int2(c, q);
                             }
@@ -334,8 +333,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_scan(const ScanParams p) {
         }
     }
     if (tid == 0) {
-        atomicAdd(p.cells, (unsigned long long)rows * (unsigned long long)kW);
-        atomicAdd(p.seeds, (unsigned long long)kW);
+        atomicAdd(&p.acc[0], (unsigned long long)rows * (unsigned long long)kW);
+        atomicAdd(&p.acc[1], (unsigned long long)evals * (unsigned long long)kW);
+        atomicAdd(&p.acc[2], (unsigned long long)kW);
     }
 }
 
