@@ -72,6 +72,8 @@ typedef struct {
     double sparse_ms;       /* ... of which sparse full-row phase */
     double collect_ms;      /* ... of which survivor near-pair collection */
     double total_ms;        /* device time of the last merlin/pardrag call (CUDA events) */
+    double host_wall_ms;    /* host wall time inside DRAG tries */
+    double host_wait_ms;    /* ... of which blocked in stream synchronisation */
 } tsd_counters;
 
 /* ---- context ------------------------------------------------------------ */

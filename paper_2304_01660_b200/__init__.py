@@ -49,7 +49,8 @@ class Counters(C.Structure):
                 ("pardrag_calls", C.c_uint64), ("scan_launches", C.c_uint64),
                 ("kernel_launches", C.c_uint64), ("host_syncs", C.c_uint64),
                 ("scan_ms", C.c_double), ("dense_ms", C.c_double), ("sparse_ms", C.c_double),
-                ("collect_ms", C.c_double), ("total_ms", C.c_double)]
+                ("collect_ms", C.c_double), ("total_ms", C.c_double),
+                ("host_wall_ms", C.c_double), ("host_wait_ms", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

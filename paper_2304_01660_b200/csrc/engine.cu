@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -116,7 +117,8 @@ struct tsd_ctx {
     DBuf<double> nnout;
     DBuf<TileDesc> tiles;
     HBuf<TileDesc> h_tiles;
-    HBuf<int> h_int;
+    HBuf<int> h_int, h_listbuf;
+    HBuf<unsigned long long> h_acc;
     HBuf<double> h_dbl;
     std::vector<int> h_list;
     int last_queue = 0;
@@ -135,8 +137,14 @@ struct tsd_ctx {
     void* comm = nullptr;
 
     // ------------------------------------------------------------------
+    static double now_ms() {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch())
+            .count();
+    }
     void sync() {
+        const double t0 = now_ms();
         ck(cudaStreamSynchronize(st), "stream sync");
+        ctr.host_wait_ms += now_ms() - t0;
         ctr.host_syncs += 1;
     }
 
@@ -213,6 +221,21 @@ struct tsd_ctx {
         return p;
     }
 
+    // Tile lists of one pardrag call are appended to a pinned arena and its
+    // device mirror (uploads are async; the arena resets when the call starts).
+    size_t tile_off = 0;
+    struct EvPair {
+        cudaEvent_t a, b;
+        int mode;
+    };
+    std::vector<EvPair> ev_pool;
+    size_t ev_used = 0;
+
+    void arena_reset() {
+        tile_off = 0;
+        ev_used = 0;
+    }
+
     void run_scan(int mode, const std::vector<TileDesc>& tl, ScanParams p) {
         // shard tiles cyclically across ranks: every rank sweeps a disjoint set
         std::vector<TileDesc> mine;
@@ -223,27 +246,49 @@ struct tsd_ctx {
         }
         const size_t nt = use->size();
         if (nt == 0) return;
-        h_tiles.ensure(nt);
-        tiles.ensure(nt);
-        // the previous scan (if any) must have consumed the pinned staging buffer
-        sync();
-        std::memcpy(h_tiles.p, use->data(), nt * sizeof(TileDesc));
-        ck(cudaMemcpyAsync(tiles.p, h_tiles.p, nt * sizeof(TileDesc), cudaMemcpyHostToDevice, st),
-           "tiles H2D");
-        p.tiles = tiles.p;
-        ck(cudaEventRecord(ev_a, st), "event");
+        if (tile_off + nt > h_tiles.cap || tile_off + nt > tiles.cap) {
+            // growing the arena: in-flight uploads must finish first
+            sync();
+            const size_t want = std::max<size_t>(2 * (tile_off + nt), 1 << 16);
+            std::vector<TileDesc> keep(h_tiles.p, h_tiles.p + tile_off);
+            h_tiles.release();
+            h_tiles.ensure(want);
+            tiles.ensure(want);
+            if (tile_off) std::memcpy(h_tiles.p, keep.data(), tile_off * sizeof(TileDesc));
+        }
+        TileDesc* hp = h_tiles.p + tile_off;
+        TileDesc* dp = tiles.p + tile_off;
+        tile_off += nt;
+        std::memcpy(hp, use->data(), nt * sizeof(TileDesc));
+        ck(cudaMemcpyAsync(dp, hp, nt * sizeof(TileDesc), cudaMemcpyHostToDevice, st), "tiles H2D");
+        p.tiles = dp;
+        if (ev_used == ev_pool.size()) {
+            EvPair e{};
+            ck(cudaEventCreate(&e.a), "event");
+            ck(cudaEventCreate(&e.b), "event");
+            ev_pool.push_back(e);
+        }
+        EvPair& e = ev_pool[ev_used++];
+        e.mode = mode;
+        ck(cudaEventRecord(e.a, st), "event");
         launch_scan(mode, (int)nt, p, st);
         ck(cudaGetLastError(), "scan launch");
-        ck(cudaEventRecord(ev_b, st), "event");
-        ck(cudaEventSynchronize(ev_b), "scan sync");
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, ev_a, ev_b);
-        ctr.scan_ms += ms;
-        if (mode == kPrune) ctr.dense_ms += ms;
-        else if (mode == kPruneTrack) ctr.sparse_ms += ms;
-        else ctr.collect_ms += ms;
+        ck(cudaEventRecord(e.b, st), "event");
         ctr.scan_launches += 1;
         ctr.kernel_launches += 1;
+    }
+
+    // after a full sync: fold the scan launch times of this call into ctr
+    void harvest_events() {
+        for (size_t i = 0; i < ev_used; ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev_pool[i].a, ev_pool[i].b);
+            ctr.scan_ms += ms;
+            if (ev_pool[i].mode == kPrune) ctr.dense_ms += ms;
+            else if (ev_pool[i].mode == kPruneTrack) ctr.sparse_ms += ms;
+            else ctr.collect_ms += ms;
+        }
+        ev_used = 0;
     }
 
     void recheck(int64_t m, double r_sq) {
@@ -253,26 +298,31 @@ struct tsd_ctx {
         ctr.kernel_launches += 1;
     }
 
-    // returns count of set flags in alive[0..N) and (optionally) the ordered list on host
-    int compact_alive(int N, bool want_list) {
+    // Count of set flags in alive[0..N) with one host round trip; with
+    // list_bound > 0 also the ordered list (list_bound must be >= the count,
+    // e.g. the previous count: flags only ever clear).
+    int compact_alive(int N, int list_bound) {
         const int nb = compact_blocks(N);
         blk.ensure(nb + 1);
         list.ensure(N);
         launch_compact(alive.p, N, blk.p, list.p, st);
         ctr.kernel_launches += 3;
         ck(cudaGetLastError(), "compact");
-        h_int.ensure(4);
         ck(cudaMemcpyAsync(h_int.p, blk.p + nb, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
         ck(cudaMemcpyAsync(h_int.p + 1, counters.p, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaMemcpyAsync(h_acc.p, acc.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "D2H");
+        if (list_bound > 0) {
+            h_listbuf.ensure(N);
+            ck(cudaMemcpyAsync(h_listbuf.p, list.p, (size_t)std::min(list_bound, N) * sizeof(int),
+                               cudaMemcpyDeviceToHost, st),
+               "list D2H");
+        }
         sync();
         const int cnt = h_int.p[0];
         last_queue = h_int.p[1];
-        if (want_list) {
-            h_list.resize(cnt);
-            if (cnt > 0) {
-                ck(cudaMemcpy(h_list.data(), list.p, cnt * sizeof(int), cudaMemcpyDeviceToHost),
-                   "list D2H");
-            }
+        if (list_bound > 0) {
+            if (cnt > list_bound) fail(TSD_ERUNTIME, "internal: alive count grew");
+            h_list.assign(h_listbuf.p, h_listbuf.p + cnt);
         }
         return cnt;
     }
@@ -315,6 +365,22 @@ struct tsd_ctx {
         return best_span;
     }
 
+    // diagonals k in [K0, K0 + nb*kW) right of each group's rows and the mirror
+    // range left of them, band-major so near diagonals run first
+    void band_tiles(const std::vector<int2>& groups, long long K0, long long nb, int N,
+                    std::vector<TileDesc>& out) {
+        out.clear();
+        for (long long b = 0; b < nb; ++b) {
+            const long long k0 = K0 + b * kW;
+            for (const auto& g : groups) {
+                const int a = g.x, rows = g.y - g.x + 1;
+                if (a + k0 < N) out.push_back(TileDesc{a, rows, (int)k0, +1});
+                const long long khi = -k0;  // tile covers [khi - kW + 1, khi]
+                if (g.y + khi >= 0) out.push_back(TileDesc{a, rows, (int)(khi - kW + 1), -1});
+            }
+        }
+    }
+
     void full_row_tiles(const std::vector<int2>& groups, int64_t m, int N, std::vector<TileDesc>& out) {
         out.clear();
         std::vector<int> npos(groups.size()), nneg(groups.size());
@@ -350,9 +416,9 @@ struct tsd_ctx {
     }
 
     // fold the device work counters of the current call into ctr
+    // (h_acc is refreshed by every compact_alive and by the final copy of a call)
     void harvest(int64_t m) {
-        unsigned long long hacc[3];
-        ck(cudaMemcpy(hacc, acc.p, sizeof(hacc), cudaMemcpyDeviceToHost), "acc D2H");
+        const unsigned long long* hacc = h_acc.p;
         ctr.cells += hacc[0];
         ctr.cells_eval += hacc[1];
         ctr.seed_dots += hacc[2];
@@ -363,9 +429,18 @@ struct tsd_ctx {
     // sort_discords.  If `all_nn` is given (r_sq must be 0) it receives nn for
     // every index.
     std::vector<tsd_record> pardrag_core(int64_t m, double r_sq, double* all_nn = nullptr) {
+        const double t_start = now_ms();
+        struct WallGuard {
+            tsd_ctx* c;
+            double t0;
+            ~WallGuard() { c->ctr.host_wall_ms += now_ms() - t0; }
+        } wall_guard{this, t_start};
         const int N = (int)(n - m + 1);
         derive(m);
         ensure_scan_buffers(N);
+        h_int.ensure(8);
+        h_acc.ensure(4);
+        arena_reset();
         ctr.pardrag_calls += 1;
         ck(cudaMemsetAsync(counters.p, 0, 2 * sizeof(int), st), "memset");
         ck(cudaMemsetAsync(acc.p, 0, 3 * sizeof(unsigned long long), st), "memset");
@@ -373,111 +448,111 @@ struct tsd_ctx {
         ctr.kernel_launches += 1;
         const ScanParams P = params(m, r_sq);
         std::vector<TileDesc> tl;
+        std::vector<int2> groups;
+        std::vector<tsd_record> out;
 
-        // ---- dense phase: bands of kW diagonals right of the main diagonal
+        // ---- band passes (PD3 selection): diagonals |k| in [K0, K0 + B) on both
+        // sides of every undecided row; only certain FP32 kills, no knife-edge
+        // work.  Pass 0 tiles all rows in blocks; later passes tile groups of the
+        // remaining rows (span chosen by the seed/walk cost model).  One host
+        // round trip per pass (count + ordered list of undecided rows).
         int alive_cnt = N;
         if (r_sq > 0.0) {
-            long long k_lo = m;
+            long long K0 = m;
             const long long k_max = (long long)N - 1;
-            int batch = 2;
-            int prev = N;
-            const int L = dense_rows;
-            while (k_lo <= k_max) {
-                tl.clear();
-                const long long nb = std::min<long long>(batch, (k_max - k_lo + kW) / kW);
-                // band b: diagonals k in [k_lo + b*kW, +kW) right of every row and the
-                // mirror band left of it; each row is decided by its own cells only
-                for (long long b = 0; b < nb; ++b) {
-                    const long long k0 = k_lo + b * kW;
-                    for (long long r0 = 0; r0 < N; r0 += L) {
-                        const int rows = (int)std::min<long long>(L, N - r0);
-                        if (r0 + k0 < N) tl.push_back(TileDesc{(int)r0, rows, (int)k0, +1});
-                        const long long khi = -k0;  // tile covers [khi - kW + 1, khi]
-                        if (r0 + rows - 1 + khi >= 0)
-                            tl.push_back(TileDesc{(int)r0, rows, (int)(khi - kW + 1), -1});
-                    }
+            for (int pass = 0; K0 <= k_max; ++pass) {
+                const long long nb = std::min<long long>(1ll << std::min(pass, 5), (k_max - K0 + kW) / kW);
+                if (pass == 0) {
+                    groups.clear();
+                    for (int r0 = 0; r0 < N; r0 += dense_rows)
+                        groups.push_back(make_int2(r0, std::min(N, r0 + dense_rows) - 1));
+                } else {
+                    group_rows(h_list, choose_span(h_list, m), groups);
                 }
-                k_lo += nb * kW;
+                band_tiles(groups, K0, nb, N, tl);
+                K0 += nb * kW;
                 run_scan(kPrune, tl, P);
                 allreduce_min_u8(alive.p, N);
-                recheck(m, r_sq);
-                allreduce_min_u8(alive.p, N);
-                alive_cnt = compact_alive(N, false);
-                ctr.rechecks += (unsigned long long)std::min(last_queue, kQueueCap);
-                if (last_queue > kQueueCap) fail(TSD_ERUNTIME, "knife-edge queue overflow (degenerate series?)");
-                ck(cudaMemsetAsync(counters.p, 0, sizeof(int), st), "memset");
+                const int prev = alive_cnt;
+                alive_cnt = compact_alive(N, prev);
                 if (alive_cnt == 0) break;
-                if (alive_cnt <= std::max(32, N / 8192)) break;
-                if ((double)alive_cnt > 0.7 * (double)prev) break;  // kill rate stalled
-                prev = alive_cnt;
-                batch *= 2;
+                if (alive_cnt <= std::max(64, N / 4096)) break;
+                if ((double)alive_cnt > 0.85 * (double)prev) break;  // bands stopped paying
             }
+        } else {
+            compact_alive(N, N);
         }
+        if (alive_cnt == 0) return finish(m, out);
 
-        std::vector<tsd_record> out;
-        if (alive_cnt == 0) {
-            harvest(m);
-            return out;
-        }
-
-        // ---- sparse phase: full rows for every remaining candidate
-        alive_cnt = compact_alive(N, true);
-        std::vector<int2> groups;
+        // ---- full rows (PD3 refinement) for every remaining candidate: prune,
+        // queue knife edges, and track a lower bound of each row's best corr
         group_rows(h_list, choose_span(h_list, m), groups);
         full_row_tiles(groups, m, N, tl);
         ck(cudaMemsetAsync(ymax.p, 0, (size_t)N * sizeof(unsigned), st), "memset");
         run_scan(kPruneTrack, tl, P);
         allreduce_min_u8(alive.p, N);
         allreduce_max_u32(ymax.p, N);
-        recheck(m, r_sq);
-        allreduce_min_u8(alive.p, N);
-
-        // ---- survivors: exact nearest neighbours
-        const int sc = compact_alive(N, true);
-        ctr.rechecks += (unsigned long long)std::min(last_queue, kQueueCap);
+        int sc = compact_alive(N, alive_cnt);
         if (last_queue > kQueueCap) fail(TSD_ERUNTIME, "knife-edge queue overflow (degenerate series?)");
-        if (sc == 0) {
-            harvest(m);
-            return out;
+        ctr.rechecks += (unsigned long long)last_queue;
+        if (last_queue > 0 && sc > 0) {
+            // knife edges: the reference's FP64 distance decides (pardrag.cpp:255)
+            launch_ref_pairs(0, t.p, (int)m, queue.p, counters.p + 0, kQueueCap, r_sq, alive.p, nnkey.p,
+                             last_queue, st);
+            ck(cudaGetLastError(), "recheck");
+            ctr.kernel_launches += 1;
+            allreduce_min_u8(alive.p, N);
+            sc = compact_alive(N, sc);
         }
+        if (sc == 0) return finish(m, out);
+
+        // ---- survivors: exact nearest neighbours (pardrag.cpp:378-416)
         launch_prep_survivors(list.p, sc, ymax.p, ythr.p, nnkey.p, st);
         ctr.kernel_launches += 1;
         group_rows(h_list, choose_span(h_list, m), groups);
         full_row_tiles(groups, m, N, tl);
         ck(cudaMemsetAsync(counters.p + 1, 0, sizeof(int), st), "memset");
         run_scan(kCollect, tl, P);
-        const int cc = read_counter(1);
-        if (cc > kCollCap) fail(TSD_ERUNTIME, "near-pair buffer overflow (degenerate series?)");
         launch_ref_pairs(1, t.p, (int)m, coll.p, counters.p + 1, kCollCap, r_sq, alive.p, nnkey.p,
-                         std::max(cc, 1), st);
+                         148 * 32, st);
         ck(cudaGetLastError(), "exact");
         // constant rows follow the constant conventions
-        h_int.ensure(4);
-        int cr_init[2] = {N, -1};
-        ck(cudaMemcpyAsync(counters.p + 2, cr_init, 2 * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+        h_int.p[2] = N;
+        h_int.p[3] = -1;
+        ck(cudaMemcpyAsync(counters.p + 2, h_int.p + 2, 2 * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
         launch_const_range(nrm.p, N, counters.p + 2, st);
         launch_const_nn(list.p, sc, nrm.p, counters.p + 2, N, (int)m, nnkey.p, st);
         allreduce_min_u64(nnkey.p, N);
         launch_gather_nn(list.p, sc, nnkey.p, nnout.p, st);
         ck(cudaGetLastError(), "gather");
         ctr.kernel_launches += 4;  // exact pairs, const range, const nn, gather
-        std::vector<double> nn(sc);
-        ck(cudaMemcpyAsync(nn.data(), nnout.p, sc * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
-        h_int.ensure(2);
+        h_dbl.ensure(sc);
+        ck(cudaMemcpyAsync(h_dbl.p, nnout.p, sc * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaMemcpyAsync(h_int.p, counters.p + 1, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaMemcpyAsync(h_acc.p, acc.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "D2H");
         sync();
-        harvest(m);
+        const int cc = h_int.p[0];
+        if (cc > kCollCap) fail(TSD_ERUNTIME, "near-pair buffer overflow (degenerate series?)");
         ctr.exact_pairs += (unsigned long long)cc;
         out.reserve(sc);
         for (int e = 0; e < sc; ++e) {
             const int c = h_list[e];
-            if (all_nn) all_nn[c] = nn[e];
-            out.push_back(tsd_record{(int64_t)c + 1, nn[e], std::sqrt(nn[e])});
+            const double d = h_dbl.p[e];
+            if (all_nn) all_nn[c] = d;
+            out.push_back(tsd_record{(int64_t)c + 1, d, std::sqrt(d)});
         }
         // sort_discords: nn_dist_sq desc, index asc (src/types.cpp:15-20)
         std::sort(out.begin(), out.end(), [](const tsd_record& a, const tsd_record& b) {
             if (a.nn_dist_sq != b.nn_dist_sq) return a.nn_dist_sq > b.nn_dist_sq;
             return a.index < b.index;
         });
+        return finish(m, out);
+    }
+
+    // end of a pardrag call (the stream is idle): fold in counters and timings
+    std::vector<tsd_record>& finish(int64_t m, std::vector<tsd_record>& out) {
+        harvest(m);
+        harvest_events();
         return out;
     }
 };
@@ -620,7 +695,13 @@ void tsd_ctx_destroy(tsd_ctx* c) {
     c->tiles.release();
     c->h_tiles.release();
     c->h_int.release();
+    c->h_listbuf.release();
+    c->h_acc.release();
     c->h_dbl.release();
+    for (auto& e : c->ev_pool) {
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
     if (c->ev_a) cudaEventDestroy(c->ev_a);
     if (c->ev_b) cudaEventDestroy(c->ev_b);
     if (c->ev_t0) cudaEventDestroy(c->ev_t0);

@@ -214,6 +214,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_scan(const ScanParams p) {
             tc = kNoEval;
         } else if (cn == 0.f) {
             tc = -FLT_MAX;  // constant row: always take the exact-convention slow path
+        } else if (MODE == kPrune) {
+            // band passes only make certain kills: every cell with x > tk has
+            // corr - eps_cell > thr0 (eps_cell <= eps_row); knife edges are left
+            // to the full-row pass
+            const double eps_row = E * (double)cn * (double)qn_max + kSlack + 8.0 * (double)kEps32;
+            const double tk = (p.thr0 + eps_row) / (double)cn;
+            tc = tk > 0.0 ? (float)tk * (1.f + 2.4e-7f) : -FLT_MAX;  // round up; tk<=0: careful path
         } else {
             const double eps_row = E * (double)cn * (double)qn_max + kSlack + 8.0 * (double)kEps32;
             tc = (float)((p.thr0 - eps_row) / (double)cn);
@@ -258,7 +265,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_scan(const ScanParams p) {
                         x[j] = cov[j] * rc[(j + uu) % kDiag];
                         mx = fmaxf(mx, x[j]);
                     }
-                    if (MODE != kCollect && mx > cr.z) {
+                    if (MODE == kPrune && mx > cr.z && cr.z > 0.f) {
+                        // certain kill of the row candidate (FP32 only)
+                        p.alive[dir > 0 ? td.r0 + ss : r_end - ss] = 0;
+                    } else if (MODE != kCollect && mx > cr.z) {
                         // ---- slow path: exact conventions, certain kill, knife edges.
                         // Only the row candidate is killed (the pair's other end is
                         // decided by its own row), so a decided row never re-enters.
@@ -279,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_scan(const ScanParams p) {
                             const double ec = E * (double)cr.w * (double)qn + kSlack;
                             if (corr - ec > p.thr0) {
                                 p.alive[c] = 0;
-                            } else if (corr + ec >= p.thr0) {
+                            } else if (MODE == kPruneTrack && corr + ec >= p.thr0) {
                                 const int at = atomicAdd(p.queue_count, 1);
                                 if (at < p.queue_cap) p.queue[at] = make_int2(c, q);
                             }

@@ -14,27 +14,52 @@
 
 namespace tsd {
 
-__global__ void k_init_prefix(const double* __restrict__ t, int n, int m,
-                              double* __restrict__ sum, double* __restrict__ sum_sq) {
-    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+// One CTA: the whole block stages the series through shared memory in
+// coalesced chunks; thread 0 runs the reference's sequential recurrence out of
+// shared memory (the only serial part), and the block writes the prefix
+// values back coalesced.
+constexpr int kPrefixChunk = 1024;  // 4 x 8 KB static shared memory
+
+__global__ void __launch_bounds__(1024) k_init_prefix(const double* __restrict__ t, int n, int m,
+                                                      double* __restrict__ sum,
+                                                      double* __restrict__ sum_sq) {
+    __shared__ double sin_[kPrefixChunk], sout[kPrefixChunk], ps[kPrefixChunk], pq[kPrefixChunk];
     const int cnt = n - m + 1;
     double s = 0.0, q = 0.0;
-    for (int k = 0; k < m; ++k) {
-        const double v = t[k];
-        s = __dadd_rn(s, v);
-        q = __dadd_rn(q, __dmul_rn(v, v));
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < m; ++k) {
+            const double v = t[k];
+            s = __dadd_rn(s, v);
+            q = __dadd_rn(q, __dmul_rn(v, v));
+        }
     }
-    sum[0] = s;
-    sum_sq[0] = q;
-    // sum += in - out; sum_sq += in*in - out*out   (stats.cpp:30-33)
-    int i = 0;
-    for (; i + 1 < cnt; ++i) {
-        const double out = t[i];
-        const double in = t[i + m];
-        s = __dadd_rn(s, __dsub_rn(in, out));
-        q = __dadd_rn(q, __dsub_rn(__dmul_rn(in, in), __dmul_rn(out, out)));
-        sum[i + 1] = s;
-        sum_sq[i + 1] = q;
+    // sums for index i+1 use out = t[i], in = t[i+m]   (stats.cpp:30-33)
+    for (int base = 0; base < cnt; base += kPrefixChunk) {
+        const int len = min(kPrefixChunk, cnt - base);
+        __syncthreads();
+        for (int x = threadIdx.x; x < len; x += blockDim.x) {
+            const int i = base + x;
+            sout[x] = t[i - 1 >= 0 ? i - 1 : 0];
+            sin_[x] = t[i - 1 >= 0 ? i - 1 + m : 0];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int x = 0; x < len; ++x) {
+                const int i = base + x;
+                if (i > 0) {
+                    const double out = sout[x], in = sin_[x];
+                    s = __dadd_rn(s, __dsub_rn(in, out));
+                    q = __dadd_rn(q, __dsub_rn(__dmul_rn(in, in), __dmul_rn(out, out)));
+                }
+                ps[x] = s;
+                pq[x] = q;
+            }
+        }
+        __syncthreads();
+        for (int x = threadIdx.x; x < len; x += blockDim.x) {
+            sum[base + x] = ps[x];
+            sum_sq[base + x] = pq[x];
+        }
     }
 }
 
@@ -98,7 +123,7 @@ static int grid_for(long long work, int threads) {
 void launch_init_stats(const double* t, int n, int m, double* mu, double* sig, double* scratch_a,
                        double* scratch_b, cudaStream_t st) {
     const int cnt = n - m + 1;
-    k_init_prefix<<<1, 32, 0, st>>>(t, n, m, scratch_a, scratch_b);
+    k_init_prefix<<<1, 1024, 0, st>>>(t, n, m, scratch_a, scratch_b);
     k_init_finish<<<grid_for(cnt, 256), 256, 0, st>>>(scratch_a, scratch_b, cnt, m, mu, sig);
 }
 
