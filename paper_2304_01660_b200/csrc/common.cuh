@@ -49,7 +49,8 @@ struct ScanParams {
     int2* queue;         // knife-edge pairs for the exact FP64 recheck
     int* queue_count;
     int queue_cap;
-    unsigned* ymax;      // kPruneTrack: ordered-float key of max lower-bound (x - E*qn) per row
+    unsigned* ymax;      // kPruneTrack: ordered-float key of the row's max route value x = cov*qn
+    unsigned* emax;      // kPruneTrack: bits of the largest tile error term E*qn_max seen by the row
     const float* ythr;   // kCollect: per-row collection threshold (decoded ymax)
     int2* coll;          // kCollect output pairs
     int* coll_count;

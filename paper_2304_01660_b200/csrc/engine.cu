@@ -19,6 +19,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <stdexcept>
@@ -110,7 +111,9 @@ struct tsd_ctx {
     DBuf<uint8_t> alive;
     DBuf<int2> queue, coll;
     DBuf<int> counters;  // [0] queue, [1] coll, [2..3] const range
-    DBuf<unsigned> ymax;
+    DBuf<unsigned> ymax, emax;
+    DBuf<double> bnd_lo, bnd_hi;
+    DBuf<int> cand;
     DBuf<float> ythr;
     DBuf<unsigned long long> nnkey, acc;  // acc: [0] cells, [1] seeds
     DBuf<int> blk, list;
@@ -124,6 +127,7 @@ struct tsd_ctx {
     int last_queue = 0;
 
     // tuning
+    bool debug = std::getenv("TSD_DEBUG") != nullptr;
     int dense_rows = 512;
     int sparse_rows = 0;  // 0: choose by cost model
     double err_k = 4.0;
@@ -212,6 +216,7 @@ struct tsd_ctx {
         p.queue_count = counters.p + 0;
         p.queue_cap = kQueueCap;
         p.ymax = ymax.p;
+        p.emax = emax.p;
         p.ythr = ythr.p;
         p.coll = coll.p;
         p.coll_count = counters.p + 1;
@@ -409,6 +414,10 @@ struct tsd_ctx {
         coll.ensure(kCollCap);
         counters.ensure(8);
         ymax.ensure(N);
+        emax.ensure(N);
+        bnd_lo.ensure(N);
+        bnd_hi.ensure(N);
+        cand.ensure(N);
         ythr.ensure(N);
         nnkey.ensure(N);
         acc.ensure(3);
@@ -428,7 +437,11 @@ struct tsd_ctx {
     // Core PD3: survivors {c : nn(c)^2 >= r_sq} with exact nn, sorted like
     // sort_discords.  If `all_nn` is given (r_sq must be 0) it receives nn for
     // every index.
-    std::vector<tsd_record> pardrag_core(int64_t m, double r_sq, double* all_nn = nullptr) {
+    // need_top > 0 (MERLIN): only the records that can be in the top need_top
+    // get exact distances; last_count still receives the full survivor count.
+    int last_count = 0;
+    std::vector<tsd_record> pardrag_core(int64_t m, double r_sq, double* all_nn = nullptr,
+                                         int64_t need_top = 0) {
         const double t_start = now_ms();
         struct WallGuard {
             tsd_ctx* c;
@@ -475,6 +488,9 @@ struct tsd_ctx {
                 allreduce_min_u8(alive.p, N);
                 const int prev = alive_cnt;
                 alive_cnt = compact_alive(N, prev);
+                if (debug)
+                    fprintf(stderr, "[tsd] m=%lld r2=%.6g pass=%d groups=%zu tiles=%zu K=%lld alive=%d\n",
+                            (long long)m, r_sq, pass, groups.size(), tl.size(), K0, alive_cnt);
                 if (alive_cnt == 0) break;
                 if (alive_cnt <= std::max(64, N / 4096)) break;
                 if ((double)alive_cnt > 0.85 * (double)prev) break;  // bands stopped paying
@@ -482,6 +498,7 @@ struct tsd_ctx {
         } else {
             compact_alive(N, N);
         }
+        last_count = 0;
         if (alive_cnt == 0) return finish(m, out);
 
         // ---- full rows (PD3 refinement) for every remaining candidate: prune,
@@ -489,10 +506,14 @@ struct tsd_ctx {
         group_rows(h_list, choose_span(h_list, m), groups);
         full_row_tiles(groups, m, N, tl);
         ck(cudaMemsetAsync(ymax.p, 0, (size_t)N * sizeof(unsigned), st), "memset");
+        ck(cudaMemsetAsync(emax.p, 0, (size_t)N * sizeof(unsigned), st), "memset");
         run_scan(kPruneTrack, tl, P);
         allreduce_min_u8(alive.p, N);
         allreduce_max_u32(ymax.p, N);
         int sc = compact_alive(N, alive_cnt);
+        if (debug)
+            fprintf(stderr, "[tsd] m=%lld full-rows groups=%zu tiles=%zu survivors=%d queue=%d\n",
+                    (long long)m, groups.size(), tl.size(), sc, last_queue);
         if (last_queue > kQueueCap) fail(TSD_ERUNTIME, "knife-edge queue overflow (degenerate series?)");
         ctr.rechecks += (unsigned long long)last_queue;
         if (last_queue > 0 && sc > 0) {
@@ -504,12 +525,44 @@ struct tsd_ctx {
             allreduce_min_u8(alive.p, N);
             sc = compact_alive(N, sc);
         }
+        last_count = sc;
         if (sc == 0) return finish(m, out);
 
         // ---- survivors: exact nearest neighbours (pardrag.cpp:378-416)
-        launch_prep_survivors(list.p, sc, ymax.p, ythr.p, nnkey.p, st);
+        last_count = sc;
+        h_int.p[2] = N;
+        h_int.p[3] = -1;
+        ck(cudaMemcpyAsync(counters.p + 2, h_int.p + 2, 2 * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
+        launch_const_range(nrm.p, N, counters.p + 2, st);
         ctr.kernel_launches += 1;
-        group_rows(h_list, choose_span(h_list, m), groups);
+        const int* ex_list = list.p;  // rows whose exact nn is computed
+        std::vector<int> cand_h;
+        const std::vector<int>* ex_h = &h_list;
+        if (need_top > 0 && sc > need_top) {
+            // MERLIN keeps only the top need_top records: exact distances only for
+            // survivors whose nn interval reaches the need_top-th largest lower bound
+            launch_nn_bounds(list.p, sc, ymax.p, emax.p, nrm.p, counters.p + 2, N, (int)m, bnd_lo.p, bnd_hi.p, st);
+            ctr.kernel_launches += 1;
+            h_dbl.ensure(2 * (size_t)sc);
+            ck(cudaMemcpyAsync(h_dbl.p, bnd_lo.p, sc * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaMemcpyAsync(h_dbl.p + sc, bnd_hi.p, sc * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+            sync();
+            std::vector<double> lo(h_dbl.p, h_dbl.p + sc);
+            std::nth_element(lo.begin(), lo.begin() + (need_top - 1), lo.end(), std::greater<double>());
+            const double lk = lo[need_top - 1];
+            for (int e = 0; e < sc; ++e)
+                if (h_dbl.p[sc + e] >= lk) cand_h.push_back(h_list[e]);
+            h_listbuf.ensure(cand_h.size());
+            std::memcpy(h_listbuf.p, cand_h.data(), cand_h.size() * sizeof(int));
+            ck(cudaMemcpyAsync(cand.p, h_listbuf.p, cand_h.size() * sizeof(int), cudaMemcpyHostToDevice, st),
+               "H2D");
+            ex_list = cand.p;
+            ex_h = &cand_h;
+        }
+        const int ec = (int)ex_h->size();
+        launch_prep_survivors(ex_list, ec, ymax.p, emax.p, ythr.p, nnkey.p, st);
+        ctr.kernel_launches += 1;
+        group_rows(*ex_h, choose_span(*ex_h, m), groups);
         full_row_tiles(groups, m, N, tl);
         ck(cudaMemsetAsync(counters.p + 1, 0, sizeof(int), st), "memset");
         run_scan(kCollect, tl, P);
@@ -517,26 +570,22 @@ struct tsd_ctx {
                          148 * 32, st);
         ck(cudaGetLastError(), "exact");
         // constant rows follow the constant conventions
-        h_int.p[2] = N;
-        h_int.p[3] = -1;
-        ck(cudaMemcpyAsync(counters.p + 2, h_int.p + 2, 2 * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
-        launch_const_range(nrm.p, N, counters.p + 2, st);
-        launch_const_nn(list.p, sc, nrm.p, counters.p + 2, N, (int)m, nnkey.p, st);
+        launch_const_nn(ex_list, ec, nrm.p, counters.p + 2, N, (int)m, nnkey.p, st);
         allreduce_min_u64(nnkey.p, N);
-        launch_gather_nn(list.p, sc, nnkey.p, nnout.p, st);
+        launch_gather_nn(ex_list, ec, nnkey.p, nnout.p, st);
         ck(cudaGetLastError(), "gather");
-        ctr.kernel_launches += 4;  // exact pairs, const range, const nn, gather
-        h_dbl.ensure(sc);
-        ck(cudaMemcpyAsync(h_dbl.p, nnout.p, sc * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+        ctr.kernel_launches += 3;  // exact pairs, const nn, gather
+        h_dbl.ensure(ec);
+        ck(cudaMemcpyAsync(h_dbl.p, nnout.p, ec * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
         ck(cudaMemcpyAsync(h_int.p, counters.p + 1, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
         ck(cudaMemcpyAsync(h_acc.p, acc.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "D2H");
         sync();
         const int cc = h_int.p[0];
         if (cc > kCollCap) fail(TSD_ERUNTIME, "near-pair buffer overflow (degenerate series?)");
         ctr.exact_pairs += (unsigned long long)cc;
-        out.reserve(sc);
-        for (int e = 0; e < sc; ++e) {
-            const int c = h_list[e];
+        out.reserve(ec);
+        for (int e = 0; e < ec; ++e) {
+            const int c = (*ex_h)[e];
             const double d = h_dbl.p[e];
             if (all_nn) all_nn[c] = d;
             out.push_back(tsd_record{(int64_t)c + 1, d, std::sqrt(d)});
@@ -686,6 +735,10 @@ void tsd_ctx_destroy(tsd_ctx* c) {
     c->coll.release();
     c->counters.release();
     c->ymax.release();
+    c->emax.release();
+    c->bnd_lo.release();
+    c->bnd_hi.release();
+    c->cand.release();
     c->ythr.release();
     c->nnkey.release();
     c->acc.release();
@@ -880,13 +933,14 @@ int tsd_merlin(tsd_ctx* c, int64_t min_len, int64_t max_len, const tsd_merlin_op
             bool success = false;
             for (;;) {
                 const double r_sq = r > 0.0 ? r * r : 0.0;
-                got = c->pardrag_core(m, r_sq);
-                if ((int64_t)got.size() >= top_k) {
+                got = c->pardrag_core(m, r_sq, nullptr, top_k);
+                const int64_t found = c->last_count;  // every survivor counts (merlin.cpp:100)
+                if (found >= top_k) {
                     success = true;
                     break;
                 }
                 if (tries >= max_retries) {
-                    success = !got.empty();
+                    success = found > 0;
                     break;
                 }
                 ++tries;

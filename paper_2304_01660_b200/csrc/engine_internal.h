@@ -23,8 +23,10 @@ void launch_ref_pairs(int mode, const double* t, int m, const int2* pairs, const
 void launch_fill_u8(uint8_t* a, int n, uint8_t v, cudaStream_t st);
 int compact_blocks(int n);
 void launch_compact(const uint8_t* a, int n, int* blk, int* out, cudaStream_t st);
-void launch_prep_survivors(const int* list, int cnt, const unsigned* ymax, float* ythr,
+void launch_prep_survivors(const int* list, int cnt, const unsigned* ymax, const unsigned* emax, float* ythr,
                            unsigned long long* nnkey, cudaStream_t st);
+void launch_nn_bounds(const int* list, int cnt, const unsigned* ymax, const unsigned* emax, const float* nrm,
+                      const int* const_range, int N, int m, double* lo, double* hi, cudaStream_t st);
 void launch_const_range(const float* nrm, int N, int* out, cudaStream_t st);
 void launch_const_nn(const int* list, int cnt, const float* nrm, const int* const_range, int N, int m,
                      unsigned long long* nnkey, cudaStream_t st);

@@ -296,15 +296,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_scan(const ScanParams p) {
                         }
                     }
                     if (MODE == kPruneTrack && S.ykey[ss] != 0u) {
-                        // lower bound of the row's max corr / cn: max_j (cov - E) * qn
-                        // (a constant q contributes corr 0 exactly: x = 0, rc = 0)
+                        // row max of the FP32 route value x = cov*qn over valid q (a
+                        // constant q contributes corr 0 exactly); the tile's error term
+                        // E*qn_max is folded in per row at the end
+                        const int lim = (dir > 0 ? N - qbase : qbase + 1) - ss - ub;
                         float y = -FLT_MAX;
 #pragma unroll
-                        for (int j = 0; j < kDiag; ++j) {
-                            const int u = ss + ub + j;
-                            const int q = dir > 0 ? qbase + u : qbase - u;
-                            if (q >= 0 && q < N) y = fmaxf(y, fmaf(-Ef, rc[(j + uu) % kDiag], x[j]));
-                        }
+                        for (int j = 0; j < kDiag; ++j)
+                            if (j < lim) y = fmaxf(y, x[j]);
                         y = warp_max(y);
                         if (lane == 0 && y > -FLT_MAX) atomicMax(&S.ykey[ss], f2key(y));
                     }
@@ -334,11 +333,13 @@ __global__ void __launch_bounds__(kThreads, 3) k_scan(const ScanParams p) {
 
     if (MODE == kPruneTrack) {
         __syncthreads();
+        const unsigned ekey = __float_as_uint(Ef * qn_max * (1.f + 4.8e-7f));  // >= 0: bit order
         for (int s = tid; s < rows; s += kThreads) {
             const unsigned k = S.ykey[s];
             if (k > 1u) {
                 const int c = dir > 0 ? td.r0 + s : r_end - s;
                 atomicMax(&p.ymax[c], k);
+                atomicMax(&p.emax[c], ekey);
             }
         }
     }
@@ -533,18 +534,55 @@ __global__ void k_compact_scatter(const uint8_t* __restrict__ a, int n, const in
     }
 }
 
-// survivors: reset exact-nn keys and decode collection thresholds
+// survivors: reset exact-nn keys and decode collection thresholds.  The
+// tracked max route value x* and the row's largest tile error term e give a
+// lower bound x* - e of the row's true best corr / cn; every q whose upper
+// bound x + E*qn reaches it may be the reference's minimiser.
 __global__ void k_prep_survivors(const int* __restrict__ list, int cnt, const unsigned* __restrict__ ymax,
-                                 float* __restrict__ ythr, unsigned long long* __restrict__ nnkey) {
+                                 const unsigned* __restrict__ emax, float* __restrict__ ythr,
+                                 unsigned long long* __restrict__ nnkey) {
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += gridDim.x * blockDim.x) {
         const int c = list[e];
         const unsigned k = ymax[c];
-        // two ulps below the best lower bound, so FP64 rounding of near-ties in the
-        // exact distance can never exclude the reference's minimiser
-        ythr[c] = k > 1u ? nextafterf(nextafterf(key2f(k), -FLT_MAX), -FLT_MAX)
-                         : -FLT_MAX;  // no tracked data: collect everything
+        float th = -FLT_MAX;  // no tracked data: collect everything
+        if (k > 1u) {
+            const float lo = key2f(k) - __uint_as_float(emax[c]);
+            // two ulps down: FP64 rounding of near-ties can never exclude the minimiser
+            th = nextafterf(nextafterf(lo - fabsf(lo) * 2.4e-7f, -FLT_MAX), -FLT_MAX);
+        }
+        ythr[c] = th;
+        nnkey[c] = 0x7ff0000000000000ull;  // +inf
+    }
+}
 
-        nnkey[c] = 0x7ff0000000000000ull;       // +inf
+// per-survivor interval [lo, hi] of the exact nn^2 from the tracked route maxima
+// (constant rows: the exact convention value)
+__global__ void k_nn_bounds(const int* __restrict__ list, int cnt, const unsigned* __restrict__ ymax,
+                            const unsigned* __restrict__ emax, const float* __restrict__ nrm,
+                            const int* __restrict__ const_range, int N, int m, double* __restrict__ lo,
+                            double* __restrict__ hi) {
+    const double inf = __longlong_as_double(0x7ff0000000000000ll);
+    const double two_m = 2.0 * (double)m;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += gridDim.x * blockDim.x) {
+        const int c = list[e];
+        const float cn = nrm[c];
+        double l = 0.0, h = inf;
+        if (cn == 0.f) {
+            const int a = const_range[0], b = const_range[1];
+            double d = inf;
+            if (c - a >= m || b - c >= m) d = 0.0;
+            else if (c - m >= 0 || c + m <= N - 1) d = two_m;
+            l = h = d;
+        } else if (ymax[c] > 1u) {
+            const double x = (double)key2f(ymax[c]);
+            const double ee = (double)__uint_as_float(emax[c]);
+            const double slack = 1e-6 + 1e-9;
+            l = two_m * (1.0 - ((x + ee) * (double)cn + slack));
+            h = two_m * (1.0 - ((x - ee) * (double)cn - slack));
+            if (l < 0.0) l = 0.0;
+        }
+        lo[e] = l;
+        hi[e] = h;
     }
 }
 
@@ -630,9 +668,14 @@ void launch_compact(const uint8_t* a, int n, int* blk, int* out, cudaStream_t st
     k_compact_scatter<<<nb, kCompactBlock, 0, st>>>(a, n, blk, out);
 }
 
-void launch_prep_survivors(const int* list, int cnt, const unsigned* ymax, float* ythr,
+void launch_prep_survivors(const int* list, int cnt, const unsigned* ymax, const unsigned* emax, float* ythr,
                            unsigned long long* nnkey, cudaStream_t st) {
-    k_prep_survivors<<<grid_for(cnt, 256), 256, 0, st>>>(list, cnt, ymax, ythr, nnkey);
+    k_prep_survivors<<<grid_for(cnt, 256), 256, 0, st>>>(list, cnt, ymax, emax, ythr, nnkey);
+}
+
+void launch_nn_bounds(const int* list, int cnt, const unsigned* ymax, const unsigned* emax, const float* nrm,
+                      const int* const_range, int N, int m, double* lo, double* hi, cudaStream_t st) {
+    k_nn_bounds<<<grid_for(cnt, 256), 256, 0, st>>>(list, cnt, ymax, emax, nrm, const_range, N, m, lo, hi);
 }
 
 void launch_const_range(const float* nrm, int N, int* out, cudaStream_t st) {

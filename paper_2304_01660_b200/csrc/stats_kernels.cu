@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(1024) k_init_prefix(const double* __restrict__
     __shared__ double sin_[kPrefixChunk], sout[kPrefixChunk], ps[kPrefixChunk], pq[kPrefixChunk];
     const int cnt = n - m + 1;
     double s = 0.0, q = 0.0;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 || threadIdx.x == 32) {
         for (int k = 0; k < m; ++k) {
             const double v = t[k];
             s = __dadd_rn(s, v);
@@ -43,16 +43,36 @@ __global__ void __launch_bounds__(1024) k_init_prefix(const double* __restrict__
             sin_[x] = t[i - 1 >= 0 ? i - 1 + m : 0];
         }
         __syncthreads();
+        // the two chains are independent: warp 0 lane 0 runs sum, warp 1 lane 0 sum_sq
         if (threadIdx.x == 0) {
-            for (int x = 0; x < len; ++x) {
-                const int i = base + x;
-                if (i > 0) {
-                    const double out = sout[x], in = sin_[x];
-                    s = __dadd_rn(s, __dsub_rn(in, out));
-                    q = __dadd_rn(q, __dsub_rn(__dmul_rn(in, in), __dmul_rn(out, out)));
+            for (int x = 0; x < len; x += 8) {
+                double d[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    d[u] = (x + u < len) ? __dsub_rn(sin_[x + u], sout[x + u]) : 0.0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (x + u < len) {
+                        if (base + x + u > 0) s = __dadd_rn(s, d[u]);
+                        ps[x + u] = s;
+                    }
                 }
-                ps[x] = s;
-                pq[x] = q;
+            }
+        } else if (threadIdx.x == 32) {
+            for (int x = 0; x < len; x += 8) {
+                double d[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const double in = x + u < len ? sin_[x + u] : 0.0, out = x + u < len ? sout[x + u] : 0.0;
+                    d[u] = __dsub_rn(__dmul_rn(in, in), __dmul_rn(out, out));
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (x + u < len) {
+                        if (base + x + u > 0) q = __dadd_rn(q, d[u]);
+                        pq[x + u] = q;
+                    }
+                }
             }
         }
         __syncthreads();
