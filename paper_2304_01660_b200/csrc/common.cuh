@@ -26,6 +26,7 @@ struct TileDesc {
     int rows;  // number of rows (<= kMaxRows), all < N
     int k0;    // lowest diagonal of the tile; the tile covers [k0, k0 + kW)
     int dir;   // +1: positive side walked downward; -1: negative side walked upward
+    int seed;  // >= 0: seed row kept resident across lengths (ScanParams::seedqt), else -1
 };
 
 enum ScanMode : int {
@@ -56,6 +57,7 @@ struct ScanParams {
     int* coll_count;
     int coll_cap;
     const TileDesc* tiles;
+    const double* seedqt;  // resident raw dot products QT(i, i+k) of the band-0 tiles (kW per tile)
     unsigned long long* acc;  // accounting: [0] cells walked, [1] cells evaluated, [2] seed dots
 };
 

@@ -113,6 +113,10 @@ struct tsd_ctx {
     DBuf<int> counters;  // [0] queue, [1] coll, [2..3] const range
     DBuf<unsigned> ymax, emax;
     DBuf<double> bnd_lo, bnd_hi;
+    // resident band-0 seed rows (length recurrence), valid for length seed_m
+    DBuf<double> seedqt;
+    int64_t seed_m = -1;
+    int seed_L = 0, seed_kA = 0, seed_nb = 0;
     DBuf<int> cand;
     DBuf<float> ythr;
     DBuf<unsigned long long> nnkey, acc;  // acc: [0] cells, [1] seeds
@@ -196,6 +200,25 @@ struct tsd_ctx {
         derived_m = m;
     }
 
+    // ---- resident seed rows ----------------------------------------------
+    void seed_init(int64_t m, int64_t kA) {
+        const int64_t N = n - m + 1;
+        seed_L = dense_rows;
+        seed_kA = (int)kA;
+        seed_nb = 2 * (int)((N + seed_L - 1) / seed_L);
+        seedqt.ensure((size_t)seed_nb * kW);
+        launch_seed_init(t.p, (int)n, (int)m, seed_L, seed_kA, seed_nb, seedqt.p, st);
+        ck(cudaGetLastError(), "seed init");
+        ctr.kernel_launches += 1;
+        seed_m = m;
+    }
+    void seed_advance() {  // seed_m -> seed_m + 1
+        launch_seed_advance(t.p, (int)n, (int)seed_m, seed_L, seed_kA, seed_nb, seedqt.p, st);
+        ck(cudaGetLastError(), "seed advance");
+        ctr.kernel_launches += 1;
+        ++seed_m;
+    }
+
     // ---- scan helpers ---------------------------------------------------
     ScanParams params(int64_t m, double r_sq) {
         ScanParams p{};
@@ -217,6 +240,7 @@ struct tsd_ctx {
         p.queue_cap = kQueueCap;
         p.ymax = ymax.p;
         p.emax = emax.p;
+        p.seedqt = seedqt.p;
         p.ythr = ythr.p;
         p.coll = coll.p;
         p.coll_count = counters.p + 1;
@@ -379,9 +403,9 @@ struct tsd_ctx {
             const long long k0 = K0 + b * kW;
             for (const auto& g : groups) {
                 const int a = g.x, rows = g.y - g.x + 1;
-                if (a + k0 < N) out.push_back(TileDesc{a, rows, (int)k0, +1});
+                if (a + k0 < N) out.push_back(TileDesc{a, rows, (int)k0, +1, -1});
                 const long long khi = -k0;  // tile covers [khi - kW + 1, khi]
-                if (g.y + khi >= 0) out.push_back(TileDesc{a, rows, (int)(khi - kW + 1), -1});
+                if (g.y + khi >= 0) out.push_back(TileDesc{a, rows, (int)(khi - kW + 1), -1, -1});
             }
         }
     }
@@ -402,8 +426,8 @@ struct tsd_ctx {
             for (size_t g = 0; g < groups.size(); ++g) {
                 const int a = groups[g].x, b = groups[g].y;
                 const int rows = b - a + 1;
-                if (i < npos[g]) out.push_back(TileDesc{a, rows, (int)m + i * kW, +1});
-                if (i < nneg[g]) out.push_back(TileDesc{a, rows, -(int)m - (i + 1) * kW + 1, -1});
+                if (i < npos[g]) out.push_back(TileDesc{a, rows, (int)m + i * kW, +1, -1});
+                if (i < nneg[g]) out.push_back(TileDesc{a, rows, -(int)m - (i + 1) * kW + 1, -1, -1});
             }
         }
     }
@@ -475,15 +499,30 @@ struct tsd_ctx {
             const long long k_max = (long long)N - 1;
             for (int pass = 0; K0 <= k_max; ++pass) {
                 const long long nb = std::min<long long>(1ll << std::min(pass, 5), (k_max - K0 + kW) / kW);
-                if (pass == 0) {
-                    groups.clear();
-                    for (int r0 = 0; r0 < N; r0 += dense_rows)
-                        groups.push_back(make_int2(r0, std::min(N, r0 + dense_rows) - 1));
+                if (pass == 0 && seed_m == m && seed_L == dense_rows) {
+                    // band 0 at the fixed offset kA (>= m for every length of the run)
+                    // seeded from the resident rows: no direct dot products
+                    tl.clear();
+                    const long long kA = seed_kA;
+                    for (int j = 0; (long long)j * seed_L < N; ++j) {
+                        const int r0 = j * seed_L, rows = std::min(N, r0 + seed_L) - r0;
+                        if (r0 + kA < N) tl.push_back(TileDesc{r0, rows, (int)kA, +1, 2 * j});
+                        if (r0 + rows - 1 - kA >= 0)
+                            tl.push_back(TileDesc{r0, rows, (int)(-kA - kW + 1), -1,
+                                                  rows == seed_L ? 2 * j + 1 : -1});
+                    }
+                    K0 = kA + kW;
                 } else {
-                    group_rows(h_list, choose_span(h_list, m), groups);
+                    if (pass == 0) {
+                        groups.clear();
+                        for (int r0 = 0; r0 < N; r0 += dense_rows)
+                            groups.push_back(make_int2(r0, std::min(N, r0 + dense_rows) - 1));
+                    } else {
+                        group_rows(h_list, choose_span(h_list, m), groups);
+                    }
+                    band_tiles(groups, K0, nb, N, tl);
+                    K0 += nb * kW;
                 }
-                band_tiles(groups, K0, nb, N, tl);
-                K0 += nb * kW;
                 run_scan(kPrune, tl, P);
                 allreduce_min_u8(alive.p, N);
                 const int prev = alive_cnt;
@@ -736,6 +775,7 @@ void tsd_ctx_destroy(tsd_ctx* c) {
     c->counters.release();
     c->ymax.release();
     c->emax.release();
+    c->seedqt.release();
     c->bnd_lo.release();
     c->bnd_hi.release();
     c->cand.release();
@@ -798,6 +838,7 @@ int tsd_series_set(tsd_ctx* c, const double* v, int64_t n) {
         c->sync();
         c->stats_m = -1;
         c->derived_m = -1;
+        c->seed_m = -1;
     });
 }
 
@@ -856,6 +897,7 @@ int tsd_pardrag(tsd_ctx* c, int64_t m, double r_sq, int64_t seglen, const double
         layout(c->n, m, seglen, lay);  // same preconditions as the reference call
         ck(cudaSetDevice(c->device), "cudaSetDevice");
         ck(cudaEventRecord(c->ev_t0, c->st), "event");
+        c->seed_m = -1;
         const int64_t N = c->n - m + 1;
         if (mu && sigma) {
             c->mu.ensure(c->n);
@@ -885,6 +927,7 @@ int tsd_brute_force_nn(tsd_ctx* c, int64_t m, double* out) {
         if (m < 3 || m > c->n - 2) fail(TSD_EINVAL, "brute_force_nn: length out of range");
         ck(cudaSetDevice(c->device), "cudaSetDevice");
         if (c->stats_m != m) c->init_stats_dev(m);
+        c->seed_m = -1;
         const int64_t N = c->n - m + 1;
         for (int64_t i = 0; i < N; ++i) out[i] = INFINITY;
         c->pardrag_core(m, 0.0, out);
@@ -909,6 +952,10 @@ int tsd_merlin(tsd_ctx* c, int64_t min_len, int64_t max_len, const tsd_merlin_op
 
         std::vector<double> history;
         c->init_stats_dev(min_len);
+        // band-0 seeds resident for the whole run when the band fits (kA = maxL
+        // keeps every band-0 diagonal a non-self match at every length)
+        c->seed_m = -1;
+        if ((int64_t)max_len + kW < n - max_len + 1) c->seed_init(min_len, max_len);
         for (int64_t m = min_len; m <= max_len; ++m) {
             const int64_t k = m - min_len;
             counts[k] = 0;
@@ -916,6 +963,7 @@ int tsd_merlin(tsd_ctx* c, int64_t min_len, int64_t max_len, const tsd_merlin_op
             if (m > min_len) {
                 if (reuse) c->advance_stats_dev();
                 else c->init_stats_dev(m);
+                if (c->seed_m == m - 1) c->seed_advance();
             }
             const int phase = m == min_len ? 0 : (m < min_len + 5 ? 1 : 2);
             if (phase != 0 && history.empty()) {

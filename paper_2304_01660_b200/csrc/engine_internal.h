@@ -27,6 +27,8 @@ void launch_prep_survivors(const int* list, int cnt, const unsigned* ymax, const
                            unsigned long long* nnkey, cudaStream_t st);
 void launch_nn_bounds(const int* list, int cnt, const unsigned* ymax, const unsigned* emax, const float* nrm,
                       const int* const_range, int N, int m, double* lo, double* hi, cudaStream_t st);
+void launch_seed_init(const double* t, int n, int m, int L, int kA, int nb, double* qt, cudaStream_t st);
+void launch_seed_advance(const double* t, int n, int m, int L, int kA, int nb, double* qt, cudaStream_t st);
 void launch_const_range(const float* nrm, int N, int* out, cudaStream_t st);
 void launch_const_nn(const int* list, int cnt, const float* nrm, const int* const_range, int N, int m,
                      unsigned long long* nnkey, cudaStream_t st);

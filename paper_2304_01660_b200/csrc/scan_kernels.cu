@@ -82,6 +82,19 @@ __global__ void __launch_bounds__(kThreads, 3) k_scan(const ScanParams p) {
     }
 
     // ---- 1. seeds: cov(c_first, q) for this thread's kDiag diagonals (FP64) --
+    float cov[kDiag];
+    if (td.seed >= 0) {
+        // resident seed row, carried across lengths by the dot-product length
+        // recurrence (k_seed_advance): cov = QT - m mu_c mu_q
+        const double* qt = p.seedqt + (size_t)td.seed * kW + tid * kDiag;
+        const double mmu = (double)m * p.mu[c_first];
+#pragma unroll
+        for (int j = 0; j < kDiag; ++j) {
+            const int u = tid * kDiag + j;
+            const int q = dir > 0 ? qbase + u : qbase - u;
+            cov[j] = (q >= 0 && q < N) ? (float)(qt[j] - mmu * p.mu[q]) : 0.f;
+        }
+    } else {
     // cov = sum_p (t[c+p]-mu_c) t[q+p] - mu_q * sum_p (t[c+p]-mu_c)
     const int qlo = dir > 0 ? qbase : qbase - (kW - 1);
     const int o_t = dir > 0 ? tid * kDiag : kW - kDiag - tid * kDiag;  // lowest window offset
@@ -121,7 +134,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_scan(const ScanParams p) {
             for (int i = 0; i < kDiag; ++i) acc[i] = fma(av, S.u.seed.win[o_t + pp + i], acc[i]);
         }
     }
-    float cov[kDiag];
 #pragma unroll
     for (int i = 0; i < kDiag; ++i) {
         const int q = qlo + o_t + i;
@@ -133,6 +145,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_scan(const ScanParams p) {
     } else {
 #pragma unroll
         for (int j = 0; j < kDiag; ++j) cov[j] = (float)acc[kDiag - 1 - j];
+    }
     }
     __syncthreads();  // seed buffers are reused below
 
@@ -346,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_scan(const ScanParams p) {
     if (tid == 0) {
         atomicAdd(&p.acc[0], (unsigned long long)rows * (unsigned long long)kW);
         atomicAdd(&p.acc[1], (unsigned long long)evals * (unsigned long long)kW);
-        atomicAdd(&p.acc[2], (unsigned long long)kW);
+        if (td.seed < 0) atomicAdd(&p.acc[2], (unsigned long long)kW);
     }
 }
 
@@ -618,6 +631,50 @@ __global__ void k_gather_nn(const int* __restrict__ list, int cnt,
 }
 
 // ---------------------------------------------------------------------------
+// Resident band-0 seed rows (north_star (a)): tile b = 2*j + side holds the raw
+// dot products QT(i, i+k) of row i = j*L (side 0, k = kA + u) or i = j*L + L - 1
+// (side 1, k = -kA - u), u in [0, kW).  Initialised once at the first length,
+// then carried m -> m+1 with QT_{m+1}(i,q) = QT_m(i,q) + t[i+m] t[q+m].
+__device__ __forceinline__ bool seed_pair(int b, int u, int L, int kA, int N, int& i, int& q) {
+    const int j = b >> 1;
+    i = (b & 1) ? j * L + L - 1 : j * L;
+    q = (b & 1) ? i - kA - u : i + kA + u;
+    return i < N && q >= 0 && q < N;
+}
+
+__global__ void k_seed_init(const double* __restrict__ t, int n, int m, int L, int kA, int nb,
+                            double* __restrict__ qt) {
+    const int N = n - m + 1;
+    const long long total = (long long)nb * kW;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        int i, q;
+        double s = 0.0;
+        if (seed_pair((int)(e / kW), (int)(e % kW), L, kA, N, i, q))
+            for (int k = 0; k < m; ++k) s = fma(t[i + k], t[q + k], s);
+        qt[e] = s;
+    }
+}
+
+__global__ void k_seed_advance(const double* __restrict__ t, int n, int m, int L, int kA, int nb,
+                               double* __restrict__ qt) {
+    const int N1 = n - m;  // subsequence count of length m+1
+    const long long total = (long long)nb * kW;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        int i, q;
+        if (seed_pair((int)(e / kW), (int)(e % kW), L, kA, N1, i, q)) qt[e] = fma(t[i + m], t[q + m], qt[e]);
+    }
+}
+
+void launch_seed_init(const double* t, int n, int m, int L, int kA, int nb, double* qt, cudaStream_t st) {
+    k_seed_init<<<148 * 8, 256, 0, st>>>(t, n, m, L, kA, nb, qt);
+}
+
+void launch_seed_advance(const double* t, int n, int m, int L, int kA, int nb, double* qt, cudaStream_t st) {
+    k_seed_advance<<<148 * 8, 256, 0, st>>>(t, n, m, L, kA, nb, qt);
+}
+
 static int grid_for(long long work, int threads) {
     long long b = (work + threads - 1) / threads;
     if (b < 1) b = 1;

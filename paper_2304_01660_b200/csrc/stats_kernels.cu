@@ -18,12 +18,14 @@ namespace tsd {
 // coalesced chunks; thread 0 runs the reference's sequential recurrence out of
 // shared memory (the only serial part), and the block writes the prefix
 // values back coalesced.
-constexpr int kPrefixChunk = 1024;  // 4 x 8 KB static shared memory
+constexpr int kPrefixChunk = 2048;  // 2 x 16 KB static shared memory
 
 __global__ void __launch_bounds__(1024) k_init_prefix(const double* __restrict__ t, int n, int m,
                                                       double* __restrict__ sum,
                                                       double* __restrict__ sum_sq) {
-    __shared__ double sin_[kPrefixChunk], sout[kPrefixChunk], ps[kPrefixChunk], pq[kPrefixChunk];
+    // ds/dq hold the per-step increments, then are overwritten in place by the
+    // running sums (each position is read before it is written)
+    __shared__ double ds[kPrefixChunk], dq[kPrefixChunk];
     const int cnt = n - m + 1;
     double s = 0.0, q = 0.0;
     if (threadIdx.x == 0 || threadIdx.x == 32) {
@@ -33,52 +35,49 @@ __global__ void __launch_bounds__(1024) k_init_prefix(const double* __restrict__
             q = __dadd_rn(q, __dmul_rn(v, v));
         }
     }
-    // sums for index i+1 use out = t[i], in = t[i+m]   (stats.cpp:30-33)
+    // index i >= 1 adds in - out and in*in - out*out with out = t[i-1], in = t[i-1+m]
     for (int base = 0; base < cnt; base += kPrefixChunk) {
         const int len = min(kPrefixChunk, cnt - base);
         __syncthreads();
         for (int x = threadIdx.x; x < len; x += blockDim.x) {
             const int i = base + x;
-            sout[x] = t[i - 1 >= 0 ? i - 1 : 0];
-            sin_[x] = t[i - 1 >= 0 ? i - 1 + m : 0];
+            if (i > 0) {
+                const double out = t[i - 1], in = t[i - 1 + m];
+                ds[x] = __dsub_rn(in, out);
+                dq[x] = __dsub_rn(__dmul_rn(in, in), __dmul_rn(out, out));
+            }
         }
         __syncthreads();
-        // the two chains are independent: warp 0 lane 0 runs sum, warp 1 lane 0 sum_sq
-        if (threadIdx.x == 0) {
-            for (int x = 0; x < len; x += 8) {
-                double d[8];
+        // the two sequential chains run concurrently on two warps
+        if (threadIdx.x == 0 || threadIdx.x == 32) {
+            double* d = threadIdx.x == 0 ? ds : dq;
+            double acc = threadIdx.x == 0 ? s : q;
+            int x = 0;
+            if (base == 0) {
+                d[0] = acc;  // index 0: the initial window sums
+                x = 1;
+            }
+            for (; x + 16 <= len; x += 16) {
+                double v[16];
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    d[u] = (x + u < len) ? __dsub_rn(sin_[x + u], sout[x + u]) : 0.0;
+                for (int u = 0; u < 16; ++u) v[u] = d[x + u];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    if (x + u < len) {
-                        if (base + x + u > 0) s = __dadd_rn(s, d[u]);
-                        ps[x + u] = s;
-                    }
+                for (int u = 0; u < 16; ++u) {
+                    acc = __dadd_rn(acc, v[u]);
+                    d[x + u] = acc;
                 }
             }
-        } else if (threadIdx.x == 32) {
-            for (int x = 0; x < len; x += 8) {
-                double d[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const double in = x + u < len ? sin_[x + u] : 0.0, out = x + u < len ? sout[x + u] : 0.0;
-                    d[u] = __dsub_rn(__dmul_rn(in, in), __dmul_rn(out, out));
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    if (x + u < len) {
-                        if (base + x + u > 0) q = __dadd_rn(q, d[u]);
-                        pq[x + u] = q;
-                    }
-                }
+            for (; x < len; ++x) {
+                acc = __dadd_rn(acc, d[x]);
+                d[x] = acc;
             }
+            if (threadIdx.x == 0) s = acc;
+            else q = acc;
         }
         __syncthreads();
         for (int x = threadIdx.x; x < len; x += blockDim.x) {
-            sum[base + x] = ps[x];
-            sum_sq[base + x] = pq[x];
+            sum[base + x] = ds[x];
+            sum_sq[base + x] = dq[x];
         }
     }
 }

@@ -113,6 +113,25 @@ def test_merlin_golden_c2(engine):
     check_merlin(rep, fx)
 
 
+@pytest.mark.slow
+def test_merlin_golden_c4(engine):
+    # BASELINE config 4: n=1,000,000 random walk, lengths 512..1024 (513 lengths);
+    # the reference needed ~57 min on 6 threads to produce this fixture
+    fx = load_golden("c4.json")
+    engine.set_series(series_of(fx["input"]))
+    rep = engine.merlin_full(fx["min_len"], fx["max_len"], top_k=fx["top_k"], seglen=fx["seglen"])
+    check_merlin(rep, fx)
+
+
+@pytest.mark.slow
+def test_merlin_golden_c5(engine):
+    # BASELINE config 5: n=2,000,000 random walk, lengths 128..640, top-3
+    fx = load_golden("c5.json")
+    engine.set_series(series_of(fx["input"]))
+    rep = engine.merlin_full(fx["min_len"], fx["max_len"], top_k=fx["top_k"], seglen=fx["seglen"])
+    check_merlin(rep, fx)
+
+
 def test_merlin_csv_bytes(engine):
     import paper_2304_01660_b200 as P
     g = load_golden("small.json")
