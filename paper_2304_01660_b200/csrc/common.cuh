@@ -18,7 +18,7 @@ constexpr double kSigmaEps = 1e-12;
 constexpr int kThreads = 128;            // threads per scan CTA
 constexpr int kDiag = 9;                 // diagonals per thread (odd: conflict-free strided smem)
 constexpr int kW = kThreads * kDiag;     // 1152 diagonals per tile
-constexpr int kMaxRows = 1024;           // max rows per tile
+constexpr int kMaxRows = 512;            // max rows per tile
 constexpr int kSeedChunk = 512;          // seed dot products are staged m in chunks of this
 
 struct TileDesc {

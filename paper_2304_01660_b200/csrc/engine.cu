@@ -382,7 +382,7 @@ struct tsd_ctx {
         double best = 1e300;
         int best_span = 64;
         std::vector<int2> g;
-        for (int span : {16, 32, 64, 128, 256, 512, 1024}) {
+        for (int span : {16, 32, 64, 128, 256, 512}) {
             group_rows(lst, span, g);
             double cost = 0.0;
             for (const auto& x : g) cost += 2.0 * (double)m + 3.0 * (double)(x.y - x.x + 1 + kDiag);

@@ -58,7 +58,7 @@ __device__ __forceinline__ float warp_max(float v) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 3) k_scan(const ScanParams p) {
+__global__ void __launch_bounds__(kThreads, 6) k_scan(const ScanParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ScanSmem& S = *reinterpret_cast<ScanSmem*>(smem_raw);
 
@@ -256,12 +256,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_scan(const ScanParams p) {
     }
     const int lane = tid & 31;
 
+    float4 cr_next = S.crow[0];  // row operands are prefetched one step ahead
     for (int s0 = 0; s0 < rows; s0 += kDiag) {
 #pragma unroll
         for (int uu = 0; uu < kDiag; ++uu) {
             const int ss = s0 + uu;
             if (ss < rows) {
-                const float4 cr = S.crow[ss];
+                const float4 cr = cr_next;
+                cr_next = S.crow[ss + 1 < rows ? ss + 1 : ss];
                 if (uu > 0 || s0 > 0) {
 #pragma unroll
                     for (int j = 0; j < kDiag; ++j) {
