@@ -46,6 +46,10 @@ struct __align__(16) ScanSmem {
             double a[kSeedChunk];
             double win[kW + kSeedChunk];
         } seed;
+        struct {
+            float a[kSeedChunk];
+            float win[kW + kSeedChunk];
+        } seed32;
     } u;
     float red[3][kThreads / 32];
     int flag;
@@ -81,8 +85,9 @@ __global__ void __launch_bounds__(kThreads, 6) k_scan(const ScanParams p) {
         if (!__syncthreads_or(any)) return;
     }
 
-    // ---- 1. seeds: cov(c_first, q) for this thread's kDiag diagonals (FP64) --
+    // ---- 1. seeds: cov(c_first, q) for this thread's kDiag diagonals --------
     float cov[kDiag];
+    double e_seed = 0.0;  // absolute error bound of FP32 seeds (0 for FP64 / resident seeds)
     if (td.seed >= 0) {
         // resident seed row, carried across lengths by the dot-product length
         // recurrence (k_seed_advance): cov = QT - m mu_c mu_q
@@ -93,6 +98,72 @@ __global__ void __launch_bounds__(kThreads, 6) k_scan(const ScanParams p) {
             const int u = tid * kDiag + j;
             const int q = dir > 0 ? qbase + u : qbase - u;
             cov[j] = (q >= 0 && q < N) ? (float)(qt[j] - mmu * p.mu[q]) : 0.f;
+        }
+    } else if (MODE == kPrune) {
+        // band passes only make certain kills, so their seeds may be FP32: the
+        // rounding of a = t[c+p]-mu_c, w = t[q+p]-anchor and of the m-term sums is
+        // bounded by E_seed (added to the tile's error bound below)
+        const int qlo = dir > 0 ? qbase : qbase - (kW - 1);
+        const int o_t = dir > 0 ? tid * kDiag : kW - kDiag - tid * kDiag;
+        const int qmid = min(max(qlo + kW / 2, 0), N - 1);
+        const double anchor = p.mu[qmid];
+        const double mu_c = p.mu[c_first];
+        float acc[kDiag];
+#pragma unroll
+        for (int i = 0; i < kDiag; ++i) acc[i] = 0.f;
+        float delta = 0.f, wmax = 0.f;
+        for (int pc = 0; pc < m; pc += kSeedChunk) {
+            const int len = min(kSeedChunk, m - pc);
+            __syncthreads();
+            for (int x = tid; x < len; x += kThreads) S.u.seed32.a[x] = (float)(p.t[c_first + pc + x] - mu_c);
+            for (int x = tid; x < kW + len - 1; x += kThreads) {
+                const int g = qlo + pc + x;
+                const float w = (g >= 0 && g < p.n) ? (float)(p.t[g] - anchor) : 0.f;
+                S.u.seed32.win[x] = w;
+                wmax = fmaxf(wmax, fabsf(w));
+            }
+            __syncthreads();
+            float w[kDiag];
+#pragma unroll
+            for (int i = 0; i < kDiag - 1; ++i) w[i] = S.u.seed32.win[o_t + i];
+            int pp = 0;
+            for (; pp + kDiag <= len; pp += kDiag) {
+#pragma unroll
+                for (int uu = 0; uu < kDiag; ++uu) {
+                    w[(uu + kDiag - 1) % kDiag] = S.u.seed32.win[o_t + pp + uu + kDiag - 1];
+                    const float av = S.u.seed32.a[pp + uu];
+                    delta += av;
+#pragma unroll
+                    for (int i = 0; i < kDiag; ++i) acc[i] = fmaf(av, w[(uu + i) % kDiag], acc[i]);
+                }
+            }
+            for (; pp < len; ++pp) {
+                const float av = S.u.seed32.a[pp];
+                delta += av;
+#pragma unroll
+                for (int i = 0; i < kDiag; ++i) acc[i] = fmaf(av, S.u.seed32.win[o_t + pp + i], acc[i]);
+            }
+        }
+        wmax = warp_max(wmax);
+        if ((tid & 31) == 0) S.red[0][tid >> 5] = wmax;
+        __syncthreads();
+        wmax = 0.f;
+#pragma unroll
+        for (int w2 = 0; w2 < kThreads / 32; ++w2) wmax = fmaxf(wmax, S.red[0][w2]);
+        // |seed error| <= (m + 4) eps * sum|a| * wmax, sum|a| <= m sigma_c
+        e_seed = (double)(m + 4) * (double)kEps32 * (double)m * p.sig[c_first] * (double)wmax;
+        double seedv[kDiag];
+#pragma unroll
+        for (int i = 0; i < kDiag; ++i) {
+            const int q = qlo + o_t + i;
+            seedv[i] = (q >= 0 && q < N) ? (double)acc[i] - (p.mu[q] - anchor) * (double)delta : 0.0;
+        }
+        if (dir > 0) {
+#pragma unroll
+            for (int j = 0; j < kDiag; ++j) cov[j] = (float)seedv[j];
+        } else {
+#pragma unroll
+            for (int j = 0; j < kDiag; ++j) cov[j] = (float)seedv[kDiag - 1 - j];
         }
     } else {
     // cov = sum_p (t[c+p]-mu_c) t[q+p] - mu_q * sum_p (t[c+p]-mu_c)
@@ -186,7 +257,9 @@ __global__ void __launch_bounds__(kThreads, 6) k_scan(const ScanParams p) {
         }
         S.u.walk.qdf[u] = a;
         S.u.walk.qdg[u] = b;
-        S.u.walk.qn[u] = nn;
+        // an invalid q gets a NaN norm: its x = cov*qn is NaN, which never passes a
+        // threshold test and is ignored by fmaxf (a constant q keeps qn = 0, x = 0)
+        S.u.walk.qn[u] = (u < nq && q >= 0 && q < N) ? nn : __int_as_float(0x7fffffff);
     }
     smax_c = warp_max(smax_c);
     smax_q = warp_max(smax_q);
@@ -208,7 +281,8 @@ __global__ void __launch_bounds__(kThreads, 6) k_scan(const ScanParams p) {
     }
     // absolute FP32 covariance error bound for every cell of this tile
     const double E = p.err_k * (double)kEps32 * (double)m * (double)smax_c * (double)smax_q *
-                     (double)(rows + 8);
+                         (double)(rows + 8) +
+                     e_seed;
     const float Ef = (float)E;
     // Row thresholds.  crow.z = tc: a live row's cells with x = cov*qn > tc may be
     // within the error band of d^2 = r^2 (slow path); kNoEval marks rows whose
@@ -233,7 +307,8 @@ __global__ void __launch_bounds__(kThreads, 6) k_scan(const ScanParams p) {
             // to the full-row pass
             const double eps_row = E * (double)cn * (double)qn_max + kSlack + 8.0 * (double)kEps32;
             const double tk = (p.thr0 + eps_row) / (double)cn;
-            tc = tk > 0.0 ? (float)tk * (1.f + 2.4e-7f) : -FLT_MAX;  // round up; tk<=0: careful path
+            tc = (float)tk;
+            tc = tc + fabsf(tc) * 2.4e-7f;  // round toward +inf (conservative)
         } else {
             const double eps_row = E * (double)cn * (double)qn_max + kSlack + 8.0 * (double)kEps32;
             tc = (float)((p.thr0 - eps_row) / (double)cn);
@@ -280,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_scan(const ScanParams p) {
                         x[j] = cov[j] * rc[(j + uu) % kDiag];
                         mx = fmaxf(mx, x[j]);
                     }
-                    if (MODE == kPrune && mx > cr.z && cr.z > 0.f) {
+                    if (MODE == kPrune && mx > cr.z && cr.w != 0.f) {
                         // certain kill of the row candidate (FP32 only)
                         p.alive[dir > 0 ? td.r0 + ss : r_end - ss] = 0;
                     } else if (MODE != kCollect && mx > cr.z) {
