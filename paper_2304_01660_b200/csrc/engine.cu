@@ -340,10 +340,12 @@ struct tsd_ctx {
         ck(cudaMemcpyAsync(h_int.p, blk.p + nb, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
         ck(cudaMemcpyAsync(h_int.p + 1, counters.p, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
         ck(cudaMemcpyAsync(h_acc.p, acc.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "D2H");
-        if (list_bound > 0) {
+        // speculative list copy: flags only clear, and after the first band pass
+        // few rows remain, so copy a bounded prefix and fetch the rest only if needed
+        const int spec = list_bound > 0 ? std::min(list_bound, std::max(65536, N / 16)) : 0;
+        if (spec > 0) {
             h_listbuf.ensure(N);
-            ck(cudaMemcpyAsync(h_listbuf.p, list.p, (size_t)std::min(list_bound, N) * sizeof(int),
-                               cudaMemcpyDeviceToHost, st),
+            ck(cudaMemcpyAsync(h_listbuf.p, list.p, (size_t)spec * sizeof(int), cudaMemcpyDeviceToHost, st),
                "list D2H");
         }
         sync();
@@ -351,6 +353,12 @@ struct tsd_ctx {
         last_queue = h_int.p[1];
         if (list_bound > 0) {
             if (cnt > list_bound) fail(TSD_ERUNTIME, "internal: alive count grew");
+            if (cnt > spec) {
+                ck(cudaMemcpyAsync(h_listbuf.p + spec, list.p + spec, (size_t)(cnt - spec) * sizeof(int),
+                                   cudaMemcpyDeviceToHost, st),
+                   "list D2H");
+                sync();
+            }
             h_list.assign(h_listbuf.p, h_listbuf.p + cnt);
         }
         return cnt;
@@ -366,26 +374,31 @@ struct tsd_ctx {
     // group sorted row indices into spans of at most `span` rows
     static void group_rows(const std::vector<int>& lst, int span, std::vector<int2>& groups) {
         groups.clear();
-        size_t i = 0;
-        while (i < lst.size()) {
-            const int a = lst[i];
-            size_t j = i;
-            while (j + 1 < lst.size() && lst[j + 1] - a < span) ++j;
-            groups.push_back(make_int2(a, lst[j]));
-            i = j + 1;
+        auto it = lst.begin();
+        while (it != lst.end()) {
+            const int a = *it;
+            auto nx = std::lower_bound(it, lst.end(), a + span);
+            groups.push_back(make_int2(a, *(nx - 1)));
+            it = nx;
         }
     }
 
+    // span (max rows per group) minimising ~sum over groups of (2m seed work + 3 per
+    // walked row) per diagonal; groups are counted by galloping, not built
     int choose_span(const std::vector<int>& lst, int64_t m) {
         if (sparse_rows > 0) return sparse_rows;
-        // cost per q of one group ~ seeds (2*m FP32-equivalent FMAs per FP64 seed) + 3 per row
         double best = 1e300;
         int best_span = 64;
-        std::vector<int2> g;
         for (int span : {16, 32, 64, 128, 256, 512}) {
-            group_rows(lst, span, g);
             double cost = 0.0;
-            for (const auto& x : g) cost += 2.0 * (double)m + 3.0 * (double)(x.y - x.x + 1 + kDiag);
+            auto it = lst.begin();
+            while (it != lst.end()) {
+                const int a = *it;
+                auto nx = std::lower_bound(it, lst.end(), a + span);
+                cost += 2.0 * (double)m + 3.0 * (double)(*(nx - 1) - a + 1 + kDiag);
+                it = nx;
+                if (cost >= best) break;
+            }
             if (cost < best) {
                 best = cost;
                 best_span = span;
