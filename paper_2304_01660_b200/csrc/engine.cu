@@ -129,6 +129,7 @@ struct tsd_ctx {
     HBuf<double> h_dbl;
     std::vector<int> h_list;
     int last_queue = 0;
+    double hs_build = 0, hs_group = 0, hs_scan_api = 0, hs_compact = 0, hs_tail = 0;  // debug host timers (ms)
 
     // tuning
     bool debug = std::getenv("TSD_DEBUG") != nullptr;
@@ -266,6 +267,12 @@ struct tsd_ctx {
     }
 
     void run_scan(int mode, const std::vector<TileDesc>& tl, ScanParams p) {
+        const double t_in = now_ms();
+        struct Acc {
+            double& a;
+            double t0;
+            ~Acc() { a += now_ms() - t0; }
+        } acc_guard{hs_scan_api, t_in};
         // shard tiles cyclically across ranks: every rank sweeps a disjoint set
         std::vector<TileDesc> mine;
         const std::vector<TileDesc>* use = &tl;
@@ -331,6 +338,13 @@ struct tsd_ctx {
     // list_bound > 0 also the ordered list (list_bound must be >= the count,
     // e.g. the previous count: flags only ever clear).
     int compact_alive(int N, int list_bound) {
+        const double t_in = now_ms();
+        const double w_in = ctr.host_wait_ms;
+        struct Acc {
+            tsd_ctx* c;
+            double t0, w0;
+            ~Acc() { c->hs_compact += (now_ms() - t0) - (c->ctr.host_wait_ms - w0); }
+        } acc_guard{this, t_in, w_in};
         const int nb = compact_blocks(N);
         blk.ensure(nb + 1);
         list.ensure(N);
@@ -386,7 +400,15 @@ struct tsd_ctx {
     // span (max rows per group) minimising ~sum over groups of (2m seed work + 3 per
     // walked row) per diagonal; groups are counted by galloping, not built
     int choose_span(const std::vector<int>& lst, int64_t m) {
+        const double t_in = now_ms();
+        struct Acc {
+            double& a;
+            double t0;
+            ~Acc() { a += now_ms() - t0; }
+        } acc_guard{hs_group, t_in};
         if (sparse_rows > 0) return sparse_rows;
+        // dense lists (>= 1 row in 64 undecided): whole 512-row blocks are cheapest
+        if (!lst.empty() && (long long)lst.size() * 64 >= (long long)(lst.back() - lst.front() + 1)) return 512;
         double best = 1e300;
         int best_span = 64;
         for (int span : {16, 32, 64, 128, 256, 512}) {
@@ -424,6 +446,12 @@ struct tsd_ctx {
     }
 
     void full_row_tiles(const std::vector<int2>& groups, int64_t m, int N, std::vector<TileDesc>& out) {
+        const double t_in = now_ms();
+        struct Acc {
+            double& a;
+            double t0;
+            ~Acc() { a += now_ms() - t0; }
+        } acc_guard{hs_build, t_in};
         out.clear();
         std::vector<int> npos(groups.size()), nneg(groups.size());
         int maxc = 0;
@@ -772,6 +800,9 @@ int tsd_ctx_create(int device, tsd_ctx** out) {
 
 void tsd_ctx_destroy(tsd_ctx* c) {
     if (!c) return;
+    if (c->debug)
+        fprintf(stderr, "[tsd] host ms: build %.1f group %.1f scan_api %.1f compact %.1f | wall %.1f wait %.1f\n",
+                c->hs_build, c->hs_group, c->hs_scan_api, c->hs_compact, c->ctr.host_wall_ms, c->ctr.host_wait_ms);
     cudaSetDevice(c->device);
     if (c->comm) nccl_destroy(c->comm);
     c->t.release();

@@ -32,15 +32,19 @@ namespace tsd {
 constexpr float kEps32 = 5.9604645e-08f;  // 2^-24
 constexpr double kSlack = 1e-9;           // absolute corr slack around the threshold
 
+// rows are padded to a multiple of kDiag (+1 for the one-step prefetch); padded
+// rows carry zero operands (exact no-op increments) and are never evaluated
+constexpr int kRowsPad = kMaxRows + kDiag + 1;
+constexpr int kQPad = kMaxRows + kDiag + kW + kDiag;
+
 struct __align__(16) ScanSmem {
-    float4 crow[kMaxRows];  // per row: {cdf, cdg, tc, cn}
-    float cy[kMaxRows];     // kCollect: per-row collection threshold
-    unsigned ykey[kMaxRows];
+    float4 crow[kRowsPad];  // per row: {cdf, cdg, tc, cn}
+    float cy[kRowsPad];     // kCollect: per-row collection threshold
+    unsigned ykey[kRowsPad];
     union {
         struct {
-            float qdf[kMaxRows + kW + kDiag];
-            float qdg[kMaxRows + kW + kDiag];
-            float qn[kMaxRows + kW + kDiag];
+            float2 qd[kQPad];  // (df, dg) of the q side
+            float qn[kQPad];   // norm of the q side (NaN: invalid q)
         } walk;
         struct {
             double a[kSeedChunk];
@@ -240,7 +244,9 @@ __global__ void __launch_bounds__(kThreads, 6) k_scan(const ScanParams p) {
         if (v.w != 0.f) smax_c = fmaxf(smax_c, (float)p.sig[c]);
         S.crow[s] = v;
     }
-    for (int u = tid; u < nq + kDiag; u += kThreads) {
+    const int rows_p = (rows + kDiag - 1) / kDiag * kDiag;
+    for (int s = rows + tid; s <= rows_p; s += kThreads) S.crow[s] = make_float4(0.f, 0.f, FLT_MAX, 0.f);
+    for (int u = tid; u < rows_p + kW + kDiag; u += kThreads) {
         const int q = dir > 0 ? qbase + u : qbase - u;
         float a = 0.f, b = 0.f, nn = 0.f;
         if (u < nq && q >= 0 && q < N) {
@@ -255,8 +261,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_scan(const ScanParams p) {
                 qn_max = fmaxf(qn_max, nn);
             }
         }
-        S.u.walk.qdf[u] = a;
-        S.u.walk.qdg[u] = b;
+        S.u.walk.qd[u] = make_float2(a, b);
         // an invalid q gets a NaN norm: its x = cov*qn is NaN, which never passes a
         // threshold test and is ignored by fmaxf (a constant q keeps qn = 0, x = 0)
         S.u.walk.qn[u] = (u < nq && q >= 0 && q < N) ? nn : __int_as_float(0x7fffffff);
@@ -321,103 +326,103 @@ __global__ void __launch_bounds__(kThreads, 6) k_scan(const ScanParams p) {
     evals = __syncthreads_count(evals);
 
     // ---- 3. walk ----------------------------------------------------------
-    float ra[kDiag], rb[kDiag], rc[kDiag];  // ring of q-side operands
+    // Step s: row c(s) against q(u), u = s + t*kDiag + j.  The q-side operands of
+    // slot j at step s live in ring[(j + s) % kDiag]; rows are padded so the
+    // loop runs in whole kDiag blocks with compile-time ring indices and no
+    // bounds checks.  Step 0 carries zero row operands (no increment).
+    float2 rd[kDiag];
+    float rn[kDiag];
     const int ub = tid * kDiag;
+    const float2* qdp = S.u.walk.qd + ub;
+    const float* qnp = S.u.walk.qn + ub;
+    const float4* crp = S.crow;
 #pragma unroll
     for (int j = 0; j < kDiag; ++j) {
-        ra[j] = S.u.walk.qdf[ub + j];
-        rb[j] = S.u.walk.qdg[ub + j];
-        rc[j] = S.u.walk.qn[ub + j];
+        rd[j] = qdp[j];
+        rn[j] = qnp[j];
     }
     const int lane = tid & 31;
 
-    float4 cr_next = S.crow[0];  // row operands are prefetched one step ahead
-    for (int s0 = 0; s0 < rows; s0 += kDiag) {
+    float4 cr_next = crp[0];  // row operands are prefetched one step ahead
+    for (int s0 = 0; s0 < rows_p; s0 += kDiag) {
 #pragma unroll
         for (int uu = 0; uu < kDiag; ++uu) {
             const int ss = s0 + uu;
-            if (ss < rows) {
-                const float4 cr = cr_next;
-                cr_next = S.crow[ss + 1 < rows ? ss + 1 : ss];
-                if (uu > 0 || s0 > 0) {
+            const float4 cr = cr_next;
+            cr_next = crp[ss + 1];
 #pragma unroll
-                    for (int j = 0; j < kDiag; ++j) {
-                        const int rj = (j + uu) % kDiag;
-                        cov[j] = fmaf(cr.x, rb[rj], cov[j]);
-                        cov[j] = fmaf(ra[rj], cr.y, cov[j]);
-                    }
-                }
-                if (cr.z != kNoEval) {  // CTA-uniform branch: the row is undecided
-                    float x[kDiag];
-                    float mx = -FLT_MAX;
-#pragma unroll
-                    for (int j = 0; j < kDiag; ++j) {
-                        x[j] = cov[j] * rc[(j + uu) % kDiag];
-                        mx = fmaxf(mx, x[j]);
-                    }
-                    if (MODE == kPrune && mx > cr.z && cr.w != 0.f) {
-                        // certain kill of the row candidate (FP32 only)
-                        p.alive[dir > 0 ? td.r0 + ss : r_end - ss] = 0;
-                    } else if (MODE != kCollect && mx > cr.z) {
-                        // ---- slow path: exact conventions, certain kill, knife edges.
-                        // Only the row candidate is killed (the pair's other end is
-                        // decided by its own row), so a decided row never re-enters.
-                        const int c = dir > 0 ? td.r0 + ss : r_end - ss;
-#pragma unroll
-                        for (int j = 0; j < kDiag; ++j) {
-                            if (!(x[j] > cr.z)) continue;
-                            const int u = ss + ub + j;
-                            const int q = dir > 0 ? qbase + u : qbase - u;
-                            if (q < 0 || q >= N) continue;
-                            const float qn = rc[(j + uu) % kDiag];
-                            if (cr.w == 0.f || qn == 0.f) {
-                                const double d = (cr.w == 0.f && qn == 0.f) ? 0.0 : 2.0 * (double)m;
-                                if (d < p.r_sq) p.alive[c] = 0;
-                                continue;
-                            }
-                            const double corr = (double)x[j] * (double)cr.w;
-                            const double ec = E * (double)cr.w * (double)qn + kSlack;
-                            if (corr - ec > p.thr0) {
-                                p.alive[c] = 0;
-                            } else if (MODE == kPruneTrack && corr + ec >= p.thr0) {
-                                const int at = atomicAdd(p.queue_count, 1);
-                                if (at < p.queue_cap) p.queue[at] = make_int2(c, q);
-                            }
-                        }
-                    }
-                    if (MODE == kPruneTrack && S.ykey[ss] != 0u) {
-                        // row max of the FP32 route value x = cov*qn over valid q (a
-                        // constant q contributes corr 0 exactly); the tile's error term
-                        // E*qn_max is folded in per row at the end
-                        const int lim = (dir > 0 ? N - qbase : qbase + 1) - ss - ub;
-                        float y = -FLT_MAX;
-#pragma unroll
-                        for (int j = 0; j < kDiag; ++j)
-                            if (j < lim) y = fmaxf(y, x[j]);
-                        y = warp_max(y);
-                        if (lane == 0 && y > -FLT_MAX) atomicMax(&S.ykey[ss], f2key(y));
-                    }
-                    if (MODE == kCollect) {
-                        const float th = S.cy[ss];
-                        const int c = dir > 0 ? td.r0 + ss : r_end - ss;
-#pragma unroll
-                        for (int j = 0; j < kDiag; ++j) {
-                            const int u = ss + ub + j;
-                            const int q = dir > 0 ? qbase + u : qbase - u;
-                            // upper bound (cov + E) * qn reaches the row's best lower bound
-                            if (q >= 0 && q < N && fmaf(Ef, rc[(j + uu) % kDiag], x[j]) >= th) {
-                                const int at = atomicAdd(p.coll_count, 1);
-                                if (at < p.coll_cap) p.coll[at] = make_int2(c, q);
-                            }
-                        }
-                    }
-                }
-                // slide: slot D-1 of the next step is u = ss + 1 + ub + kDiag - 1
-                const int un = ss + ub + kDiag;
-                ra[uu % kDiag] = S.u.walk.qdf[un];
-                rb[uu % kDiag] = S.u.walk.qdg[un];
-                rc[uu % kDiag] = S.u.walk.qn[un];
+            for (int j = 0; j < kDiag; ++j) {
+                const int rj = (j + uu) % kDiag;
+                cov[j] = fmaf(cr.x, rd[rj].y, cov[j]);
+                cov[j] = fmaf(rd[rj].x, cr.y, cov[j]);
             }
+            if (cr.z != kNoEval) {  // CTA-uniform branch: the row is undecided
+                float x[kDiag];
+                float mx = -FLT_MAX;
+#pragma unroll
+                for (int j = 0; j < kDiag; ++j) {
+                    x[j] = cov[j] * rn[(j + uu) % kDiag];
+                    mx = fmaxf(mx, x[j]);
+                }
+                if (MODE == kPrune && mx > cr.z && cr.w != 0.f) {
+                    // certain kill of the row candidate (FP32 only)
+                    p.alive[dir > 0 ? td.r0 + ss : r_end - ss] = 0;
+                } else if (MODE != kCollect && mx > cr.z) {
+                    // ---- slow path: exact conventions, certain kill, knife edges.
+                    // Only the row candidate is killed (the pair's other end is
+                    // decided by its own row), so a decided row never re-enters.
+                    const int c = dir > 0 ? td.r0 + ss : r_end - ss;
+#pragma unroll
+                    for (int j = 0; j < kDiag; ++j) {
+                        if (!(x[j] > cr.z)) continue;
+                        const int u = ss + ub + j;
+                        const int q = dir > 0 ? qbase + u : qbase - u;
+                        if (q < 0 || q >= N) continue;
+                        const float qn = rn[(j + uu) % kDiag];
+                        if (cr.w == 0.f || qn == 0.f) {
+                            const double d = (cr.w == 0.f && qn == 0.f) ? 0.0 : 2.0 * (double)m;
+                            if (d < p.r_sq) p.alive[c] = 0;
+                            continue;
+                        }
+                        const double corr = (double)x[j] * (double)cr.w;
+                        const double ec = E * (double)cr.w * (double)qn + kSlack;
+                        if (corr - ec > p.thr0) {
+                            p.alive[c] = 0;
+                        } else if (MODE == kPruneTrack && corr + ec >= p.thr0) {
+                            const int at = atomicAdd(p.queue_count, 1);
+                            if (at < p.queue_cap) p.queue[at] = make_int2(c, q);
+                        }
+                    }
+                }
+                if (MODE == kPruneTrack && S.ykey[ss] != 0u) {
+                    // row max of the FP32 route value x = cov*qn over valid q (NaN for
+                    // invalid q is ignored by fmaxf; a constant q contributes exactly
+                    // 0); the tile's error term E*qn_max is folded in at the end
+                    float y = -FLT_MAX;
+#pragma unroll
+                    for (int j = 0; j < kDiag; ++j) y = fmaxf(y, x[j]);
+                    y = warp_max(y);
+                    if (lane == 0 && y > -FLT_MAX) atomicMax(&S.ykey[ss], f2key(y));
+                }
+                if (MODE == kCollect) {
+                    const float th = S.cy[ss];
+                    const int c = dir > 0 ? td.r0 + ss : r_end - ss;
+#pragma unroll
+                    for (int j = 0; j < kDiag; ++j) {
+                        // upper bound (cov + E) * qn reaches the row's best lower bound
+                        // (NaN for an invalid q fails the comparison)
+                        if (fmaf(Ef, rn[(j + uu) % kDiag], x[j]) >= th) {
+                            const int u = ss + ub + j;
+                            const int q = dir > 0 ? qbase + u : qbase - u;
+                            const int at = atomicAdd(p.coll_count, 1);
+                            if (at < p.coll_cap) p.coll[at] = make_int2(c, q);
+                        }
+                    }
+                }
+            }
+            // slide: slot kDiag-1 of step ss+1 is u = ss + 1 + ub + kDiag - 1
+            rd[uu % kDiag] = qdp[ss + kDiag];
+            rn[uu % kDiag] = qnp[ss + kDiag];
         }
     }
 

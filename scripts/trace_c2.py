@@ -14,3 +14,4 @@ t = time.time()
 rep = e.merlin_full(lo, hi)
 print("wall", time.time() - t, file=sys.stderr)
 print(e.counters(), file=sys.stderr)
+e.close()
