@@ -28,10 +28,9 @@ def hexf(s):
 
 
 def series_of(inp):
-    """Regenerates a fixture's input series with the library's host generator."""
-    from paper_2304_01660_b200 import gen_randomwalk
-    assert inp["gen"] == "randomwalk"
-    return gen_randomwalk(inp["n"], inp["seed"])
+    """Regenerates a fixture's input series (the library's generators)."""
+    from paper_2304_01660_b200.datasets import make_series
+    return make_series(inp)
 
 
 @pytest.fixture(scope="session")

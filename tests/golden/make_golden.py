@@ -25,6 +25,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 from oracle.refbind import Ref  # noqa: E402
 
 CONFIGS = {
+    # c3: BASELINE config 3 (ECG-like n=500,000, lengths 64-512); "c3s" is its first
+    # 64 lengths, the parity fixture that fits the build container's CPU budget
+    "c3": (500_000, 1, 64, 512, 1, 512),
+    "c3s": (500_000, 1, 64, 127, 1, 512),
     # name: (n, seed, minL, maxL, top_k, seglen)   (BASELINE.json configs)
     "c1": (10_000, 1, 64, 128, 1, 512),
     "c2": (100_000, 1, 128, 256, 1, 512),
@@ -103,9 +107,14 @@ def small(R):
 
 def big(R, name, workers):
     n, seed, minL, maxL, top_k, seglen = CONFIGS[name]
-    x = R.gen_randomwalk(n, seed)
-    fx = merlin_fixture(R, x, dict(gen="randomwalk", n=n, seed=seed), minL, maxL, top_k, seglen,
-                        workers)
+    if name.startswith("c3"):
+        from paper_2304_01660_b200.datasets import gen_ecg_like
+        x = gen_ecg_like(n, seed)
+        spec = dict(gen="ecg", n=n, seed=seed)
+    else:
+        x = R.gen_randomwalk(n, seed)
+        spec = dict(gen="randomwalk", n=n, seed=seed)
+    fx = merlin_fixture(R, x, spec, minL, maxL, top_k, seglen, workers)
     fx["config"] = name
     with open(os.path.join(HERE, f"{name}.json"), "w") as f:
         json.dump(fx, f, indent=0)
