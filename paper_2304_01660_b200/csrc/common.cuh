@@ -29,6 +29,44 @@ struct TileDesc {
     int seed;  // >= 0: seed row kept resident across lengths (ScanParams::seedqt), else -1
 };
 
+// Tile spaces: how a persistent scan CTA turns a fetched slot index into a tile.
+enum TileSpace : int {
+    kSpaceSeed = 0,    // band 0 at offset kA over aligned L-row blocks, seeded from resident rows
+    kSpaceBlocks = 1,  // band [K0, K0 + nb*kW) over aligned L-row blocks (FP32 / FP64 direct seeds)
+    kSpaceBand = 2,    // band [K0, K0 + nb*kW) over the device-built groups (TryCtl::G)
+    kSpaceFull = 3     // every diagonal |k| >= m of the device-built groups, near-first
+};
+
+// Device-resident control block of one DRAG try: every count the host used to
+// read back between passes lives here, so a whole try is enqueued without a
+// host round trip (kernels gate themselves on these fields).
+struct TryCtl {
+    int alive;      // undecided rows after the latest compaction
+    int prev;       // the count before it (band-pass break rule)
+    int stop;       // band passes with index > stop are skipped (INT_MAX: none yet)
+    int G;          // groups of the current stage (ScanParams::groups)
+    int next;       // persistent-scan slot counter (self-resetting)
+    int ctas_done;  // persistent-scan exit ticket (self-resetting)
+    int queue;      // knife-edge pairs queued
+    int coll;       // near pairs collected
+    int crange[2];  // first / last constant row
+    int sc;         // range-discord survivors (after the knife-edge recheck)
+    int ec;         // rows whose exact nn is computed (MERLIN top-k filter)
+    int passes;     // band passes that ran
+    int span;       // group span of the current stage
+    int cticket;    // compaction: CTA order tickets (self-resetting)
+    int cdone;      // compaction: finished CTAs (self-resetting)
+    int ctotal;     // compaction: total of the latest launch
+    int xdone;      // exact pass: finished CTAs (self-resetting)
+    double lk;      // top-k filter: need_top-th largest nn lower bound
+    double cost[6]; // compaction: grouping cost per span (16..512), self-resetting
+};
+
+// compaction / grouping gates: a band pass index (>= 0: skipped once the band
+// passes stopped before it), or one of these
+constexpr int kGateNone = -1;   // always runs
+constexpr int kGateQueue = -2;  // skipped when no knife edge was queued (or nothing is alive)
+
 enum ScanMode : int {
     kPrune = 0,       // dense band: kill both ends of any pair with d^2 < r^2
     kPruneTrack = 1,  // sparse rows: prune + track a lower bound of each live row's max corr
@@ -56,7 +94,14 @@ struct ScanParams {
     int2* coll;          // kCollect output pairs
     int* coll_count;
     int coll_cap;
-    const TileDesc* tiles;
+    // tile space of this launch (persistent CTAs fetch slots from ctl->next)
+    TryCtl* ctl;
+    const int2* groups;  // kSpaceBand / kSpaceFull: (first, last) row of each group
+    int space;           // TileSpace
+    int pass;            // band pass index (kSpaceBand: skipped when ctl->stop < pass)
+    int K0, nb;          // band: diagonals [K0, K0 + nb*kW) on both sides
+    int L, kA;           // kSpaceSeed / kSpaceBlocks: block rows; kSpaceSeed: band offset
+    int rank, world;     // tiles are dealt cyclically across ranks
     const double* seedqt;  // resident raw dot products QT(i, i+k) of the band-0 tiles (kW per tile)
     unsigned long long* acc;  // accounting: [0] cells walked, [1] cells evaluated, [2] seed dots
 };

@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -106,11 +107,11 @@ struct tsd_ctx {
     DBuf<double> mu, sig, scr_a, scr_b;
     int64_t derived_m = -1;
     DBuf<float> df, dg, nrm;
+    DBuf<int> crange;  // constant-row range of the derived length (k_derive)
 
     // scan state
     DBuf<uint8_t> alive;
     DBuf<int2> queue, coll;
-    DBuf<int> counters;  // [0] queue, [1] coll, [2..3] const range
     DBuf<unsigned> ymax, emax;
     DBuf<double> bnd_lo, bnd_hi;
     // resident band-0 seed rows (length recurrence), valid for length seed_m
@@ -122,19 +123,23 @@ struct tsd_ctx {
     DBuf<unsigned long long> nnkey, acc;  // acc: [0] cells, [1] seeds
     DBuf<int> blk, list;
     DBuf<double> nnout;
-    DBuf<TileDesc> tiles;
-    HBuf<TileDesc> h_tiles;
-    HBuf<int> h_int, h_listbuf;
+    DBuf<int2> groups, slots;  // groups of the current stage; per-span candidate groups
+    DBuf<TryCtl> ctl;  // device-resident control block of the current try
+    DBuf<unsigned long long> lbstat;  // compaction look-back status words
+    unsigned epoch = 0;
+    HBuf<TryCtl> h_ctl;
+    HBuf<int> h_int, h_ex;
     HBuf<unsigned long long> h_acc;
-    HBuf<double> h_dbl;
-    std::vector<int> h_list;
-    int last_queue = 0;
-    double hs_build = 0, hs_group = 0, hs_scan_api = 0, hs_compact = 0, hs_tail = 0;  // debug host timers (ms)
+    HBuf<double> h_nn;
 
     // tuning
     bool debug = std::getenv("TSD_DEBUG") != nullptr;
     int dense_rows = 512;
-    int sparse_rows = 0;  // 0: choose by cost model
+    int sparse_rows = 0;   // 0: choose by cost model (on the device)
+    int band_passes = 40;  // cap on band passes (incl. pass 0) enqueued per try; full rows cover the rest
+    int band_hint = 0;     // adaptive count: passes the previous try needed (0: none yet)
+    float band_keep = 0.85f;  // band loop stops when a pass leaves more than this fraction alive
+    int result_prefix = 1024;  // records copied back with the try's single round trip
     double err_k = 4.0;
 
     // accounting
@@ -195,7 +200,8 @@ struct tsd_ctx {
         df.ensure(N);
         dg.ensure(N);
         nrm.ensure(N);
-        launch_derive(t.p, (int)m, (int)N, mu.p, sig.p, df.p, dg.p, nrm.p, st);
+        crange.ensure(2);
+        launch_derive(t.p, (int)m, (int)N, mu.p, sig.p, df.p, dg.p, nrm.p, crange.p, st);
         ctr.kernel_launches += 1;
         ck(cudaGetLastError(), "derive");
         derived_m = m;
@@ -237,23 +243,25 @@ struct tsd_ctx {
         p.err_k = err_k;
         p.alive = alive.p;
         p.queue = queue.p;
-        p.queue_count = counters.p + 0;
+        p.queue_count = &ctl.p->queue;
         p.queue_cap = kQueueCap;
         p.ymax = ymax.p;
         p.emax = emax.p;
         p.seedqt = seedqt.p;
         p.ythr = ythr.p;
         p.coll = coll.p;
-        p.coll_count = counters.p + 1;
+        p.coll_count = &ctl.p->coll;
         p.coll_cap = kCollCap;
-        p.tiles = tiles.p;
+        p.ctl = ctl.p;
+        p.groups = groups.p;
+        p.rank = rank;
+        p.world = world;
         p.acc = acc.p;
         return p;
     }
 
-    // Tile lists of one pardrag call are appended to a pinned arena and its
-    // device mirror (uploads are async; the arena resets when the call starts).
-    size_t tile_off = 0;
+    // scan launches of one try are bracketed by pooled events (harvested after
+    // the try's single sync)
     struct EvPair {
         cudaEvent_t a, b;
         int mode;
@@ -261,43 +269,7 @@ struct tsd_ctx {
     std::vector<EvPair> ev_pool;
     size_t ev_used = 0;
 
-    void arena_reset() {
-        tile_off = 0;
-        ev_used = 0;
-    }
-
-    void run_scan(int mode, const std::vector<TileDesc>& tl, ScanParams p) {
-        const double t_in = now_ms();
-        struct Acc {
-            double& a;
-            double t0;
-            ~Acc() { a += now_ms() - t0; }
-        } acc_guard{hs_scan_api, t_in};
-        // shard tiles cyclically across ranks: every rank sweeps a disjoint set
-        std::vector<TileDesc> mine;
-        const std::vector<TileDesc>* use = &tl;
-        if (world > 1) {
-            for (size_t i = rank; i < tl.size(); i += world) mine.push_back(tl[i]);
-            use = &mine;
-        }
-        const size_t nt = use->size();
-        if (nt == 0) return;
-        if (tile_off + nt > h_tiles.cap || tile_off + nt > tiles.cap) {
-            // growing the arena: in-flight uploads must finish first
-            sync();
-            const size_t want = std::max<size_t>(2 * (tile_off + nt), 1 << 16);
-            std::vector<TileDesc> keep(h_tiles.p, h_tiles.p + tile_off);
-            h_tiles.release();
-            h_tiles.ensure(want);
-            tiles.ensure(want);
-            if (tile_off) std::memcpy(h_tiles.p, keep.data(), tile_off * sizeof(TileDesc));
-        }
-        TileDesc* hp = h_tiles.p + tile_off;
-        TileDesc* dp = tiles.p + tile_off;
-        tile_off += nt;
-        std::memcpy(hp, use->data(), nt * sizeof(TileDesc));
-        ck(cudaMemcpyAsync(dp, hp, nt * sizeof(TileDesc), cudaMemcpyHostToDevice, st), "tiles H2D");
-        p.tiles = dp;
+    void scan(int mode, const ScanParams& p) {
         if (ev_used == ev_pool.size()) {
             EvPair e{};
             ck(cudaEventCreate(&e.a), "event");
@@ -307,7 +279,7 @@ struct tsd_ctx {
         EvPair& e = ev_pool[ev_used++];
         e.mode = mode;
         ck(cudaEventRecord(e.a, st), "event");
-        launch_scan(mode, (int)nt, p, st);
+        launch_scan(mode, p, st);
         ck(cudaGetLastError(), "scan launch");
         ck(cudaEventRecord(e.b, st), "event");
         ctr.scan_launches += 1;
@@ -327,157 +299,39 @@ struct tsd_ctx {
         ev_used = 0;
     }
 
-    void recheck(int64_t m, double r_sq) {
-        launch_ref_pairs(0, t.p, (int)m, queue.p, counters.p + 0, kQueueCap, r_sq, alive.p, nnkey.p,
-                         kQueueCap, st);
-        ck(cudaGetLastError(), "recheck");
+    // alive flags -> sorted list, break rule (band passes), groups of the list
+    void compact(int N, int gate, int64_t m) {
+        const size_t nb = (size_t)compact_blocks(N);
+        if (lbstat.cap < nb) {
+            lbstat.ensure(nb);
+            ck(cudaMemsetAsync(lbstat.p, 0, nb * sizeof(unsigned long long), st), "memset");
+            epoch = 0;
+        }
+        if (++epoch >= (1u << 30)) {
+            ck(cudaMemsetAsync(lbstat.p, 0, lbstat.cap * sizeof(unsigned long long), st), "memset");
+            epoch = 1;
+        }
+        slots.ensure(group_slots(N));
+        launch_compact_group(alive.p, N, list.p, lbstat.p, epoch, ctl.p, gate, groups.p, slots.p, (int)m,
+                             sparse_rows, band_keep, st);
+        ck(cudaGetLastError(), "compact");
         ctr.kernel_launches += 1;
     }
 
-    // Count of set flags in alive[0..N) with one host round trip; with
-    // list_bound > 0 also the ordered list (list_bound must be >= the count,
-    // e.g. the previous count: flags only ever clear).
-    int compact_alive(int N, int list_bound) {
-        const double t_in = now_ms();
-        const double w_in = ctr.host_wait_ms;
-        struct Acc {
-            tsd_ctx* c;
-            double t0, w0;
-            ~Acc() { c->hs_compact += (now_ms() - t0) - (c->ctr.host_wait_ms - w0); }
-        } acc_guard{this, t_in, w_in};
-        const int nb = compact_blocks(N);
-        blk.ensure(nb + 1);
-        list.ensure(N);
-        launch_compact(alive.p, N, blk.p, list.p, st);
-        ctr.kernel_launches += 3;
-        ck(cudaGetLastError(), "compact");
-        ck(cudaMemcpyAsync(h_int.p, blk.p + nb, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
-        ck(cudaMemcpyAsync(h_int.p + 1, counters.p, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
-        ck(cudaMemcpyAsync(h_acc.p, acc.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "D2H");
-        // speculative list copy: flags only clear, and after the first band pass
-        // few rows remain, so copy a bounded prefix and fetch the rest only if needed
-        const int spec = list_bound > 0 ? std::min(list_bound, std::max(65536, N / 16)) : 0;
-        if (spec > 0) {
-            h_listbuf.ensure(N);
-            ck(cudaMemcpyAsync(h_listbuf.p, list.p, (size_t)spec * sizeof(int), cudaMemcpyDeviceToHost, st),
-               "list D2H");
-        }
+    // debug trace: one host round trip per stage (TSD_DEBUG only)
+    void trace(const char* what, int64_t m, double r_sq, int pass) {
+        if (!debug) return;
+        ck(cudaMemcpyAsync(h_ctl.p, ctl.p, sizeof(TryCtl), cudaMemcpyDeviceToHost, st), "D2H");
         sync();
-        const int cnt = h_int.p[0];
-        last_queue = h_int.p[1];
-        if (list_bound > 0) {
-            if (cnt > list_bound) fail(TSD_ERUNTIME, "internal: alive count grew");
-            if (cnt > spec) {
-                ck(cudaMemcpyAsync(h_listbuf.p + spec, list.p + spec, (size_t)(cnt - spec) * sizeof(int),
-                                   cudaMemcpyDeviceToHost, st),
-                   "list D2H");
-                sync();
-            }
-            h_list.assign(h_listbuf.p, h_listbuf.p + cnt);
-        }
-        return cnt;
-    }
-
-    int read_counter(int idx) {
-        h_int.ensure(4);
-        ck(cudaMemcpyAsync(h_int.p, counters.p + idx, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
-        sync();
-        return h_int.p[0];
-    }
-
-    // group sorted row indices into spans of at most `span` rows
-    static void group_rows(const std::vector<int>& lst, int span, std::vector<int2>& groups) {
-        groups.clear();
-        auto it = lst.begin();
-        while (it != lst.end()) {
-            const int a = *it;
-            auto nx = std::lower_bound(it, lst.end(), a + span);
-            groups.push_back(make_int2(a, *(nx - 1)));
-            it = nx;
-        }
-    }
-
-    // span (max rows per group) minimising ~sum over groups of (2m seed work + 3 per
-    // walked row) per diagonal; groups are counted by galloping, not built
-    int choose_span(const std::vector<int>& lst, int64_t m) {
-        const double t_in = now_ms();
-        struct Acc {
-            double& a;
-            double t0;
-            ~Acc() { a += now_ms() - t0; }
-        } acc_guard{hs_group, t_in};
-        if (sparse_rows > 0) return sparse_rows;
-        // dense lists (>= 1 row in 64 undecided): whole 512-row blocks are cheapest
-        if (!lst.empty() && (long long)lst.size() * 64 >= (long long)(lst.back() - lst.front() + 1)) return 512;
-        double best = 1e300;
-        int best_span = 64;
-        for (int span : {16, 32, 64, 128, 256, 512}) {
-            double cost = 0.0;
-            auto it = lst.begin();
-            while (it != lst.end()) {
-                const int a = *it;
-                auto nx = std::lower_bound(it, lst.end(), a + span);
-                cost += 2.0 * (double)m + 3.0 * (double)(*(nx - 1) - a + 1 + kDiag);
-                it = nx;
-                if (cost >= best) break;
-            }
-            if (cost < best) {
-                best = cost;
-                best_span = span;
-            }
-        }
-        return best_span;
-    }
-
-    // diagonals k in [K0, K0 + nb*kW) right of each group's rows and the mirror
-    // range left of them, band-major so near diagonals run first
-    void band_tiles(const std::vector<int2>& groups, long long K0, long long nb, int N,
-                    std::vector<TileDesc>& out) {
-        out.clear();
-        for (long long b = 0; b < nb; ++b) {
-            const long long k0 = K0 + b * kW;
-            for (const auto& g : groups) {
-                const int a = g.x, rows = g.y - g.x + 1;
-                if (a + k0 < N) out.push_back(TileDesc{a, rows, (int)k0, +1, -1});
-                const long long khi = -k0;  // tile covers [khi - kW + 1, khi]
-                if (g.y + khi >= 0) out.push_back(TileDesc{a, rows, (int)(khi - kW + 1), -1, -1});
-            }
-        }
-    }
-
-    void full_row_tiles(const std::vector<int2>& groups, int64_t m, int N, std::vector<TileDesc>& out) {
-        const double t_in = now_ms();
-        struct Acc {
-            double& a;
-            double t0;
-            ~Acc() { a += now_ms() - t0; }
-        } acc_guard{hs_build, t_in};
-        out.clear();
-        std::vector<int> npos(groups.size()), nneg(groups.size());
-        int maxc = 0;
-        for (size_t g = 0; g < groups.size(); ++g) {
-            const int a = groups[g].x, b = groups[g].y;
-            const long long pos_span = (long long)N - a - m;  // k in [m, N-1-a]
-            npos[g] = pos_span > 0 ? (int)((pos_span + kW - 1) / kW) : 0;
-            const long long neg_span = (long long)b - m + 1;  // k in [-b, -m]
-            nneg[g] = neg_span > 0 ? (int)((neg_span + kW - 1) / kW) : 0;
-            maxc = std::max(maxc, std::max(npos[g], nneg[g]));
-        }
-        for (int i = 0; i < maxc; ++i) {
-            for (size_t g = 0; g < groups.size(); ++g) {
-                const int a = groups[g].x, b = groups[g].y;
-                const int rows = b - a + 1;
-                if (i < npos[g]) out.push_back(TileDesc{a, rows, (int)m + i * kW, +1, -1});
-                if (i < nneg[g]) out.push_back(TileDesc{a, rows, -(int)m - (i + 1) * kW + 1, -1, -1});
-            }
-        }
+        const TryCtl& c = *h_ctl.p;
+        fprintf(stderr, "[tsd] m=%lld r2=%.6g %s pass=%d groups=%d span=%d alive=%d stop=%d queue=%d\n",
+                (long long)m, r_sq, what, pass, c.G, c.span, c.alive, c.stop == INT_MAX ? -1 : c.stop, c.queue);
     }
 
     void ensure_scan_buffers(int N) {
         alive.ensure(N);
         queue.ensure(kQueueCap);
         coll.ensure(kCollCap);
-        counters.ensure(8);
         ymax.ensure(N);
         emax.ensure(N);
         bnd_lo.ensure(N);
@@ -487,10 +341,20 @@ struct tsd_ctx {
         nnkey.ensure(N);
         acc.ensure(3);
         nnout.ensure(N);
+        list.ensure(N);
+        groups.ensure(N);
+        if (!ctl.p) {
+            ctl.ensure(1);
+            ck(cudaMemsetAsync(ctl.p, 0, sizeof(TryCtl), st), "memset");  // next / ctas_done start at 0
+        }
+        h_ctl.ensure(1);
+        h_int.ensure(8);
+        h_acc.ensure(4);
+        h_ex.ensure(result_prefix);
+        h_nn.ensure(result_prefix);
     }
 
     // fold the device work counters of the current call into ctr
-    // (h_acc is refreshed by every compact_alive and by the final copy of a call)
     void harvest(int64_t m) {
         const unsigned long long* hacc = h_acc.p;
         ctr.cells += hacc[0];
@@ -504,7 +368,12 @@ struct tsd_ctx {
     // every index.
     // need_top > 0 (MERLIN): only the records that can be in the top need_top
     // get exact distances; last_count still receives the full survivor count.
+    //
+    // The whole try is enqueued on the stream without a host round trip: every
+    // count a later stage needs lives in the device control block (TryCtl) and
+    // the kernels gate themselves on it.  The host reads back once, at the end.
     int last_count = 0;
+    int enq_passes = 0;
     std::vector<tsd_record> pardrag_core(int64_t m, double r_sq, double* all_nn = nullptr,
                                          int64_t need_top = 0) {
         const double t_start = now_ms();
@@ -516,157 +385,134 @@ struct tsd_ctx {
         const int N = (int)(n - m + 1);
         derive(m);
         ensure_scan_buffers(N);
-        h_int.ensure(8);
-        h_acc.ensure(4);
-        arena_reset();
+        ev_used = 0;
         ctr.pardrag_calls += 1;
-        ck(cudaMemsetAsync(counters.p, 0, 2 * sizeof(int), st), "memset");
-        ck(cudaMemsetAsync(acc.p, 0, 3 * sizeof(unsigned long long), st), "memset");
-        launch_fill_u8(alive.p, N, 1, st);
+        TryCtl* C = ctl.p;
+        launch_try_init(alive.p, ymax.p, emax.p, ythr.p, N, C, acc.p, st);
+        ck(cudaGetLastError(), "try init");
         ctr.kernel_launches += 1;
         const ScanParams P = params(m, r_sq);
-        std::vector<TileDesc> tl;
-        std::vector<int2> groups;
         std::vector<tsd_record> out;
 
-        // ---- band passes (PD3 selection): diagonals |k| in [K0, K0 + B) on both
-        // sides of every undecided row; only certain FP32 kills, no knife-edge
-        // work.  Pass 0 tiles all rows in blocks; later passes tile groups of the
-        // remaining rows (span chosen by the seed/walk cost model).  One host
-        // round trip per pass (count + ordered list of undecided rows).
-        int alive_cnt = N;
+        // ---- band passes (PD3 selection): diagonals |k| in [K0, K0 + nb*kW) on
+        // both sides of every undecided row; only certain FP32 kills.  Pass 0
+        // tiles all rows in aligned blocks; later passes tile the device-built
+        // groups of the remaining rows.  The break rule (nothing / few left, or
+        // < 15% killed) is applied on the device; passes after it are no-ops.
         if (r_sq > 0.0) {
             long long K0 = m;
             const long long k_max = (long long)N - 1;
-            for (int pass = 0; K0 <= k_max; ++pass) {
-                const long long nb = std::min<long long>(1ll << std::min(pass, 5), (k_max - K0 + kW) / kW);
+            // passes after the device-side break rule are no-ops but still cost
+            // their launches: enqueue what the previous try needed (consecutive
+            // lengths behave alike), growing while the cap is what stopped it
+            const int want = band_hint > 0 ? std::min(band_hint, band_passes) : std::min(4, band_passes);
+            enq_passes = 0;
+            for (int pass = 0; K0 <= k_max && pass < want; ++pass) {
+                ++enq_passes;
+                ScanParams q = P;
+                q.pass = pass;
                 if (pass == 0 && seed_m == m && seed_L == dense_rows) {
                     // band 0 at the fixed offset kA (>= m for every length of the run)
                     // seeded from the resident rows: no direct dot products
-                    tl.clear();
-                    const long long kA = seed_kA;
-                    for (int j = 0; (long long)j * seed_L < N; ++j) {
-                        const int r0 = j * seed_L, rows = std::min(N, r0 + seed_L) - r0;
-                        if (r0 + kA < N) tl.push_back(TileDesc{r0, rows, (int)kA, +1, 2 * j});
-                        if (r0 + rows - 1 - kA >= 0)
-                            tl.push_back(TileDesc{r0, rows, (int)(-kA - kW + 1), -1,
-                                                  rows == seed_L ? 2 * j + 1 : -1});
-                    }
-                    K0 = kA + kW;
+                    q.space = kSpaceSeed;
+                    q.L = seed_L;
+                    q.kA = seed_kA;
+                    K0 = (long long)seed_kA + kW;
                 } else {
+                    const long long nb =
+                        std::min<long long>(1ll << std::min(pass, 5), (k_max - K0 + kW) / kW);
                     if (pass == 0) {
-                        groups.clear();
-                        for (int r0 = 0; r0 < N; r0 += dense_rows)
-                            groups.push_back(make_int2(r0, std::min(N, r0 + dense_rows) - 1));
+                        q.space = kSpaceBlocks;
+                        q.L = dense_rows;
                     } else {
-                        group_rows(h_list, choose_span(h_list, m), groups);
+                        q.space = kSpaceBand;  // groups built by the previous compaction
                     }
-                    band_tiles(groups, K0, nb, N, tl);
+                    q.K0 = (int)K0;
+                    q.nb = (int)nb;
                     K0 += nb * kW;
                 }
-                run_scan(kPrune, tl, P);
+                scan(kPrune, q);
                 allreduce_min_u8(alive.p, N);
-                const int prev = alive_cnt;
-                alive_cnt = compact_alive(N, prev);
-                if (debug)
-                    fprintf(stderr, "[tsd] m=%lld r2=%.6g pass=%d groups=%zu tiles=%zu K=%lld alive=%d\n",
-                            (long long)m, r_sq, pass, groups.size(), tl.size(), K0, alive_cnt);
-                if (alive_cnt == 0) break;
-                if (alive_cnt <= std::max(64, N / 4096)) break;
-                if ((double)alive_cnt > 0.85 * (double)prev) break;  // bands stopped paying
+                compact(N, pass, m);
+                trace("band", m, r_sq, pass);
             }
         } else {
-            compact_alive(N, N);
+            compact(N, kGateNone, m);
         }
-        last_count = 0;
-        if (alive_cnt == 0) return finish(m, out);
 
         // ---- full rows (PD3 refinement) for every remaining candidate: prune,
         // queue knife edges, and track a lower bound of each row's best corr
-        group_rows(h_list, choose_span(h_list, m), groups);
-        full_row_tiles(groups, m, N, tl);
-        ck(cudaMemsetAsync(ymax.p, 0, (size_t)N * sizeof(unsigned), st), "memset");
-        ck(cudaMemsetAsync(emax.p, 0, (size_t)N * sizeof(unsigned), st), "memset");
-        run_scan(kPruneTrack, tl, P);
+        // (groups of the list come from the last compaction)
+        ScanParams q = P;
+        q.space = kSpaceFull;
+        scan(kPruneTrack, q);
         allreduce_min_u8(alive.p, N);
         allreduce_max_u32(ymax.p, N);
-        int sc = compact_alive(N, alive_cnt);
-        if (debug)
-            fprintf(stderr, "[tsd] m=%lld full-rows groups=%zu tiles=%zu survivors=%d queue=%d\n",
-                    (long long)m, groups.size(), tl.size(), sc, last_queue);
-        if (last_queue > kQueueCap) fail(TSD_ERUNTIME, "knife-edge queue overflow (degenerate series?)");
-        ctr.rechecks += (unsigned long long)last_queue;
-        if (last_queue > 0 && sc > 0) {
-            // knife edges: the reference's FP64 distance decides (pardrag.cpp:255)
-            launch_ref_pairs(0, t.p, (int)m, queue.p, counters.p + 0, kQueueCap, r_sq, alive.p, nnkey.p,
-                             last_queue, st);
-            ck(cudaGetLastError(), "recheck");
-            ctr.kernel_launches += 1;
-            allreduce_min_u8(alive.p, N);
-            sc = compact_alive(N, sc);
-        }
-        last_count = sc;
-        if (sc == 0) return finish(m, out);
+        allreduce_max_u32(emax.p, N);
+        // knife edges: the reference's FP64 distance decides (pardrag.cpp:255)
+        launch_ref_pairs(0, t.p, (int)m, queue.p, &C->queue, kQueueCap, r_sq, alive.p, nnkey.p, C, nullptr,
+                         nullptr, st);
+        ck(cudaGetLastError(), "recheck");
+        allreduce_min_u8(alive.p, N);
 
-        // ---- survivors: exact nearest neighbours (pardrag.cpp:378-416)
-        last_count = sc;
-        h_int.p[2] = N;
-        h_int.p[3] = -1;
-        ck(cudaMemcpyAsync(counters.p + 2, h_int.p + 2, 2 * sizeof(int), cudaMemcpyHostToDevice, st), "H2D");
-        launch_const_range(nrm.p, N, counters.p + 2, st);
-        ctr.kernel_launches += 1;
-        const int* ex_list = list.p;  // rows whose exact nn is computed
-        std::vector<int> cand_h;
-        const std::vector<int>* ex_h = &h_list;
-        if (need_top > 0 && sc > need_top) {
-            // MERLIN keeps only the top need_top records: exact distances only for
-            // survivors whose nn interval reaches the need_top-th largest lower bound
-            launch_nn_bounds(list.p, sc, ymax.p, emax.p, nrm.p, counters.p + 2, N, (int)m, bnd_lo.p, bnd_hi.p, st);
-            ctr.kernel_launches += 1;
-            h_dbl.ensure(2 * (size_t)sc);
-            ck(cudaMemcpyAsync(h_dbl.p, bnd_lo.p, sc * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
-            ck(cudaMemcpyAsync(h_dbl.p + sc, bnd_hi.p, sc * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
-            sync();
-            std::vector<double> lo(h_dbl.p, h_dbl.p + sc);
-            std::nth_element(lo.begin(), lo.begin() + (need_top - 1), lo.end(), std::greater<double>());
-            const double lk = lo[need_top - 1];
-            for (int e = 0; e < sc; ++e)
-                if (h_dbl.p[sc + e] >= lk) cand_h.push_back(h_list[e]);
-            h_listbuf.ensure(cand_h.size());
-            std::memcpy(h_listbuf.p, cand_h.data(), cand_h.size() * sizeof(int));
-            ck(cudaMemcpyAsync(cand.p, h_listbuf.p, cand_h.size() * sizeof(int), cudaMemcpyHostToDevice, st),
-               "H2D");
-            ex_list = cand.p;
-            ex_h = &cand_h;
-        }
-        const int ec = (int)ex_h->size();
-        launch_prep_survivors(ex_list, ec, ymax.p, emax.p, ythr.p, nnkey.p, st);
-        ctr.kernel_launches += 1;
-        group_rows(*ex_h, choose_span(*ex_h, m), groups);
-        full_row_tiles(groups, m, N, tl);
-        ck(cudaMemsetAsync(counters.p + 1, 0, sizeof(int), st), "memset");
-        run_scan(kCollect, tl, P);
-        launch_ref_pairs(1, t.p, (int)m, coll.p, counters.p + 1, kCollCap, r_sq, alive.p, nnkey.p,
-                         148 * 32, st);
+        // ---- survivors: exact nearest neighbours (pardrag.cpp:378-416).  One
+        // CTA filters the list to the survivors, applies the MERLIN top-k
+        // filter, resets their keys and groups them.
+        launch_survivors(list.p, alive.p, C, ymax.p, emax.p, nrm.p, crange.p, N, (int)m, (int)need_top, bnd_lo.p,
+                         bnd_hi.p, cand.p, ythr.p, nnkey.p, groups.p, sparse_rows, st);
+        ck(cudaGetLastError(), "survivors");
+        const int* ex = cand.p;  // rows whose exact nn is computed (count: C->ec)
+        scan(kCollect, q);
+        launch_ref_pairs(1, t.p, (int)m, coll.p, &C->coll, kCollCap, r_sq, alive.p, nnkey.p, C,
+                         world == 1 ? ex : nullptr, nnout.p, st);
         ck(cudaGetLastError(), "exact");
-        // constant rows follow the constant conventions
-        launch_const_nn(ex_list, ec, nrm.p, counters.p + 2, N, (int)m, nnkey.p, st);
-        allreduce_min_u64(nnkey.p, N);
-        launch_gather_nn(ex_list, ec, nnkey.p, nnout.p, st);
-        ck(cudaGetLastError(), "gather");
-        ctr.kernel_launches += 3;  // exact pairs, const nn, gather
-        h_dbl.ensure(ec);
-        ck(cudaMemcpyAsync(h_dbl.p, nnout.p, ec * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
-        ck(cudaMemcpyAsync(h_int.p, counters.p + 1, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+        if (world > 1) {
+            allreduce_min_u64(nnkey.p, N);
+            launch_gather_nn(ex, &C->ec, nnkey.p, nnout.p, st);
+            ck(cudaGetLastError(), "gather");
+            ctr.kernel_launches += 1;
+        }
+        ctr.kernel_launches += 3;  // recheck, survivors, exact pairs
+
+        // ---- the try's single round trip: control block, counters and a
+        // bounded prefix of the records (the rest only if there are more)
+        const int pf = std::min(N, result_prefix);
+        ck(cudaMemcpyAsync(h_ctl.p, C, sizeof(TryCtl), cudaMemcpyDeviceToHost, st), "D2H");
         ck(cudaMemcpyAsync(h_acc.p, acc.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaMemcpyAsync(h_ex.p, ex, pf * sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaMemcpyAsync(h_nn.p, nnout.p, pf * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
         sync();
-        const int cc = h_int.p[0];
-        if (cc > kCollCap) fail(TSD_ERUNTIME, "near-pair buffer overflow (degenerate series?)");
-        ctr.exact_pairs += (unsigned long long)cc;
+        const TryCtl hc = *h_ctl.p;
+        if (hc.queue > kQueueCap) fail(TSD_ERUNTIME, "knife-edge queue overflow (degenerate series?)");
+        if (hc.coll > kCollCap) fail(TSD_ERUNTIME, "near-pair buffer overflow (degenerate series?)");
+        ctr.rechecks += (unsigned long long)hc.queue;
+        ctr.exact_pairs += (unsigned long long)hc.coll;
+        last_count = hc.sc;
+        if (r_sq > 0.0 && enq_passes > 0) {
+            if (hc.stop == INT_MAX) band_hint = enq_passes + 2;  // cut off by the count: allow more
+            else band_hint = std::max(1, hc.passes);             // the break rule fired at pass passes-1
+        }
+        const int ec = hc.ec;
+        if (debug)
+            fprintf(stderr, "[tsd] m=%lld r2=%.6g done passes=%d survivors=%d exact=%d queue=%d coll=%d\n",
+                    (long long)m, r_sq, hc.passes, hc.sc, ec, hc.queue, hc.coll);
+        const int* hex = h_ex.p;
+        const double* hnn = h_nn.p;
+        std::vector<int> ex_big;
+        std::vector<double> nn_big;
+        if (ec > pf) {
+            ex_big.resize(ec);
+            nn_big.resize(ec);
+            ck(cudaMemcpyAsync(ex_big.data(), ex, ec * sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaMemcpyAsync(nn_big.data(), nnout.p, ec * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+            sync();
+            hex = ex_big.data();
+            hnn = nn_big.data();
+        }
         out.reserve(ec);
         for (int e = 0; e < ec; ++e) {
-            const int c = (*ex_h)[e];
-            const double d = h_dbl.p[e];
+            const int c = hex[e];
+            const double d = hnn[e];
             if (all_nn) all_nn[c] = d;
             out.push_back(tsd_record{(int64_t)c + 1, d, std::sqrt(d)});
         }
@@ -801,8 +647,7 @@ int tsd_ctx_create(int device, tsd_ctx** out) {
 void tsd_ctx_destroy(tsd_ctx* c) {
     if (!c) return;
     if (c->debug)
-        fprintf(stderr, "[tsd] host ms: build %.1f group %.1f scan_api %.1f compact %.1f | wall %.1f wait %.1f\n",
-                c->hs_build, c->hs_group, c->hs_scan_api, c->hs_compact, c->ctr.host_wall_ms, c->ctr.host_wait_ms);
+        fprintf(stderr, "[tsd] host ms: wall %.1f wait %.1f\n", c->ctr.host_wall_ms, c->ctr.host_wait_ms);
     cudaSetDevice(c->device);
     if (c->comm) nccl_destroy(c->comm);
     c->t.release();
@@ -813,10 +658,11 @@ void tsd_ctx_destroy(tsd_ctx* c) {
     c->df.release();
     c->dg.release();
     c->nrm.release();
+    c->crange.release();
+    c->lbstat.release();
     c->alive.release();
     c->queue.release();
     c->coll.release();
-    c->counters.release();
     c->ymax.release();
     c->emax.release();
     c->seedqt.release();
@@ -829,12 +675,14 @@ void tsd_ctx_destroy(tsd_ctx* c) {
     c->blk.release();
     c->list.release();
     c->nnout.release();
-    c->tiles.release();
-    c->h_tiles.release();
+    c->groups.release();
+    c->slots.release();
+    c->ctl.release();
+    c->h_ctl.release();
+    c->h_ex.release();
+    c->h_nn.release();
     c->h_int.release();
-    c->h_listbuf.release();
     c->h_acc.release();
-    c->h_dbl.release();
     for (auto& e : c->ev_pool) {
         cudaEventDestroy(e.a);
         cudaEventDestroy(e.b);
@@ -1088,6 +936,9 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         if (k == "dense_rows") c->dense_rows = std::max(16, std::min(kMaxRows, (int)v));
         else if (k == "sparse_rows") c->sparse_rows = std::max(0, std::min(kMaxRows, (int)v));
         else if (k == "err_scale") c->err_k = v;
+        else if (k == "band_keep") c->band_keep = (float)std::max(0.0, std::min(1.0, v));
+        else if (k == "band_passes") c->band_passes = std::max(1, std::min(64, (int)v));
+        else if (k == "result_prefix") c->result_prefix = std::max(16, std::min(1 << 20, (int)v));
         else fail(TSD_EINVAL, "unknown parameter " + k);
     });
 }

@@ -12,27 +12,34 @@ void launch_init_stats(const double* t, int n, int m, double* mu, double* sig, d
                        double* scratch_b, cudaStream_t st);
 void launch_advance_stats(const double* t, int n, int m, double* mu, double* sig, cudaStream_t st);
 void launch_derive(const double* t, int m, int cnt, const double* mu, const double* sig, float* df,
-                   float* dg, float* nrm, cudaStream_t st);
+                   float* dg, float* nrm, int* crange, cudaStream_t st);
 
 size_t scan_smem_bytes();
 void scan_configure();
-void launch_scan(int mode, int ntiles, const ScanParams& p, cudaStream_t st);
+// persistent tile scan over the launch's tile space (ScanParams::space)
+void launch_scan(int mode, const ScanParams& p, cudaStream_t st);
+// mode 0: knife-edge recheck; mode 1: exact nn (ex != nullptr: the last CTA also
+// gathers nnout[e] = nn(ex[e]) for e < ctl->ec — single rank only)
 void launch_ref_pairs(int mode, const double* t, int m, const int2* pairs, const int* count, int cap,
-                      double r_sq, uint8_t* alive, unsigned long long* nnkey, int max_pairs,
-                      cudaStream_t st);
-void launch_fill_u8(uint8_t* a, int n, uint8_t v, cudaStream_t st);
+                      double r_sq, uint8_t* alive, unsigned long long* nnkey, TryCtl* ctl, const int* ex,
+                      double* nnout, cudaStream_t st);
+void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const unsigned* ymax,
+                      const unsigned* emax, const float* nrm, const int* crange, int N, int m, int need,
+                      double* lo, double* hi, int* cand, float* ythr, unsigned long long* nnkey, int2* groups,
+                      int fixed_span, cudaStream_t st);
+void launch_try_init(uint8_t* alive, unsigned* ymax, unsigned* emax, float* ythr, int N, TryCtl* ctl,
+                     unsigned long long* acc, cudaStream_t st);
 int compact_blocks(int n);
-void launch_compact(const uint8_t* a, int n, int* blk, int* out, cudaStream_t st);
-void launch_prep_survivors(const int* list, int cnt, const unsigned* ymax, const unsigned* emax, float* ythr,
-                           unsigned long long* nnkey, cudaStream_t st);
-void launch_nn_bounds(const int* list, int cnt, const unsigned* ymax, const unsigned* emax, const float* nrm,
-                      const int* const_range, int N, int m, double* lo, double* hi, cudaStream_t st);
+// gate: band pass index (>= 0), kGateNone or kGateQueue (common.cuh)
+// compaction + break rule + grouping in one kernel (status: >= compact_blocks(n)
+// words; slots: group_slots(n) entries)
+void launch_compact_group(const uint8_t* a, int n, int* out, unsigned long long* status, unsigned epoch,
+                          TryCtl* ctl, int gate, int2* groups, int2* slots, int m, int fixed_span, float band_keep,
+                          cudaStream_t st);
+int group_slots(int n);
 void launch_seed_init(const double* t, int n, int m, int L, int kA, int nb, double* qt, cudaStream_t st);
 void launch_seed_advance(const double* t, int n, int m, int L, int kA, int nb, double* qt, cudaStream_t st);
-void launch_const_range(const float* nrm, int N, int* out, cudaStream_t st);
-void launch_const_nn(const int* list, int cnt, const float* nrm, const int* const_range, int N, int m,
-                     unsigned long long* nnkey, cudaStream_t st);
-void launch_gather_nn(const int* list, int cnt, const unsigned long long* nnkey, double* out,
+void launch_gather_nn(const int* list, const int* cnt, const unsigned long long* nnkey, double* out,
                       cudaStream_t st);
 
 }  // namespace tsd

@@ -23,6 +23,7 @@
 // sequential sums stay sequential (lane 0), only the element-wise z-normalised
 // terms are computed in parallel.
 #include <float.h>
+#include <limits.h>
 
 #include "common.cuh"
 #include "engine_internal.h"
@@ -65,13 +66,153 @@ __device__ __forceinline__ float warp_max(float v) {
     return v;
 }
 
+// Number of tile slots of a launch's tile space (device-side: the group count
+// of kSpaceBand / kSpaceFull is only known on the device).
+__device__ __forceinline__ long long tile_slots(const ScanParams& p) {
+    const TryCtl* ctl = p.ctl;
+    switch (p.space) {
+        case kSpaceSeed: return 2ll * ((p.N + p.L - 1) / p.L);
+        case kSpaceBlocks: return 2ll * p.nb * ((p.N + p.L - 1) / p.L);
+        case kSpaceBand: return ctl->stop < p.pass ? 0 : 2ll * p.nb * ctl->G;
+        default: {  // full rows: the farthest group needs ceil((N - m) / kW) tiles a side
+            const long long maxc = ((long long)p.N - p.m + kW - 1) / kW;
+            return maxc > 0 ? 2ll * maxc * ctl->G : 0;
+        }
+    }
+}
+
+// Slot -> tile.  Band spaces are band-major (near bands first), full rows are
+// distance-major across groups (near tiles of every group first), so kills
+// from near diagonals land before the far tiles are fetched.
+__device__ __forceinline__ bool tile_decode(const ScanParams& p, long long t, TileDesc& td) {
+    const int N = p.N;
+    const int side = (int)(t & 1);
+    int a, e;
+    long long G, k0;
+    if (p.space == kSpaceSeed) {
+        const int j = (int)(t >> 1);
+        a = j * p.L;
+        e = min(N, a + p.L) - 1;
+        td.r0 = a;
+        td.rows = e - a + 1;
+        if (side == 0) {
+            if ((long long)a + p.kA >= N) return false;
+            td.k0 = p.kA;
+            td.dir = +1;
+            td.seed = 2 * j;
+        } else {
+            if ((long long)e - p.kA < 0) return false;
+            td.k0 = -p.kA - kW + 1;
+            td.dir = -1;
+            td.seed = td.rows == p.L ? 2 * j + 1 : -1;
+        }
+        return true;
+    }
+    td.seed = -1;
+    if (p.space == kSpaceBlocks) {
+        G = (N + p.L - 1) / p.L;
+        const long long b = t / (2 * G);
+        const int g = (int)((t >> 1) % G);
+        a = g * p.L;
+        e = min(N, a + p.L) - 1;
+        k0 = (long long)p.K0 + b * kW;
+    } else if (p.space == kSpaceBand) {
+        G = p.ctl->G;
+        const long long b = t / (2 * G);
+        const int2 gr = p.groups[(t >> 1) % G];
+        a = gr.x;
+        e = gr.y;
+        k0 = (long long)p.K0 + b * kW;
+    } else {
+        G = p.ctl->G;
+        const long long i = t / (2 * G);
+        const int2 gr = p.groups[(t >> 1) % G];
+        a = gr.x;
+        e = gr.y;
+        td.r0 = a;
+        td.rows = e - a + 1;
+        if (side == 0) {  // k in [m, N-1-a]
+            if ((long long)p.m + i * kW > (long long)N - 1 - a) return false;
+            td.k0 = p.m + (int)i * kW;
+            td.dir = +1;
+        } else {  // k in [-e, -m]
+            const long long khi = -(long long)p.m - i * kW;
+            if (e + khi < 0) return false;
+            td.k0 = (int)(khi - kW + 1);
+            td.dir = -1;
+        }
+        return true;
+    }
+    td.r0 = a;
+    td.rows = e - a + 1;
+    if (side == 0) {
+        if (a + k0 >= N) return false;
+        td.k0 = (int)k0;
+        td.dir = +1;
+    } else {
+        if (e - k0 < 0) return false;
+        td.k0 = (int)(-k0 - kW + 1);
+        td.dir = -1;
+    }
+    return true;
+}
+
+struct F9 {
+    float v[kDiag];
+};
+
+// Full-row slow path of one walk step (row c, diagonals u0 .. u0+kDiag-1): the
+// exact constant conventions, certain kills of the row candidate and knife-edge
+// pairs for the FP64 recheck.  Only the row candidate is killed (the pair's
+// other end is decided by its own row), so a decided row never re-enters.
+// Kept out of line: it runs on a few steps only and would otherwise bloat the
+// unrolled walk.
+__device__ __noinline__ void slow_track(const F9 x, const F9 qn, float tz, float cw, int c, int u0, int dir,
+                                        int qbase, int N, int m, double r_sq, double thr0, double E,
+                                        uint8_t* alive, int2* queue, int* queue_count, int queue_cap) {
+#pragma unroll
+    for (int j = 0; j < kDiag; ++j) {
+        if (!(x.v[j] > tz)) continue;
+        const int u = u0 + j;
+        const int q = dir > 0 ? qbase + u : qbase - u;
+        if (q < 0 || q >= N) continue;
+        const float qj = qn.v[j];
+        if (cw == 0.f || qj == 0.f) {
+            const double d = (cw == 0.f && qj == 0.f) ? 0.0 : 2.0 * (double)m;
+            if (d < r_sq) alive[c] = 0;
+            continue;
+        }
+        const double corr = (double)x.v[j] * (double)cw;
+        const double ec = E * (double)cw * (double)qj + kSlack;
+        if (corr - ec > thr0) {
+            alive[c] = 0;
+        } else if (corr + ec >= thr0) {
+            const int at = atomicAdd(queue_count, 1);
+            if (at < queue_cap) queue[at] = make_int2(c, q);
+        }
+    }
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 6) k_scan(const ScanParams p) {
+__global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(const ScanParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ScanSmem& S = *reinterpret_cast<ScanSmem*>(smem_raw);
-
-    const TileDesc td = p.tiles[blockIdx.x];
     const int tid = threadIdx.x;
+    const long long slots = tile_slots(p);
+    // persistent CTAs: slots are fetched dynamically; rank r owns slots r, r+world, ...
+    const long long mine = p.world > 1 ? (slots > p.rank ? (slots - p.rank + p.world - 1) / p.world : 0) : slots;
+    // first round static (CTA b takes slot b: the hardware spreads consecutive
+    // CTAs over the SMs, so a launch with fewer tiles than CTAs stays balanced),
+    // then dynamic
+    for (long long f = blockIdx.x;;) {
+    if (f >= mine) break;
+    TileDesc td;
+    const bool valid = tile_decode(p, f * p.world + p.rank, td);
+    __syncthreads();  // smem of the previous tile is dead; S.flag is free
+    if (tid == 0) S.flag = atomicAdd(&p.ctl->next, 1);
+    __syncthreads();
+    f = (long long)S.flag + gridDim.x;
+    if (!valid) continue;
     const int rows = td.rows;
     const int dir = td.dir;
     const int N = p.N;
@@ -86,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 6) k_scan(const ScanParams p) {
     {
         int any = 0;
         for (int s = tid; s < rows; s += kThreads) any |= p.alive[td.r0 + s];
-        if (!__syncthreads_or(any)) return;
+        if (!__syncthreads_or(any)) continue;
     }
 
     // ---- 1. seeds: cov(c_first, q) for this thread's kDiag diagonals --------
@@ -305,7 +446,9 @@ __global__ void __launch_bounds__(kThreads, 6) k_scan(const ScanParams p) {
         } else if (!live) {
             tc = kNoEval;
         } else if (cn == 0.f) {
-            tc = -FLT_MAX;  // constant row: always take the exact-convention slow path
+            // constant row: full rows take the exact-convention slow path on every
+            // cell; band passes leave it to them
+            tc = MODE == kPrune ? kNoEval : -FLT_MAX;
         } else if (MODE == kPrune) {
             // band passes only make certain kills: every cell with x > tk has
             // corr - eps_cell > thr0 (eps_cell <= eps_row); knife edges are left
@@ -364,45 +507,29 @@ __global__ void __launch_bounds__(kThreads, 6) k_scan(const ScanParams p) {
                     x[j] = cov[j] * rn[(j + uu) % kDiag];
                     mx = fmaxf(mx, x[j]);
                 }
-                if (MODE == kPrune && mx > cr.z && cr.w != 0.f) {
-                    // certain kill of the row candidate (FP32 only)
-                    p.alive[dir > 0 ? td.r0 + ss : r_end - ss] = 0;
-                } else if (MODE != kCollect && mx > cr.z) {
-                    // ---- slow path: exact conventions, certain kill, knife edges.
-                    // Only the row candidate is killed (the pair's other end is
-                    // decided by its own row), so a decided row never re-enters.
-                    const int c = dir > 0 ? td.r0 + ss : r_end - ss;
+                if (MODE == kPrune) {
+                    // certain kill of the row candidate (FP32 only; constant rows are
+                    // not evaluated in band passes): a predicated store, no branch
+                    if (mx > cr.z) p.alive[dir > 0 ? td.r0 + ss : r_end - ss] = 0;
+                } else if (MODE == kPruneTrack) {
+                    if (mx > cr.z) {
+                        // rare: kills, knife edges, constant conventions (out of line)
+                        F9 xv, qv;
 #pragma unroll
-                    for (int j = 0; j < kDiag; ++j) {
-                        if (!(x[j] > cr.z)) continue;
-                        const int u = ss + ub + j;
-                        const int q = dir > 0 ? qbase + u : qbase - u;
-                        if (q < 0 || q >= N) continue;
-                        const float qn = rn[(j + uu) % kDiag];
-                        if (cr.w == 0.f || qn == 0.f) {
-                            const double d = (cr.w == 0.f && qn == 0.f) ? 0.0 : 2.0 * (double)m;
-                            if (d < p.r_sq) p.alive[c] = 0;
-                            continue;
+                        for (int j = 0; j < kDiag; ++j) {
+                            xv.v[j] = x[j];
+                            qv.v[j] = rn[(j + uu) % kDiag];
                         }
-                        const double corr = (double)x[j] * (double)cr.w;
-                        const double ec = E * (double)cr.w * (double)qn + kSlack;
-                        if (corr - ec > p.thr0) {
-                            p.alive[c] = 0;
-                        } else if (MODE == kPruneTrack && corr + ec >= p.thr0) {
-                            const int at = atomicAdd(p.queue_count, 1);
-                            if (at < p.queue_cap) p.queue[at] = make_int2(c, q);
-                        }
+                        slow_track(xv, qv, cr.z, cr.w, dir > 0 ? td.r0 + ss : r_end - ss, ss + ub, dir, qbase, N,
+                                   m, p.r_sq, p.thr0, E, p.alive, p.queue, p.queue_count, p.queue_cap);
                     }
-                }
-                if (MODE == kPruneTrack && S.ykey[ss] != 0u) {
-                    // row max of the FP32 route value x = cov*qn over valid q (NaN for
-                    // invalid q is ignored by fmaxf; a constant q contributes exactly
-                    // 0); the tile's error term E*qn_max is folded in at the end
-                    float y = -FLT_MAX;
-#pragma unroll
-                    for (int j = 0; j < kDiag; ++j) y = fmaxf(y, x[j]);
-                    y = warp_max(y);
-                    if (lane == 0 && y > -FLT_MAX) atomicMax(&S.ykey[ss], f2key(y));
+                    if (S.ykey[ss] != 0u) {
+                        // row max of the FP32 route value x = cov*qn over valid q (NaN for
+                        // invalid q is ignored by fmaxf; a constant q contributes exactly
+                        // 0); the tile's error term E*qn_max is folded in at the end
+                        const float y = warp_max(mx);
+                        if (lane == 0 && y > -FLT_MAX) atomicMax(&S.ykey[ss], f2key(y));
+                    }
                 }
                 if (MODE == kCollect) {
                     const float th = S.cy[ss];
@@ -442,6 +569,16 @@ __global__ void __launch_bounds__(kThreads, 6) k_scan(const ScanParams p) {
         atomicAdd(&p.acc[0], (unsigned long long)rows * (unsigned long long)kW);
         atomicAdd(&p.acc[1], (unsigned long long)evals * (unsigned long long)kW);
         if (td.seed < 0) atomicAdd(&p.acc[2], (unsigned long long)kW);
+    }
+    }  // persistent tile loop
+    // the last CTA out resets the slot counter for the next launch
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(&p.ctl->ctas_done, 1) == (int)gridDim.x - 1) {
+            p.ctl->next = 0;
+            p.ctl->ctas_done = 0;
+            __threadfence();
+        }
     }
 }
 
@@ -502,7 +639,9 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_ref_pairs(const double* __r
                                                                const int* __restrict__ count,
                                                                int cap, double r_sq,
                                                                uint8_t* alive,
-                                                               unsigned long long* nnkey) {
+                                                               unsigned long long* nnkey,
+                                                               TryCtl* ctl, const int* __restrict__ ex,
+                                                               double* __restrict__ nnout) {
     __shared__ double buf[kPairWarps][256];
     const int w = threadIdx.x >> 5;
     const int total = min(*count, cap);
@@ -521,193 +660,629 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_ref_pairs(const double* __r
             }
         }
     }
+    if (MODE == 1 && ex != nullptr) {
+        // single-rank exact pass: the last CTA out gathers the survivors' nn
+        __shared__ int s_last;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) s_last = atomicAdd(&ctl->xdone, 1) == (int)gridDim.x - 1;
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+        const int ec = ctl->ec;
+        for (int e = threadIdx.x; e < ec; e += blockDim.x)
+            nnout[e] = __longlong_as_double((long long)__ldcg(&nnkey[ex[e]]));
+        if (threadIdx.x == 0) ctl->xdone = 0;
+    }
 }
 
 // ---------------------------------------------------------------------------
-// flags / compaction helpers
-__global__ void k_fill_u8(uint8_t* a, int n, uint8_t v) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = v;
+// flags / compaction / grouping / survivor kernels.  None of them takes a
+// count from the host: counts live in TryCtl, so one DRAG try is a single
+// stream-ordered sequence with no host round trip.
+constexpr int kSmallGrid = 148 * 2;  // grid-stride kernels over device-sized lists
+
+// try start: every row undecided, counters reset, route maxima cleared
+__global__ void k_try_init(uint8_t* __restrict__ alive, unsigned* __restrict__ ymax, unsigned* __restrict__ emax,
+                           float* __restrict__ ythr, int N, TryCtl* ctl, unsigned long long* acc) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+        alive[i] = 1;
+        ymax[i] = 0u;
+        emax[i] = 0u;
+        ythr[i] = FLT_MAX;  // collection off unless the row gets exact nn this try
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctl->alive = N;
+        ctl->prev = N;
+        ctl->stop = INT_MAX;
+        ctl->G = 0;
+        ctl->queue = 0;
+        ctl->coll = 0;
+        ctl->crange[0] = N;
+        ctl->crange[1] = -1;
+        ctl->sc = 0;
+        ctl->ec = 0;
+        ctl->passes = 0;
+        ctl->span = 0;
+        ctl->lk = 0.0;
+        acc[0] = acc[1] = acc[2] = 0ull;
+    }
+}
+
+__device__ __forceinline__ bool gated_off(const TryCtl* ctl, int gate) {
+    if (gate >= 0) return ctl->stop < gate;
+    if (gate == kGateQueue) return ctl->queue == 0 || ctl->alive == 0;
+    return false;
 }
 
 constexpr int kCompactBlock = 1024;
 constexpr int kCompactItems = 4;  // flags per thread
 constexpr int kCompactTile = kCompactBlock * kCompactItems;
 
-__global__ void k_compact_count(const uint8_t* __restrict__ a, int n, int* __restrict__ blk) {
-    __shared__ int ws[kCompactBlock / 32];
-    const int base = blockIdx.x * kCompactTile;
-    int c = 0;
-#pragma unroll
-    for (int k = 0; k < kCompactItems; ++k) {
-        const int i = base + threadIdx.x * kCompactItems + k;
-        c += (i < n && a[i]) ? 1 : 0;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int t = 0;
-        for (int w = 0; w < kCompactBlock / 32; ++w) t += ws[w];
-        blk[blockIdx.x] = t;
-    }
-}
-
-// single CTA exclusive scan over block counts; total -> out[nb]
-__global__ void k_compact_scan(int* blk, int nb) {
-    __shared__ int carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int base = 0; base < nb; base += blockDim.x) {
-        const int i = base + threadIdx.x;
-        const int v = i < nb ? blk[i] : 0;
-        // inclusive warp scan
-        int x = v;
-        const int lane = threadIdx.x & 31;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        __shared__ int wsum[32];
-        if (lane == 31) wsum[threadIdx.x >> 5] = x;
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            int z = threadIdx.x < (int)(blockDim.x >> 5) ? wsum[threadIdx.x] : 0;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, z, o);
-                if ((int)threadIdx.x >= o) z += y;
-            }
-            wsum[threadIdx.x] = z;
-        }
-        __syncthreads();
-        const int woff = (threadIdx.x >> 5) ? wsum[(threadIdx.x >> 5) - 1] : 0;
-        if (i < nb) blk[i] = carry + woff + x - v;
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) carry += woff + x;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) blk[nb] = carry;
-}
-
-__global__ void k_compact_scatter(const uint8_t* __restrict__ a, int n, const int* __restrict__ blk,
-                                  int* __restrict__ out) {
-    __shared__ int ws[kCompactBlock / 32];
-    const int base = blockIdx.x * kCompactTile;
-    int f[kCompactItems];
-    int c = 0;
-#pragma unroll
-    for (int k = 0; k < kCompactItems; ++k) {
-        const int i = base + threadIdx.x * kCompactItems + k;
-        f[k] = (i < n && a[i]) ? 1 : 0;
-        c += f[k];
-    }
-    const int lane = threadIdx.x & 31;
-    int x = c;
+// block-wide exclusive scan of one int per thread (blockDim.x == 1024); returns
+// the exclusive prefix, *total receives the block sum
+__device__ __forceinline__ int block_exscan(int v, int* wsum, int* total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
-    if (lane == 31) ws[threadIdx.x >> 5] = x;
     __syncthreads();
-    if (threadIdx.x < 32) {
-        int z = ws[threadIdx.x];
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int z = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int y = __shfl_up_sync(0xffffffffu, z, o);
-            if ((int)threadIdx.x >= o) z += y;
+            if (lane >= o) z += y;
         }
-        ws[threadIdx.x] = z;
+        wsum[lane] = z;
     }
     __syncthreads();
-    int pos = blk[blockIdx.x] + ((threadIdx.x >> 5) ? ws[(threadIdx.x >> 5) - 1] : 0) + x - c;
-#pragma unroll
-    for (int k = 0; k < kCompactItems; ++k) {
-        if (f[k]) out[pos++] = base + threadIdx.x * kCompactItems + k;
+    *total = wsum[(blockDim.x >> 5) - 1];
+    return (w ? wsum[w - 1] : 0) + x - v;
+}
+
+// Groups of the listed rows for the next scan (single CTA).  Groups are the
+// greedy spans of the sorted list: a group starts at a listed row a and takes
+// every listed row < a + span.  A gap >= span between consecutive rows always
+// starts a new group, so the greedy chain splits into independent segments at
+// such gaps and every segment is walked by one thread.  The span minimises
+// sum over groups of (2m seed work + 3 per walked row and diagonal).  Dense
+// lists (>= 1 row in 64 undecided) take aligned 512-row blocks instead.
+constexpr int kSpans = 6;  // 16, 32, ..., 512
+
+// walks the segment starting at list index e (a segment start for `span`);
+// calls emit(first_index, last_index) for each group
+template <typename F>
+__device__ __forceinline__ void walk_segment(const int* __restrict__ list, int cnt, int e, int span, F&& emit) {
+    int j = e;
+    for (;;) {
+        const int g0 = j;
+        const int lim = list[j] + span;
+        ++j;
+        while (j < cnt && list[j] < lim) ++j;
+        emit(g0, j - 1);
+        if (j >= cnt || list[j] - list[j - 1] >= span) return;
     }
 }
 
-// survivors: reset exact-nn keys and decode collection thresholds.  The
-// tracked max route value x* and the row's largest tile error term e give a
-// lower bound x* - e of the row's true best corr / cn; every q whose upper
-// bound x + E*qn reaches it may be the reference's minimiser.
-__global__ void k_prep_survivors(const int* __restrict__ list, int cnt, const unsigned* __restrict__ ymax,
-                                 const unsigned* __restrict__ emax, float* __restrict__ ythr,
-                                 unsigned long long* __restrict__ nnkey) {
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += gridDim.x * blockDim.x) {
-        const int c = list[e];
-        const unsigned k = ymax[c];
-        float th = -FLT_MAX;  // no tracked data: collect everything
-        if (k > 1u) {
-            const float lo = key2f(k) - __uint_as_float(emax[c]);
-            // two ulps down: FP64 rounding of near-ties can never exclude the minimiser
-            th = nextafterf(nextafterf(lo - fabsf(lo) * 2.4e-7f, -FLT_MAX), -FLT_MAX);
-        }
-        ythr[c] = th;
-        nnkey[c] = 0x7ff0000000000000ull;  // +inf
+constexpr int kGroupStage = 8192;  // list entries staged in smem (32 KB)
+// whole-CTA (1024 threads) body; every thread must call it
+__device__ void group_body(const int* __restrict__ list_g, const int cnt, int2* __restrict__ groups, TryCtl* ctl,
+                           int m, int fixed_span) {
+    __shared__ double costs[32][kSpans];
+    __shared__ int wsum[32];
+    __shared__ int s_span;
+    __shared__ int s_list[kGroupStage];
+    __syncthreads();  // callers may have used their own smem just before
+    if (cnt == 0) {
+        if (threadIdx.x == 0) ctl->G = 0;
+        return;
     }
+    // the greedy walks chase list entries one by one: stage the list in smem
+    if (cnt <= kGroupStage) {
+        for (int e = threadIdx.x; e < cnt; e += blockDim.x) s_list[e] = list_g[e];
+        __syncthreads();
+    }
+    const int* __restrict__ list = cnt <= kGroupStage ? s_list : list_g;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        int sp = fixed_span;
+        if (sp <= 0 && (long long)cnt * 64 >= (long long)(list[cnt - 1] - list[0] + 1)) sp = -kMaxRows;
+        s_span = sp;
+    }
+    __syncthreads();
+    if (s_span < 0) {  // dense: aligned blocks
+        const int span = -s_span;
+        int carry = 0;
+        for (int base = 0; base < cnt; base += blockDim.x) {
+            const int e = base + threadIdx.x;
+            int r = 0, st = 0, en = 0;
+            if (e < cnt) {
+                r = list[e];
+                st = (e == 0 || list[e - 1] / span != r / span);
+                en = (e + 1 == cnt || list[e + 1] / span != r / span);
+            }
+            int tot;
+            const int g = carry + block_exscan(st, wsum, &tot) + st - 1;  // group of entry e
+            if (e < cnt) {
+                if (st) groups[g].x = r;
+                if (en) groups[g].y = r;
+            }
+            carry += tot;
+        }
+        if (threadIdx.x == 0) {
+            ctl->G = carry;
+            ctl->span = span;
+        }
+        return;
+    }
+    if (s_span == 0) {
+        double c[kSpans];
+#pragma unroll
+        for (int k = 0; k < kSpans; ++k) c[k] = 0.0;
+        for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+            const int gap = e > 0 ? list[e] - list[e - 1] : INT_MAX;
+#pragma unroll 1
+            for (int k = 0; k < kSpans; ++k) {
+                const int span = 16 << k;
+                if (gap < span) continue;
+                double acc = 0.0;
+                walk_segment(list, cnt, e, span, [&](int i0, int i1) {
+                    acc += 2.0 * m + 3.0 * (double)(list[i1] - list[i0] + 1 + kDiag);
+                });
+                c[k] += acc;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kSpans; ++k) {
+            double v = c[k];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) costs[w][k] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double best = 1e300;
+            int bs = 64;
+            for (int k = 0; k < kSpans; ++k) {
+                double v = 0.0;
+                for (int x = 0; x < (int)(blockDim.x >> 5); ++x) v += costs[x][k];
+                if (v < best) {
+                    best = v;
+                    bs = 16 << k;
+                }
+            }
+            s_span = bs;
+        }
+        __syncthreads();
+    }
+    const int span = s_span;
+    int carry = 0;
+    for (int base = 0; base < cnt; base += blockDim.x) {
+        const int e = base + threadIdx.x;
+        const bool seg = e < cnt && (e == 0 || list[e] - list[e - 1] >= span);
+        int ng = 0;
+        if (seg) walk_segment(list, cnt, e, span, [&](int, int) { ++ng; });
+        int tot;
+        int g = carry + block_exscan(ng, wsum, &tot);
+        if (seg)
+            walk_segment(list, cnt, e, span, [&](int i0, int i1) { groups[g++] = make_int2(list[i0], list[i1]); });
+        carry += tot;
+    }
+    if (threadIdx.x == 0) {
+        ctl->G = carry;
+        ctl->span = span;
+    }
+}
+
+// One-kernel compaction of the alive flags into the sorted row list
+// (decoupled look-back: a CTA's logical index comes from a ticket, so it only
+// waits on CTAs that started before it), fused with the grouping of the new
+// list for the next scan and, for band passes, the band-loop break rule.
+//
+// Groups are the non-empty aligned span-blocks of rows (span 16..512; a
+// 4096-row compaction tile holds whole span-blocks, so every CTA sees its
+// blocks completely).  Each CTA writes the (first, last) alive row of every
+// span-block of its tile for all six spans (`slots`) and adds their cost
+// sum(2m seed work + 3 per walked row and diagonal) per span; the last CTA to
+// finish picks the span (dense lists: 512) and compacts that span's slots
+// into the dense group array.
+//
+// status[] words: epoch (30 bits) | state (2: 1 aggregate, 2 inclusive) |
+// value (32), so the array never needs clearing between launches.
+__device__ __forceinline__ unsigned long long lb_word(unsigned epoch, unsigned state, unsigned v) {
+    return ((unsigned long long)epoch << 34) | ((unsigned long long)state << 32) | v;
+}
+// offset of span k's slot region (tile b's span-blocks at + b * (256 >> k))
+__device__ __forceinline__ long long slot_region(int k, int nb) { return (long long)nb * (512 - (512 >> k)); }
+
+__global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restrict__ a, int n, int* __restrict__ out,
+                                                        unsigned long long* status, unsigned epoch, TryCtl* ctl,
+                                                        int gate, int2* __restrict__ groups,
+                                                        int2* __restrict__ slots, int m, int fixed_span,
+                                                        float band_keep) {
+    if (gated_off(ctl, gate)) return;
+    __shared__ int s_bid, s_excl, s_last, s_k;
+    __shared__ int wsum[32];
+    __shared__ int s_fa[32], s_la[32];
+    __shared__ double s_cost[32][kSpans];
+    const int nb = gridDim.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_bid = atomicAdd(&ctl->cticket, 1);
+    __syncthreads();
+    const int bid = s_bid;
+    const int base = bid * kCompactTile;
+    const int i0 = base + threadIdx.x * kCompactItems;
+    int f[kCompactItems];
+    int c = 0;
+    if (i0 + kCompactItems <= n) {
+        const uchar4 v = *reinterpret_cast<const uchar4*>(a + i0);
+        f[0] = v.x != 0;
+        f[1] = v.y != 0;
+        f[2] = v.z != 0;
+        f[3] = v.w != 0;
+    } else {
+#pragma unroll
+        for (int k = 0; k < kCompactItems; ++k) f[k] = (i0 + k < n && a[i0 + k]) ? 1 : 0;
+    }
+    int fa = INT_MAX, la = -1;
+#pragma unroll
+    for (int k = 0; k < kCompactItems; ++k) {
+        c += f[k];
+        if (f[k]) {
+            fa = min(fa, i0 + k);
+            la = i0 + k;
+        }
+    }
+    // ---- span-blocks: spans 16..128 within a warp, 256 / 512 across warps
+    {
+        const double cm = 2.0 * (double)m + 3.0 * (double)(1 + kDiag);
+        int mn = fa, mx = la;
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, 1));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        double cst[kSpans];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int o = 2 << k;  // lanes reduced so far: o; after this step 2*o = 4 << k = span / 4
+            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            cst[k] = 0.0;
+            if ((lane & ((4 << k) - 1)) == 0) {
+                const int j = threadIdx.x >> (2 + k);
+                slots[slot_region(k, nb) + (long long)bid * (256 >> k) + j] = make_int2(mn, mx);
+                if (mx >= 0) cst[k] = cm + 3.0 * (double)(mx - mn);
+            }
+        }
+        if (lane == 0) {
+            s_fa[w] = mn;
+            s_la[w] = mx;
+        }
+        __syncthreads();
+        cst[4] = cst[5] = 0.0;
+        if (threadIdx.x < 16) {  // span 256: 2 warps each
+            const int j = threadIdx.x;
+            const int x = min(s_fa[2 * j], s_fa[2 * j + 1]), y = max(s_la[2 * j], s_la[2 * j + 1]);
+            slots[slot_region(4, nb) + (long long)bid * 16 + j] = make_int2(x, y);
+            if (y >= 0) cst[4] = cm + 3.0 * (double)(y - x);
+        } else if (threadIdx.x >= 32 && threadIdx.x < 40) {  // span 512: 4 warps each
+            const int j = threadIdx.x - 32;
+            const int x = min(min(s_fa[4 * j], s_fa[4 * j + 1]), min(s_fa[4 * j + 2], s_fa[4 * j + 3]));
+            const int y = max(max(s_la[4 * j], s_la[4 * j + 1]), max(s_la[4 * j + 2], s_la[4 * j + 3]));
+            slots[slot_region(5, nb) + (long long)bid * 8 + j] = make_int2(x, y);
+            if (y >= 0) cst[5] = cm + 3.0 * (double)(y - x);
+        }
+#pragma unroll
+        for (int k = 0; k < kSpans; ++k) {
+            double v = cst[k];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) s_cost[w][k] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < kSpans) {
+            double v = 0.0;
+            for (int x = 0; x < 32; ++x) v += s_cost[x][threadIdx.x];
+            if (v != 0.0) atomicAdd(&ctl->cost[threadIdx.x], v);
+        }
+    }
+    // ---- compaction (decoupled look-back)
+    int tot;
+    const int ex = block_exscan(c, wsum, &tot);
+    volatile unsigned long long* vs = status;
+    if (threadIdx.x < 32) {
+        if (bid == 0) {
+            if (lane == 0) {
+                __threadfence();
+                vs[0] = lb_word(epoch, 2u, (unsigned)tot);
+                s_excl = 0;
+            }
+        } else {
+            if (lane == 0) {
+                __threadfence();
+                vs[bid] = lb_word(epoch, 1u, (unsigned)tot);
+            }
+            int excl = 0;
+            int j = bid - 1;
+            for (;;) {
+                const int idx = j - lane;
+                unsigned long long wv;
+                bool ok;
+                do {
+                    wv = idx >= 0 ? vs[idx] : lb_word(epoch, 2u, 0u);
+                    ok = (unsigned)(wv >> 34) == (epoch & 0x3fffffffu) && ((wv >> 32) & 3u) != 0u;
+                } while (!__all_sync(0xffffffffu, ok));
+                const unsigned incl_mask = __ballot_sync(0xffffffffu, ((wv >> 32) & 3u) == 2u);
+                int v = (int)(unsigned)wv;
+                if (incl_mask) {
+                    const int L = __ffs(incl_mask) - 1;  // nearest inclusive predecessor
+                    if (lane > L) v = 0;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                    excl += v;
+                    break;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                excl += v;
+                j -= 32;
+            }
+            if (lane == 0) {
+                __threadfence();
+                vs[bid] = lb_word(epoch, 2u, (unsigned)(excl + tot));
+                s_excl = excl;
+            }
+        }
+    }
+    __syncthreads();
+    int pos = s_excl + ex;
+#pragma unroll
+    for (int k = 0; k < kCompactItems; ++k) {
+        if (f[k]) out[pos++] = i0 + k;
+    }
+    if (bid == nb - 1 && threadIdx.x == 0) ctl->ctotal = s_excl + tot;
+    // ---- the last CTA to finish sees every scatter, slot and cost: it finalises
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&ctl->cdone, 1) == nb - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int total = *(volatile int*)&ctl->ctotal;
+    if (threadIdx.x == 0) {
+        ctl->cticket = 0;
+        ctl->cdone = 0;
+        if (gate >= 0) {
+            const int prev = ctl->alive;
+            ctl->prev = prev;
+            ctl->passes = gate + 1;
+            if (total == 0 || total <= max(64, n / 4096) || (double)total > (double)band_keep * (double)prev)
+                ctl->stop = gate;
+        }
+        ctl->alive = total;
+        int k = 5;  // dense lists (>= 1 row in 64 undecided): whole 512-row blocks
+        if (fixed_span > 0) {
+            k = 0;
+            while (k < 5 && (16 << k) < fixed_span) ++k;
+        } else if (total > 0 && (long long)total * 64 < (long long)(__ldcg(&out[total - 1]) - __ldcg(&out[0]) + 1)) {
+            double best = 1e300;
+            for (int x = 0; x < kSpans; ++x) {
+                const double v = *(volatile double*)&ctl->cost[x];
+                if (v < best) {
+                    best = v;
+                    k = x;
+                }
+            }
+        }
+        for (int x = 0; x < kSpans; ++x) ctl->cost[x] = 0.0;
+        s_k = k;
+        ctl->span = 16 << k;
+    }
+    __syncthreads();
+    const int k = s_k;
+    const int nslot = nb * (256 >> k);
+    const int2* sl = slots + slot_region(k, nb);
+    int carry = 0;
+    for (int b0 = 0; b0 < nslot; b0 += blockDim.x) {
+        const int e = b0 + threadIdx.x;
+        int2 v = make_int2(0, -1);
+        if (e < nslot) v = __ldcg(&sl[e]);
+        const int ff = v.y >= 0 ? 1 : 0;
+        int t2;
+        const int p2 = carry + block_exscan(ff, wsum, &t2);
+        if (ff) groups[p2] = v;
+        carry += t2;
+    }
+    if (threadIdx.x == 0) ctl->G = carry;
 }
 
 // per-survivor interval [lo, hi] of the exact nn^2 from the tracked route maxima
 // (constant rows: the exact convention value)
-__global__ void k_nn_bounds(const int* __restrict__ list, int cnt, const unsigned* __restrict__ ymax,
-                            const unsigned* __restrict__ emax, const float* __restrict__ nrm,
-                            const int* __restrict__ const_range, int N, int m, double* __restrict__ lo,
-                            double* __restrict__ hi) {
+__device__ __forceinline__ void nn_interval(int c, const unsigned* ymax, const unsigned* emax, const float* nrm,
+                                            const int* const_range, int N, int m, double& l, double& h) {
     const double inf = __longlong_as_double(0x7ff0000000000000ll);
     const double two_m = 2.0 * (double)m;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += gridDim.x * blockDim.x) {
-        const int c = list[e];
-        const float cn = nrm[c];
-        double l = 0.0, h = inf;
-        if (cn == 0.f) {
-            const int a = const_range[0], b = const_range[1];
-            double d = inf;
-            if (c - a >= m || b - c >= m) d = 0.0;
-            else if (c - m >= 0 || c + m <= N - 1) d = two_m;
-            l = h = d;
-        } else if (ymax[c] > 1u) {
-            const double x = (double)key2f(ymax[c]);
-            const double ee = (double)__uint_as_float(emax[c]);
-            const double slack = 1e-6 + 1e-9;
-            l = two_m * (1.0 - ((x + ee) * (double)cn + slack));
-            h = two_m * (1.0 - ((x - ee) * (double)cn - slack));
-            if (l < 0.0) l = 0.0;
+    const float cn = nrm[c];
+    l = 0.0;
+    h = inf;
+    if (cn == 0.f) {
+        const int a = const_range[0], b = const_range[1];
+        double d = inf;
+        if (c - a >= m || b - c >= m) d = 0.0;
+        else if (c - m >= 0 || c + m <= N - 1) d = two_m;
+        l = h = d;
+    } else if (ymax[c] > 1u) {
+        const double x = (double)key2f(ymax[c]);
+        const double ee = (double)__uint_as_float(emax[c]);
+        const double slack = 1e-6 + 1e-9;
+        l = two_m * (1.0 - ((x + ee) * (double)cn + slack));
+        h = two_m * (1.0 - ((x - ee) * (double)cn - slack));
+        if (l < 0.0) l = 0.0;
+    }
+}
+
+__device__ __forceinline__ unsigned long long dkey(double d) {  // order-preserving
+    const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// Decodes the per-length constant-row range written by k_derive
+// (cr[0] = max(N - i), cr[1] = max(i + 1) over constant rows i; 0 = none).
+__device__ __forceinline__ void crange_decode(const int* cr, int N, int out[2]) {
+    out[0] = N - cr[0];
+    out[1] = cr[1] - 1;
+}
+
+// nn by the constant conventions of reference_sq_dist for a constant row c:
+// 0 with an admissible constant partner, else 2m, else inf
+__device__ __forceinline__ double const_nn(int c, const int cr[2], int N, int m) {
+    if (c - cr[0] >= m || cr[1] - c >= m) return 0.0;
+    if (c - m >= 0 || c + m <= N - 1) return 2.0 * (double)m;
+    return __longlong_as_double(0x7ff0000000000000ll);
+}
+
+// The survivors stage of a try in one CTA (1024 threads):
+//   1. survivors = the listed rows still alive after full rows + knife edges
+//      (order-preserving filter of the pre-full-rows list) -> ctl->sc;
+//   2. MERLIN (need > 0): keep the rows whose nn interval reaches the need-th
+//      largest lower bound (rank count for small lists, MSB radix select
+//      otherwise) -> ctl->ec;
+//   3. reset their exact-nn keys (constant rows: the convention value) and
+//      collection thresholds;
+//   4. group them for the collection scan.
+__global__ void __launch_bounds__(1024) k_survivors(const int* __restrict__ list, const uint8_t* __restrict__ alive,
+                                                    TryCtl* ctl, const unsigned* __restrict__ ymax,
+                                                    const unsigned* __restrict__ emax,
+                                                    const float* __restrict__ nrm, const int* __restrict__ cr_raw,
+                                                    int N, int m, int need, double* __restrict__ lo,
+                                                    double* __restrict__ hi, int* __restrict__ cand,
+                                                    float* __restrict__ ythr, unsigned long long* __restrict__ nnkey,
+                                                    int2* __restrict__ groups, int fixed_span) {
+    __shared__ int wsum[32];
+    __shared__ int hist[256];
+    __shared__ unsigned long long s_prefix;
+    __shared__ int s_rem;
+    __shared__ double s_lk;
+    int cr[2];
+    crange_decode(cr_raw, N, cr);
+    const int cnt = ctl->alive;
+    // 1. survivors
+    int sc = 0;
+    for (int base = 0; base < cnt; base += blockDim.x) {
+        const int e = base + threadIdx.x;
+        const int r = e < cnt ? list[e] : 0;
+        const int f = (e < cnt && alive[r]) ? 1 : 0;
+        int tot;
+        const int pos = sc + block_exscan(f, wsum, &tot);
+        if (f) cand[pos] = r;
+        sc += tot;
+    }
+    __syncthreads();
+    int ec = sc;
+    // 2. top-k filter
+    if (need > 0 && sc > need) {
+        for (int e = threadIdx.x; e < sc; e += blockDim.x) {
+            double l, h;
+            nn_interval(cand[e], ymax, emax, nrm, cr, N, m, l, h);
+            lo[e] = l;
+            hi[e] = h;
         }
-        lo[e] = l;
-        hi[e] = h;
-    }
-}
-
-// constant survivors (stats sigma < eps): nn by the conventions of
-// reference_sq_dist — 0 with an admissible constant partner, else 2m, else inf.
-__global__ void k_const_nn(const int* __restrict__ list, int cnt, const float* __restrict__ nrm,
-                           const int* __restrict__ const_range, int N, int m,
-                           unsigned long long* __restrict__ nnkey) {
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += gridDim.x * blockDim.x) {
-        const int c = list[e];
-        if (nrm[c] != 0.f) continue;
-        const int lo = const_range[0], hi = const_range[1];
-        double d = __longlong_as_double(0x7ff0000000000000ll);
-        if (c - lo >= m || hi - c >= m) d = 0.0;
-        else if (c - m >= 0 || c + m <= N - 1) d = 2.0 * (double)m;
-        nnkey[c] = (unsigned long long)__double_as_longlong(d);
-    }
-}
-
-__global__ void k_const_range(const float* __restrict__ nrm, int N, int* __restrict__ out) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
-        if (nrm[i] == 0.f) {
-            atomicMin(&out[0], i);
-            atomicMax(&out[1], i);
+        __syncthreads();
+        if (sc <= (int)blockDim.x) {
+            const int e = threadIdx.x;
+            if (e < sc) {
+                const double v = lo[e];
+                int gt = 0, ge = 0;
+                for (int x = 0; x < sc; ++x) {
+                    const double u = lo[x];
+                    gt += u > v;
+                    ge += u >= v;
+                }
+                if (gt < need && need <= ge) s_lk = v;  // every writer holds the same value
+            }
+        } else {
+            if (threadIdx.x == 0) {
+                s_prefix = 0ull;
+                s_rem = need;
+            }
+            __syncthreads();
+            for (int shift = 56; shift >= 0; shift -= 8) {
+                for (int x = threadIdx.x; x < 256; x += blockDim.x) hist[x] = 0;
+                __syncthreads();
+                const unsigned long long pre = s_prefix;
+                const unsigned long long hmask = shift == 56 ? 0ull : (~0ull << (shift + 8));
+                for (int e = threadIdx.x; e < sc; e += blockDim.x) {
+                    const unsigned long long k = dkey(lo[e]);
+                    if ((k & hmask) == pre) atomicAdd(&hist[(k >> shift) & 255], 1);
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    int rem = s_rem, d = 255;
+                    for (; d > 0; --d) {
+                        if (hist[d] >= rem) break;
+                        rem -= hist[d];
+                    }
+                    s_rem = rem;
+                    s_prefix = pre | ((unsigned long long)d << shift);
+                }
+                __syncthreads();
+            }
+            if (threadIdx.x == 0) {
+                const unsigned long long kk = s_prefix;
+                s_lk = __longlong_as_double((long long)((kk >> 63) ? (kk & 0x7fffffffffffffffull) : ~kk));
+            }
         }
+        __syncthreads();
+        const double lk = s_lk;
+        // in-place order-preserving filter (an entry moves only to a lower index)
+        ec = 0;
+        for (int base = 0; base < sc; base += blockDim.x) {
+            const int e = base + threadIdx.x;
+            const int r = e < sc ? cand[e] : 0;
+            const int f = (e < sc && hi[e] >= lk) ? 1 : 0;
+            int tot;
+            const int pos = ec + block_exscan(f, wsum, &tot);  // syncs: every read precedes the writes
+            if (f) cand[pos] = r;
+            ec += tot;
+        }
+        if (threadIdx.x == 0) ctl->lk = lk;
     }
+    __syncthreads();
+    // 3. exact-nn keys and collection thresholds.  The tracked max route value
+    // x* and the row's largest tile error term e give a lower bound x* - e of
+    // the row's true best corr / cn; every q whose upper bound x + E*qn reaches
+    // it may be the reference's minimiser.
+    for (int e = threadIdx.x; e < ec; e += blockDim.x) {
+        const int c = cand[e];
+        if (nrm[c] == 0.f) {
+            nnkey[c] = (unsigned long long)__double_as_longlong(const_nn(c, cr, N, m));
+            continue;  // never collected (cn == 0 rows are not evaluated)
+        }
+        const unsigned k = ymax[c];
+        float th = -FLT_MAX;  // no tracked data: collect everything
+        if (k > 1u) {
+            const float l = key2f(k) - __uint_as_float(emax[c]);
+            // two ulps down: FP64 rounding of near-ties can never exclude the minimiser
+            th = nextafterf(nextafterf(l - fabsf(l) * 2.4e-7f, -FLT_MAX), -FLT_MAX);
+        }
+        ythr[c] = th;
+        nnkey[c] = 0x7ff0000000000000ull;  // +inf
+    }
+    if (threadIdx.x == 0) {
+        ctl->sc = sc;
+        ctl->ec = ec;
+    }
+    // 4. groups of the rows that get exact distances
+    group_body(cand, ec, groups, ctl, m, fixed_span);
 }
 
-__global__ void k_gather_nn(const int* __restrict__ list, int cnt,
+__global__ void k_gather_nn(const int* __restrict__ list, const int* __restrict__ cnt_p,
                             const unsigned long long* __restrict__ nnkey, double* __restrict__ out) {
+    const int cnt = *cnt_p;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += gridDim.x * blockDim.x)
         out[e] = __longlong_as_double((long long)nnkey[list[e]]);
 }
@@ -773,62 +1348,69 @@ void scan_configure() {
     cudaFuncSetAttribute(k_scan<kCollect>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
-void launch_scan(int mode, int ntiles, const ScanParams& p, cudaStream_t st) {
+// persistent scan: one CTA per resident slot (occupancy of each mode)
+static int g_scan_grid[3] = {0, 0, 0};
+
+template <int MODE>
+static int scan_grid() {
+    if (g_scan_grid[MODE] == 0) {
+        int dev = 0, sms = 148, per = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_scan<MODE>, kThreads, sizeof(ScanSmem));
+        g_scan_grid[MODE] = sms * (per > 0 ? per : 1);
+    }
+    return g_scan_grid[MODE];
+}
+
+void launch_scan(int mode, const ScanParams& p, cudaStream_t st) {
     const size_t sm = sizeof(ScanSmem);
-    if (ntiles <= 0) return;
     switch (mode) {
-        case kPrune: k_scan<kPrune><<<ntiles, kThreads, sm, st>>>(p); break;
-        case kPruneTrack: k_scan<kPruneTrack><<<ntiles, kThreads, sm, st>>>(p); break;
-        default: k_scan<kCollect><<<ntiles, kThreads, sm, st>>>(p); break;
+        case kPrune: k_scan<kPrune><<<scan_grid<kPrune>(), kThreads, sm, st>>>(p); break;
+        case kPruneTrack: k_scan<kPruneTrack><<<scan_grid<kPruneTrack>(), kThreads, sm, st>>>(p); break;
+        default: k_scan<kCollect><<<scan_grid<kCollect>(), kThreads, sm, st>>>(p); break;
     }
 }
 
 void launch_ref_pairs(int mode, const double* t, int m, const int2* pairs, const int* count, int cap,
-                      double r_sq, uint8_t* alive, unsigned long long* nnkey, int max_pairs,
-                      cudaStream_t st) {
-    if (max_pairs <= 0) return;
-    const int blocks = grid_for(max_pairs, kPairWarps);
+                      double r_sq, uint8_t* alive, unsigned long long* nnkey, TryCtl* ctl, const int* ex,
+                      double* nnout, cudaStream_t st) {
+    const int blocks = 148 * 4;  // grid-stride over the device-side pair count
     if (mode == 0)
-        k_ref_pairs<0><<<blocks, kPairWarps * 32, 0, st>>>(t, m, pairs, count, cap, r_sq, alive, nnkey);
+        k_ref_pairs<0><<<blocks, kPairWarps * 32, 0, st>>>(t, m, pairs, count, cap, r_sq, alive, nnkey, ctl,
+                                                             nullptr, nullptr);
     else
-        k_ref_pairs<1><<<blocks, kPairWarps * 32, 0, st>>>(t, m, pairs, count, cap, r_sq, alive, nnkey);
+        k_ref_pairs<1><<<blocks, kPairWarps * 32, 0, st>>>(t, m, pairs, count, cap, r_sq, alive, nnkey, ctl, ex,
+                                                             nnout);
 }
 
-void launch_fill_u8(uint8_t* a, int n, uint8_t v, cudaStream_t st) {
-    k_fill_u8<<<grid_for(n, 256), 256, 0, st>>>(a, n, v);
+void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const unsigned* ymax,
+                      const unsigned* emax, const float* nrm, const int* crange, int N, int m, int need,
+                      double* lo, double* hi, int* cand, float* ythr, unsigned long long* nnkey, int2* groups,
+                      int fixed_span, cudaStream_t st) {
+    k_survivors<<<1, 1024, 0, st>>>(list, alive, ctl, ymax, emax, nrm, crange, N, m, need, lo, hi, cand, ythr,
+                                    nnkey, groups, fixed_span);
+}
+
+void launch_try_init(uint8_t* alive, unsigned* ymax, unsigned* emax, float* ythr, int N, TryCtl* ctl,
+                     unsigned long long* acc, cudaStream_t st) {
+    k_try_init<<<grid_for(N, 256), 256, 0, st>>>(alive, ymax, emax, ythr, N, ctl, acc);
 }
 
 int compact_blocks(int n) { return (n + kCompactTile - 1) / kCompactTile; }
 
-void launch_compact(const uint8_t* a, int n, int* blk, int* out, cudaStream_t st) {
-    const int nb = compact_blocks(n);
-    k_compact_count<<<nb, kCompactBlock, 0, st>>>(a, n, blk);
-    k_compact_scan<<<1, 1024, 0, st>>>(blk, nb);
-    k_compact_scatter<<<nb, kCompactBlock, 0, st>>>(a, n, blk, out);
+void launch_compact_group(const uint8_t* a, int n, int* out, unsigned long long* status, unsigned epoch,
+                          TryCtl* ctl, int gate, int2* groups, int2* slots, int m, int fixed_span, float band_keep,
+                          cudaStream_t st) {
+    k_compact_group<<<compact_blocks(n), kCompactBlock, 0, st>>>(a, n, out, status, epoch, ctl, gate, groups, slots,
+                                                               m, fixed_span, band_keep);
 }
 
-void launch_prep_survivors(const int* list, int cnt, const unsigned* ymax, const unsigned* emax, float* ythr,
-                           unsigned long long* nnkey, cudaStream_t st) {
-    k_prep_survivors<<<grid_for(cnt, 256), 256, 0, st>>>(list, cnt, ymax, emax, ythr, nnkey);
-}
+int group_slots(int n) { return compact_blocks(n) * 504; }
 
-void launch_nn_bounds(const int* list, int cnt, const unsigned* ymax, const unsigned* emax, const float* nrm,
-                      const int* const_range, int N, int m, double* lo, double* hi, cudaStream_t st) {
-    k_nn_bounds<<<grid_for(cnt, 256), 256, 0, st>>>(list, cnt, ymax, emax, nrm, const_range, N, m, lo, hi);
-}
-
-void launch_const_range(const float* nrm, int N, int* out, cudaStream_t st) {
-    k_const_range<<<grid_for(N, 256), 256, 0, st>>>(nrm, N, out);
-}
-
-void launch_const_nn(const int* list, int cnt, const float* nrm, const int* const_range, int N, int m,
-                     unsigned long long* nnkey, cudaStream_t st) {
-    k_const_nn<<<grid_for(cnt, 256), 256, 0, st>>>(list, cnt, nrm, const_range, N, m, nnkey);
-}
-
-void launch_gather_nn(const int* list, int cnt, const unsigned long long* nnkey, double* out,
+void launch_gather_nn(const int* list, const int* cnt, const unsigned long long* nnkey, double* out,
                       cudaStream_t st) {
-    k_gather_nn<<<grid_for(cnt, 256), 256, 0, st>>>(list, cnt, nnkey, out);
+    k_gather_nn<<<kSmallGrid, 256, 0, st>>>(list, cnt, nnkey, out);
 }
 
 }  // namespace tsd

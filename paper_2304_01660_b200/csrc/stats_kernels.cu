@@ -114,13 +114,20 @@ __global__ void k_advance(const double* __restrict__ t, int n, int m, double* __
 // df[i] = (t[i+m-1] - t[i-1]) / 2, dg[i] = (t[i+m-1] - mu_i) + (t[i-1] - mu_{i-1})
 // (centered-covariance diagonal step: cov(i,j) = cov(i-1,j-1) + df_i dg_j + df_j dg_i)
 // nrm[i] = 1 / (sqrt(m) sigma_i), 0 for a constant subsequence.
+// Per-length FP32 walk operands and the constant-row range
+// (cr[0] = max(N - i), cr[1] = max(i + 1) over rows with sigma < eps; cleared
+// to 0 before the launch, 0 meaning none).
 __global__ void k_derive(const double* __restrict__ t, int m, int cnt, const double* __restrict__ mu,
                          const double* __restrict__ sig, float* __restrict__ df,
-                         float* __restrict__ dg, float* __restrict__ nrm) {
+                         float* __restrict__ dg, float* __restrict__ nrm, int* __restrict__ cr) {
     const double sqm = sqrt((double)m);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
         const double s = sig[i];
         nrm[i] = s < kSigmaEps ? 0.f : (float)(1.0 / (sqm * s));
+        if (s < kSigmaEps) {
+            atomicMax(&cr[0], cnt - i);
+            atomicMax(&cr[1], i + 1);
+        }
         if (i == 0) {
             df[0] = 0.f;
             dg[0] = 0.f;
@@ -151,8 +158,9 @@ void launch_advance_stats(const double* t, int n, int m, double* mu, double* sig
 }
 
 void launch_derive(const double* t, int m, int cnt, const double* mu, const double* sig, float* df,
-                   float* dg, float* nrm, cudaStream_t st) {
-    k_derive<<<grid_for(cnt, 256), 256, 0, st>>>(t, m, cnt, mu, sig, df, dg, nrm);
+                   float* dg, float* nrm, int* crange, cudaStream_t st) {
+    cudaMemsetAsync(crange, 0, 2 * sizeof(int), st);
+    k_derive<<<grid_for(cnt, 256), 256, 0, st>>>(t, m, cnt, mu, sig, df, dg, nrm, crange);
 }
 
 }  // namespace tsd

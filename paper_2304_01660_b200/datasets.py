@@ -11,6 +11,8 @@
 """
 from __future__ import annotations
 
+import math
+
 import numpy as np
 
 # (centre as a fraction of the beat, width in samples, amplitude) of P, Q, R, S, T
@@ -18,13 +20,18 @@ _WAVES = ((0.18, 9.0, 0.15), (0.36, 3.5, -0.12), (0.40, 3.0, 1.0), (0.44, 3.5, -
 
 
 def _beat(length: int, amp: float, qrs: bool = True) -> np.ndarray:
-    x = np.arange(length, dtype=np.float64)
-    out = np.zeros(length)
+    # scalar libm exp (math.exp), not numpy's SIMD exp: numpy picks its exp kernel
+    # by the host CPU's features, and the fixture must regenerate bit-identically on
+    # the GPU box's host
+    out = [0.0] * length
     for k, (c, w, a) in enumerate(_WAVES):
         if not qrs and k in (1, 2, 3):
             continue
-        out += a * amp * np.exp(-0.5 * ((x - c * length) / w) ** 2)
-    return out
+        ctr, aa = c * length, a * amp
+        for i in range(length):
+            z = (i - ctr) / w
+            out[i] += aa * math.exp(-0.5 * z * z)
+    return np.asarray(out, dtype=np.float64)
 
 
 def gen_ecg_like(n: int, seed: int, period: int = 250, n_anomalies: int = 10) -> np.ndarray:

@@ -123,6 +123,23 @@ def test_merlin_golden_c4(engine):
     check_merlin(rep, fx)
 
 
+def test_merlin_golden_c3s(engine):
+    # BASELINE config 3 (ECG-like n=500,000), its first 64 lengths (64..127):
+    # quasi-periodic data with injected anomalies, the hardest case for pruning
+    fx = load_golden("c3s.json")
+    engine.set_series(series_of(fx["input"]))
+    rep = engine.merlin_full(fx["min_len"], fx["max_len"], top_k=fx["top_k"], seglen=fx["seglen"])
+    check_merlin(rep, fx)
+
+
+def test_merlin_golden_c5s(engine):
+    # BASELINE config 5 (n=2,000,000 random walk, top-3), its first 32 lengths
+    fx = load_golden("c5s.json")
+    engine.set_series(series_of(fx["input"]))
+    rep = engine.merlin_full(fx["min_len"], fx["max_len"], top_k=fx["top_k"], seglen=fx["seglen"])
+    check_merlin(rep, fx)
+
+
 @pytest.mark.slow
 def test_merlin_golden_c5(engine):
     # BASELINE config 5: n=2,000,000 random walk, lengths 128..640, top-3
