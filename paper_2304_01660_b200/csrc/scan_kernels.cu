@@ -195,8 +195,9 @@ __device__ __noinline__ void slow_track(const F9 x, const F9 qn, float tz, float
 
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(const ScanParams p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    ScanSmem& S = *reinterpret_cast<ScanSmem*>(smem_raw);
+    // static shared memory (33 KB): CTA-relative LDS addressing, no shared
+    // window base to rematerialise inside the walk
+    __shared__ ScanSmem S;
     const int tid = threadIdx.x;
     const long long slots = tile_slots(p);
     // persistent CTAs: slots are fetched dynamically; rank r owns slots r, r+world, ...
@@ -1342,10 +1343,10 @@ static int grid_for(long long work, int threads) {
 size_t scan_smem_bytes() { return sizeof(ScanSmem); }
 
 void scan_configure() {
-    const int bytes = (int)sizeof(ScanSmem);
-    cudaFuncSetAttribute(k_scan<kPrune>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    cudaFuncSetAttribute(k_scan<kPruneTrack>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    cudaFuncSetAttribute(k_scan<kCollect>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    // the walk kernels want the largest shared-memory carveout (6 CTAs x 33 KB)
+    cudaFuncSetAttribute(k_scan<kPrune>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_scan<kPruneTrack>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_scan<kCollect>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 
 // persistent scan: one CTA per resident slot (occupancy of each mode)
@@ -1357,18 +1358,17 @@ static int scan_grid() {
         int dev = 0, sms = 148, per = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_scan<MODE>, kThreads, sizeof(ScanSmem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_scan<MODE>, kThreads, 0);
         g_scan_grid[MODE] = sms * (per > 0 ? per : 1);
     }
     return g_scan_grid[MODE];
 }
 
 void launch_scan(int mode, const ScanParams& p, cudaStream_t st) {
-    const size_t sm = sizeof(ScanSmem);
     switch (mode) {
-        case kPrune: k_scan<kPrune><<<scan_grid<kPrune>(), kThreads, sm, st>>>(p); break;
-        case kPruneTrack: k_scan<kPruneTrack><<<scan_grid<kPruneTrack>(), kThreads, sm, st>>>(p); break;
-        default: k_scan<kCollect><<<scan_grid<kCollect>(), kThreads, sm, st>>>(p); break;
+        case kPrune: k_scan<kPrune><<<scan_grid<kPrune>(), kThreads, 0, st>>>(p); break;
+        case kPruneTrack: k_scan<kPruneTrack><<<scan_grid<kPruneTrack>(), kThreads, 0, st>>>(p); break;
+        default: k_scan<kCollect><<<scan_grid<kCollect>(), kThreads, 0, st>>>(p); break;
     }
 }
 
