@@ -74,6 +74,7 @@ typedef struct {
     double total_ms;        /* device time of the last merlin/pardrag call (CUDA events) */
     double host_wall_ms;    /* host wall time inside DRAG tries */
     double host_wait_ms;    /* ... of which blocked in stream synchronisation */
+    double heatmap_ms;      /* device time of the last heatmap column-max pass */
 } tsd_counters;
 
 /* ---- context ------------------------------------------------------------ */
@@ -134,6 +135,29 @@ int tsd_merlin(tsd_ctx* ctx, int64_t min_len, int64_t max_len, const tsd_merlin_
  * brute_force_nn (drag.hpp:38; src/drag.cpp:137-149): exact nn^2 of every
  * subsequence (n-m+1 values) with the reference arithmetic. */
 int tsd_brute_force_nn(tsd_ctx* ctx, int64_t m, double* out);
+
+/* ---- heatmap / ranking on the device (heatmap.hpp) ------------------------
+ * One ranked column: replaces tsdiscord::RankedDiscord (include/tsdiscord/heatmap.hpp:35-39). */
+typedef struct {
+    int64_t index;  /* 1-based start index */
+    int64_t length; /* length of the column maximum (smallest on ties) */
+    double score;   /* nn_dist_sq / (2m) */
+} tsd_ranked;
+
+/* Builds the score matrix of a discord set on the device and keeps it there
+ * (build_heatmap, src/heatmap.cpp:18-31; Heatmap(minL, maxL, n) preconditions
+ * src/heatmap.cpp:10-15 -> TSD_EINVAL).  Records: `count` entries, lengths[e]
+ * the discord length of recs[e]; a record whose index exceeds n-minL is
+ * dropped, later duplicates of a cell win.  scores_out (nullable) receives the
+ * (maxL-minL+1) x (n-minL) row-major matrix. */
+int tsd_heatmap_build(tsd_ctx* ctx, int64_t min_len, int64_t max_len, int64_t n, const int64_t* lengths,
+                      const tsd_record* recs, int64_t count, double* scores_out);
+/* Replaces the device score matrix with a host one (same shape rules). */
+int tsd_heatmap_set(tsd_ctx* ctx, int64_t min_len, int64_t max_len, int64_t n, const double* scores);
+/* rank_discords (src/heatmap.cpp:33-57): per-column maximum over lengths on
+ * the device, columns ordered by (score desc, index asc, length asc), at most
+ * k, non-zero only.  k < 1 -> TSD_EINVAL.  `out` must hold min(k, n-minL). */
+int tsd_heatmap_rank(tsd_ctx* ctx, int64_t k, tsd_ranked* out, int64_t* count);
 
 /* ---- host utilities the reference API also exposes (io.hpp) --------------
  * gen_randomwalk: src/io.cpp:110-119 (libstdc++ mt19937_64 + normal_distribution). */

@@ -13,6 +13,8 @@
 //   tsdref_pardrag          -> tsdiscord::pardrag (overload) (proj/src/pardrag.cpp:429-434)
 //   tsdref_merlin           -> tsdiscord::merlin_full        (proj/src/merlin.cpp:57-132)
 //   tsdref_discords_csv     -> tsdiscord::write_discords_csv (proj/src/io.cpp:121-130)
+//   tsdref_heatmap          -> read_discords_csv + build_heatmap + rank_discords and the three
+//                              writers (proj/src/io.cpp:132-160, proj/src/heatmap.cpp:18-83)
 #include <cstdint>
 #include <cstring>
 #include <sstream>
@@ -21,6 +23,7 @@
 #include <vector>
 
 #include "tsdiscord/drag.hpp"
+#include "tsdiscord/heatmap.hpp"
 #include "tsdiscord/io.hpp"
 #include "tsdiscord/merlin.hpp"
 #include "tsdiscord/pardrag.hpp"
@@ -150,6 +153,27 @@ int64_t tsdref_merlin_csv(const double* x, int64_t n, int64_t min_len, int64_t m
         o.workers = workers;
         std::ostringstream os;
         write_discords_csv(merlin(s, min_len, max_len, o), os);
+        const std::string str = os.str();
+        if (cap >= static_cast<int64_t>(str.size())) std::memcpy(buf, str.data(), str.size());
+        return static_cast<int64_t>(str.size());
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// Heatmap outputs of a discord CSV, as the reference CLI writes them
+// (tools/main.cpp:111-136): which = 0 heatmap CSV, 1 PGM, 2 ranking CSV (k).
+// Returns the byte length (call with cap=0 to size), -1 on error.
+int64_t tsdref_heatmap(const char* csv, int64_t n, int64_t k, int which, char* buf, int64_t cap) {
+    try {
+        std::istringstream in(csv);
+        const MultiLengthDiscordSet d = read_discords_csv(in);
+        const Heatmap h = build_heatmap(d, n);
+        std::ostringstream os;
+        if (which == 0) write_heatmap_csv(h, os);
+        else if (which == 1) write_heatmap_pgm(h, os);
+        else write_ranking_csv(rank_discords(h, k), os);
         const std::string str = os.str();
         if (cap >= static_cast<int64_t>(str.size())) std::memcpy(buf, str.data(), str.size());
         return static_cast<int64_t>(str.size());

@@ -118,6 +118,16 @@ class Ref(_Common):
                                   C.POINTER(_i64)])
         self._csv = self._fn("merlin_csv", _i64, [_dp, _i64, _i64, _i64, _i64, _i64, _i64,
                                                   C.c_char_p, _i64])
+        self._hm = self._fn("heatmap", _i64, [C.c_char_p, _i64, _i64, C.c_int, C.c_char_p, _i64])
+
+    def heatmap(self, csv: str, n: int, k: int = 10, which: int = 0) -> bytes:
+        """The reference CLI's heatmap outputs: 0 heatmap CSV, 1 PGM, 2 ranking CSV."""
+        size = self._hm(csv.encode(), n, k, which, None, 0)
+        if size < 0:
+            raise CheckerError(3, self.lib.tsdref_last_error().decode())
+        buf = C.create_string_buffer(size + 1)
+        self._hm(csv.encode(), n, k, which, buf, size)
+        return buf.raw[:size]
 
     def pardrag(self, x, m: int, r_sq: float, seglen: int, workers: int = 1) -> np.ndarray:
         x = _as_series(x)

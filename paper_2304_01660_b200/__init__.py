@@ -38,6 +38,9 @@ class LogicError(RuntimeError):
     """std::logic_error of the reference (e.g. merlin.cpp:19 window too short)."""
 
 
+RANKED_DTYPE = np.dtype([("index", np.int64), ("length", np.int64), ("score", np.float64)])
+
+
 class _Opts(C.Structure):
     _fields_ = [("top_k", C.c_int64), ("seglen", C.c_int64), ("workers", C.c_int64),
                 ("max_retries", C.c_int64), ("reuse_stats", C.c_int32)]
@@ -50,7 +53,8 @@ class Counters(C.Structure):
                 ("kernel_launches", C.c_uint64), ("host_syncs", C.c_uint64),
                 ("scan_ms", C.c_double), ("dense_ms", C.c_double), ("sparse_ms", C.c_double),
                 ("collect_ms", C.c_double), ("total_ms", C.c_double),
-                ("host_wall_ms", C.c_double), ("host_wait_ms", C.c_double)]
+                ("host_wall_ms", C.c_double), ("host_wait_ms", C.c_double),
+                ("heatmap_ms", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -99,6 +103,9 @@ def load_library(path: str = LIB_PATH):
     f("tsd_reset_counters", C.c_int, [vp])
     f("tsd_set_param", C.c_int, [vp, C.c_char_p, C.c_double])
     f("tsd_fp32_peak_probe", C.c_int, [C.c_int, C.POINTER(C.c_double)])
+    f("tsd_heatmap_build", C.c_int, [vp, _i64, _i64, _i64, _ip, vp, _i64, vp])
+    f("tsd_heatmap_set", C.c_int, [vp, _i64, _i64, _i64, _dp])
+    f("tsd_heatmap_rank", C.c_int, [vp, _i64, vp, C.POINTER(_i64)])
     _lib = L
     return L
 
@@ -271,6 +278,43 @@ class Engine:
         rep.device_ms = self.counters()["total_ms"]
         return rep
 
+    # -- heatmap / ranking (heatmap.hpp) ---------------------------------------
+    def heatmap(self, per_length: dict, n: int, min_len: int | None = None, max_len: int | None = None,
+                scores: bool = False):
+        """build_heatmap (heatmap.cpp:18-31) on the device; returns the
+        (rows, cols) score matrix when `scores`, else None (it stays resident
+        for heatmap_rank)."""
+        lens = sorted(per_length)
+        if min_len is None:
+            min_len = lens[0] if lens else 0
+        if max_len is None:
+            max_len = lens[-1] if lens else -1
+        ls, rs = [], []
+        for m in lens:
+            for r in per_length[m]:
+                ls.append(m)
+                rs.append((int(r["index"]), float(r["nn_dist_sq"]), float(r["nn_dist"])))
+        recs = np.array(rs, dtype=RECORD_DTYPE) if rs else np.zeros(1, RECORD_DTYPE)
+        lens_a = np.array(ls if ls else [0], dtype=np.int64)
+        out = None
+        if scores and min_len >= 3 and max_len >= min_len and n > max_len:
+            out = np.empty((max_len - min_len + 1, n - min_len))
+        self._check(self._L.tsd_heatmap_build(self._h, min_len, max_len, n, lens_a, recs.ctypes.data, len(rs),
+                                              out.ctypes.data if out is not None else None))
+        return out
+
+    def heatmap_set(self, scores, min_len: int, max_len: int, n: int):
+        sc = np.ascontiguousarray(scores, dtype=np.float64)
+        self._check(self._L.tsd_heatmap_set(self._h, min_len, max_len, n, sc.ravel()))
+
+    def heatmap_rank(self, k: int) -> np.ndarray:
+        """rank_discords (heatmap.cpp:33-57): per-column max on the device."""
+        cap = max(int(k), 1)
+        out = np.zeros(cap, RANKED_DTYPE)
+        cnt = C.c_int64(0)
+        self._check(self._L.tsd_heatmap_rank(self._h, k, out.ctypes.data, C.byref(cnt)))
+        return out[: cnt.value].copy()
+
     # -- accounting / knobs ---------------------------------------------------
     def counters(self) -> dict:
         c = Counters()
@@ -350,3 +394,32 @@ def discords_csv(per_length: dict) -> str:
             lines.append(f"{m},{int(r['index'])},{format_double(r['nn_dist'])},"
                          f"{format_double(r['nn_dist_sq'])},{format_double(r['nn_dist_sq'] / (2.0 * m))}")
     return "\n".join(lines) + "\n"
+
+
+def ranking_csv(ranking) -> str:
+    """write_ranking_csv (heatmap.cpp:76-82)."""
+    lines = ["rank,index,length,score"]
+    for r, e in enumerate(ranking):
+        lines.append(f"{r + 1},{int(e['index'])},{int(e['length'])},{format_double(e['score'])}")
+    return "\n".join(lines) + "\n"
+
+
+def read_discords_csv(text: str) -> dict:
+    """read_discords_csv (io.cpp:132-160): {length: records} in file order."""
+    out: dict = {}
+    for no, line in enumerate(text.splitlines(), 1):
+        if not line.strip():
+            continue
+        if no == 1:
+            if not line.startswith("length,"):
+                raise RuntimeError(f"discord CSV: unexpected header '{line}'")
+            continue
+        f = line.split(",")
+        if len(f) < 4:
+            raise RuntimeError(f"discord CSV line {no}: expected at least 4 fields")
+        try:
+            m, idx, d, d2 = float(f[0]), float(f[1]), float(f[2]), float(f[3])
+        except ValueError:
+            raise RuntimeError(f"discord CSV line {no}: non-numeric field") from None
+        out.setdefault(int(m), []).append((int(idx), d2, d))
+    return {m: np.array(v, dtype=RECORD_DTYPE) for m, v in out.items()}

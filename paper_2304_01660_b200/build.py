@@ -18,6 +18,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libtsdiscord_b200.so")
+CLI = os.path.join(HERE, "tsdiscord")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -26,7 +27,7 @@ CU_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xc
 CXX_FLAGS = ["-O3", "-std=gnu++20", "-fPIC", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC,
              "-I/usr/local/cuda/include"]
 
-SOURCES = ["stats_kernels.cu", "scan_kernels.cu", "probe.cu", "engine.cu", "api.cpp"]
+SOURCES = ["stats_kernels.cu", "scan_kernels.cu", "heatmap_kernels.cu", "probe.cu", "engine.cu", "api.cpp"]
 HEADERS = ["common.cuh", "engine_internal.h", "nccl_shim.h"]
 
 
@@ -68,6 +69,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
             changed = True
     if changed:
         _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-ldl"])
+    # the command-line front end (tools/tsdiscord.cpp), linked against the library
+    cli_src = os.path.join(ROOT, "tools", "tsdiscord.cpp")
+    if os.path.exists(cli_src) and (changed or _newer(cli_src, CLI, deps)):
+        _run(["g++", *CXX_FLAGS, "-o", CLI, cli_src, "-L" + HERE, "-ltsdiscord_b200", "-Wl,-rpath,$ORIGIN"])
     return LIB
 
 

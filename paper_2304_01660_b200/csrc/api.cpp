@@ -12,12 +12,14 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <istream>
 #include <memory>
 #include <ostream>
 #include <sstream>
 #include <string>
 
 #include "tsdiscord/drag.hpp"
+#include "tsdiscord/heatmap.hpp"
 #include "tsdiscord/io.hpp"
 #include "tsdiscord/merlin.hpp"
 #include "tsdiscord/pardrag.hpp"
@@ -287,6 +289,103 @@ std::vector<std::string> split_csv(const std::string& line) {
     return f;
 }
 }  // namespace
+
+MultiLengthDiscordSet read_discords_csv(std::istream& in) {
+    // src/io.cpp:132-160: header "length,...", then length,index,nn_dist,nn_dist_sq[,score]
+    MultiLengthDiscordSet set;
+    std::string line;
+    long lineno = 0;
+    while (std::getline(in, line)) {
+        ++lineno;
+        if (strip(line).empty()) continue;
+        if (lineno == 1) {
+            if (line.rfind("length,", 0) != 0) throw std::runtime_error("discord CSV: unexpected header '" + line + "'");
+            continue;
+        }
+        const auto f = split_csv(line);
+        if (f.size() < 4)
+            throw std::runtime_error("discord CSV line " + std::to_string(lineno) + ": expected at least 4 fields");
+        double m, idx, d, d2;
+        if (!to_double(f[0], m) || !to_double(f[1], idx) || !to_double(f[2], d) || !to_double(f[3], d2))
+            throw std::runtime_error("discord CSV line " + std::to_string(lineno) + ": non-numeric field");
+        set.per_length[(index_t)m].push_back(DiscordRecord{(index_t)idx, d2, d});
+    }
+    if (!set.per_length.empty()) {
+        set.min_len = set.per_length.begin()->first;
+        set.max_len = set.per_length.rbegin()->first;
+    }
+    return set;
+}
+
+// ---- heatmap (reference: src/heatmap.cpp; built and ranked on the GPU) ---------
+namespace {
+std::uint64_t& heatmap_gen() {
+    thread_local std::uint64_t g = 0;
+    return g;
+}
+}  // namespace
+
+Heatmap::Heatmap(index_t min_len, index_t max_len, index_t n) : min_len_(min_len), max_len_(max_len), n_(n) {
+    if (min_len < 3 || min_len > max_len || max_len >= n) throw std::invalid_argument("heatmap: invalid length range");
+    scores_.assign(static_cast<std::size_t>(rows() * cols()), 0.0);
+}
+
+Heatmap build_heatmap(const MultiLengthDiscordSet& discords, index_t n) {
+    Heatmap h(discords.min_len, discords.max_len, n);
+    std::vector<int64_t> lens;
+    std::vector<tsd_record> recs;
+    for (const auto& [m, lst] : discords.per_length)
+        for (const auto& r : lst) {
+            lens.push_back(m);
+            recs.push_back(tsd_record{(int64_t)r.index, r.nn_dist_sq, r.nn_dist});
+        }
+    Ctx& c = ctx();
+    c.check(tsd_heatmap_build(c.c, h.min_len(), h.max_len(), n, lens.data(), recs.data(), (int64_t)recs.size(),
+                              h.mutable_scores().data()));
+    h.set_device_gen(++heatmap_gen());
+    return h;
+}
+
+std::vector<RankedDiscord> rank_discords(const Heatmap& heatmap, index_t k) {
+    if (k < 1) throw std::invalid_argument("rank_discords: k must be positive");
+    Ctx& c = ctx();
+    if (heatmap.device_gen() == 0 || heatmap.device_gen() != heatmap_gen()) {
+        c.check(tsd_heatmap_set(c.c, heatmap.min_len(), heatmap.max_len(), heatmap.n(), heatmap.scores().data()));
+        heatmap.set_device_gen(++heatmap_gen());
+    }
+    std::vector<tsd_ranked> buf((size_t)std::min<index_t>(k, std::max<index_t>(heatmap.cols(), 1)));
+    int64_t cnt = 0;
+    c.check(tsd_heatmap_rank(c.c, k, buf.data(), &cnt));
+    std::vector<RankedDiscord> out((size_t)cnt);
+    for (int64_t e = 0; e < cnt; ++e) out[(size_t)e] = RankedDiscord{(index_t)buf[e].index, (index_t)buf[e].length, buf[e].score};
+    return out;
+}
+
+void write_heatmap_csv(const Heatmap& h, std::ostream& out) {
+    for (index_t m = h.min_len(); m <= h.max_len(); ++m) {
+        for (index_t i = 1; i <= h.cols(); ++i) {
+            if (i > 1) out << ',';
+            out << format_double(h.score(m, i));
+        }
+        out << '\n';
+    }
+}
+
+void write_heatmap_pgm(const Heatmap& h, std::ostream& out) {
+    out << "P5\n" << h.cols() << ' ' << h.rows() << "\n255\n";
+    for (index_t m = h.min_len(); m <= h.max_len(); ++m)
+        for (index_t i = 1; i <= h.cols(); ++i) {
+            const double v = std::clamp(h.score(m, i) / 2.0, 0.0, 1.0);
+            out.put(static_cast<char>(static_cast<unsigned char>(std::lround(v * 255.0))));
+        }
+}
+
+void write_ranking_csv(const std::vector<RankedDiscord>& ranking, std::ostream& out) {
+    out << "rank,index,length,score\n";
+    for (std::size_t r = 0; r < ranking.size(); ++r)
+        out << (r + 1) << ',' << ranking[r].index << ',' << ranking[r].length << ',' << format_double(ranking[r].score)
+            << '\n';
+}
 
 TimeSeries load_series(const std::string& path, const std::string& column) {
     std::ifstream in(path);

@@ -134,7 +134,7 @@ struct tsd_ctx {
 
     // tuning
     bool debug = std::getenv("TSD_DEBUG") != nullptr;
-    int dense_rows = 512;
+    int dense_rows = 0;  // rows per band-0 block; 0: auto (block_rows)
     int sparse_rows = 0;   // 0: choose by cost model (on the device)
     int band_passes = 40;  // cap on band passes (incl. pass 0) enqueued per try; full rows cover the rest
     int band_hint = 0;     // adaptive count: passes the previous try needed (0: none yet)
@@ -145,6 +145,14 @@ struct tsd_ctx {
     // accounting
     tsd_counters ctr{};
     cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+
+    // heatmap (device-resident score matrix)
+    DBuf<double> hm;
+    int64_t hm_min = 0, hm_max = -1, hm_n = 0;
+    DBuf<HmCol> hm_cols;
+    DBuf<unsigned long long> hm_cnt;
+    DBuf<int64_t> hm_rows, hm_idx;
+    DBuf<double> hm_vals;
 
     // multi-GPU (segment-sharded tiles; flags / maxima / minima all-reduced)
     int rank = 0, world = 1;
@@ -207,10 +215,24 @@ struct tsd_ctx {
         derived_m = m;
     }
 
+    // Rows per band-0 block: 512 when the blocks fill the persistent grid about
+    // twice over, else smaller blocks (128/256) so that small series still
+    // occupy every SM (band 0 is one wave of tiles).
+    int block_rows(int64_t N) const {
+        if (dense_rows > 0) return dense_rows;
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t want = 2 * 6 * (int64_t)sms;  // two waves of the 6-CTA/SM scan grid
+        for (int L = kMaxRows; L > 128; L /= 2)
+            if (2 * ((N + L - 1) / L) >= want) return L;
+        return 128;
+    }
+
     // ---- resident seed rows ----------------------------------------------
     void seed_init(int64_t m, int64_t kA) {
         const int64_t N = n - m + 1;
-        seed_L = dense_rows;
+        seed_L = block_rows(N);
         seed_kA = (int)kA;
         seed_nb = 2 * (int)((N + seed_L - 1) / seed_L);
         seedqt.ensure((size_t)seed_nb * kW);
@@ -411,7 +433,7 @@ struct tsd_ctx {
                 ++enq_passes;
                 ScanParams q = P;
                 q.pass = pass;
-                if (pass == 0 && seed_m == m && seed_L == dense_rows) {
+                if (pass == 0 && seed_m == m) {
                     // band 0 at the fixed offset kA (>= m for every length of the run)
                     // seeded from the resident rows: no direct dot products
                     q.space = kSpaceSeed;
@@ -423,7 +445,7 @@ struct tsd_ctx {
                         std::min<long long>(1ll << std::min(pass, 5), (k_max - K0 + kW) / kW);
                     if (pass == 0) {
                         q.space = kSpaceBlocks;
-                        q.L = dense_rows;
+                        q.L = block_rows(N);
                     } else {
                         q.space = kSpaceBand;  // groups built by the previous compaction
                     }
@@ -677,6 +699,12 @@ void tsd_ctx_destroy(tsd_ctx* c) {
     c->nnout.release();
     c->groups.release();
     c->slots.release();
+    c->hm.release();
+    c->hm_cols.release();
+    c->hm_cnt.release();
+    c->hm_rows.release();
+    c->hm_idx.release();
+    c->hm_vals.release();
     c->ctl.release();
     c->h_ctl.release();
     c->h_ex.release();
@@ -907,6 +935,110 @@ int tsd_merlin(tsd_ctx* c, int64_t min_len, int64_t max_len, const tsd_merlin_op
     });
 }
 
+namespace {
+// Heatmap(minL, maxL, n) preconditions (src/heatmap.cpp:12-13)
+void hm_shape(tsd_ctx* c, int64_t min_len, int64_t max_len, int64_t n) {
+    if (min_len < 3 || min_len > max_len || max_len >= n) fail(TSD_EINVAL, "heatmap: invalid length range");
+    const int64_t rows = max_len - min_len + 1, cols = n - min_len;
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    c->hm.ensure((size_t)(rows * cols));
+    c->hm_min = min_len;
+    c->hm_max = max_len;
+    c->hm_n = n;
+}
+}  // namespace
+
+int tsd_heatmap_build(tsd_ctx* c, int64_t min_len, int64_t max_len, int64_t n, const int64_t* lengths,
+                      const tsd_record* recs, int64_t count, double* scores_out) {
+    return guard(c, [&] {
+        hm_shape(c, min_len, max_len, n);
+        const int64_t rows = max_len - min_len + 1, cols = n - min_len;
+        ck(cudaMemsetAsync(c->hm.p, 0, (size_t)(rows * cols) * sizeof(double), c->st), "memset");
+        // cells in record order; a later record of the same cell wins (set_score
+        // overwrites), so duplicates are resolved here and the scatter is conflict-free
+        std::vector<int64_t> r, i;
+        std::vector<double> v;
+        std::vector<std::pair<int64_t, int64_t>> order;  // (cell, position)
+        for (int64_t e = 0; e < count; ++e) {
+            const int64_t m = lengths[e], idx = recs[e].index;
+            if (m < min_len || m > max_len || idx < 1)
+                fail(TSD_EINVAL, "heatmap: record outside the matrix");
+            if (idx > cols) continue;  // src/heatmap.cpp:26-27
+            order.emplace_back((m - min_len) * cols + (idx - 1), e);
+        }
+        std::stable_sort(order.begin(), order.end(),
+                         [](const auto& a, const auto& b) { return a.first < b.first; });
+        for (size_t k = 0; k < order.size(); ++k) {
+            if (k + 1 < order.size() && order[k + 1].first == order[k].first) continue;  // keep the last
+            const int64_t e = order[k].second, m = lengths[e];
+            r.push_back(m - min_len);
+            i.push_back(recs[e].index - 1);
+            v.push_back(recs[e].nn_dist_sq / (2.0 * (double)m));
+        }
+        const int64_t u = (int64_t)r.size();
+        if (u > 0) {
+            c->hm_rows.ensure(u);
+            c->hm_idx.ensure(u);
+            c->hm_vals.ensure(u);
+            ck(cudaMemcpyAsync(c->hm_rows.p, r.data(), u * sizeof(int64_t), cudaMemcpyHostToDevice, c->st), "H2D");
+            ck(cudaMemcpyAsync(c->hm_idx.p, i.data(), u * sizeof(int64_t), cudaMemcpyHostToDevice, c->st), "H2D");
+            ck(cudaMemcpyAsync(c->hm_vals.p, v.data(), u * sizeof(double), cudaMemcpyHostToDevice, c->st), "H2D");
+            launch_hm_scatter(c->hm_rows.p, c->hm_idx.p, c->hm_vals.p, u, cols, c->hm.p, c->st);
+            ck(cudaGetLastError(), "heatmap scatter");
+        }
+        if (scores_out)
+            ck(cudaMemcpyAsync(scores_out, c->hm.p, (size_t)(rows * cols) * sizeof(double), cudaMemcpyDeviceToHost,
+                               c->st),
+               "D2H");
+        c->sync();
+    });
+}
+
+int tsd_heatmap_set(tsd_ctx* c, int64_t min_len, int64_t max_len, int64_t n, const double* scores) {
+    return guard(c, [&] {
+        hm_shape(c, min_len, max_len, n);
+        const int64_t rows = max_len - min_len + 1, cols = n - min_len;
+        ck(cudaMemcpyAsync(c->hm.p, scores, (size_t)(rows * cols) * sizeof(double), cudaMemcpyHostToDevice, c->st),
+           "H2D");
+        c->sync();
+    });
+}
+
+int tsd_heatmap_rank(tsd_ctx* c, int64_t k, tsd_ranked* out, int64_t* count) {
+    return guard(c, [&] {
+        if (k < 1) fail(TSD_EINVAL, "rank_discords: k must be positive");
+        if (c->hm_max < c->hm_min) fail(TSD_EINVAL, "rank_discords: no heatmap built");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        const int64_t rows = c->hm_max - c->hm_min + 1, cols = c->hm_n - c->hm_min;
+        c->hm_cols.ensure((size_t)cols);
+        c->hm_cnt.ensure(1);
+        ck(cudaMemsetAsync(c->hm_cnt.p, 0, sizeof(unsigned long long), c->st), "memset");
+        ck(cudaEventRecord(c->ev_a, c->st), "event");
+        launch_hm_colmax(c->hm.p, rows, cols, c->hm_min, c->hm_cols.p, c->hm_cnt.p, c->st);
+        ck(cudaGetLastError(), "heatmap colmax");
+        ck(cudaEventRecord(c->ev_b, c->st), "event");
+        unsigned long long nz = 0;
+        ck(cudaMemcpyAsync(&nz, c->hm_cnt.p, sizeof(nz), cudaMemcpyDeviceToHost, c->st), "D2H");
+        c->sync();
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c->ev_a, c->ev_b);
+        c->ctr.heatmap_ms = ms;
+        std::vector<HmCol> v((size_t)nz);
+        if (nz)
+            ck(cudaMemcpyAsync(v.data(), c->hm_cols.p, nz * sizeof(HmCol), cudaMemcpyDeviceToHost, c->st), "D2H");
+        c->sync();
+        // ranking order (src/heatmap.cpp:48-53)
+        std::sort(v.begin(), v.end(), [](const HmCol& a, const HmCol& b) {
+            if (a.score != b.score) return a.score > b.score;
+            if (a.index != b.index) return a.index < b.index;
+            return a.length < b.length;
+        });
+        const int64_t keep = std::min<int64_t>(k, (int64_t)v.size());
+        for (int64_t e = 0; e < keep; ++e) out[e] = tsd_ranked{v[e].index, v[e].length, v[e].score};
+        *count = keep;
+    });
+}
+
 int tsd_gen_randomwalk(int64_t n, uint64_t seed, double* out) {
     return guard(nullptr, [&] {
         // src/io.cpp:110-119 — same engine and distribution (libstdc++)
@@ -933,7 +1065,7 @@ int tsd_reset_counters(tsd_ctx* c) {
 int tsd_set_param(tsd_ctx* c, const char* key, double v) {
     return guard(c, [&] {
         const std::string k = key ? key : "";
-        if (k == "dense_rows") c->dense_rows = std::max(16, std::min(kMaxRows, (int)v));
+        if (k == "dense_rows") c->dense_rows = v <= 0 ? 0 : std::max(16, std::min(kMaxRows, (int)v));
         else if (k == "sparse_rows") c->sparse_rows = std::max(0, std::min(kMaxRows, (int)v));
         else if (k == "err_scale") c->err_k = v;
         else if (k == "band_keep") c->band_keep = (float)std::max(0.0, std::min(1.0, v));

@@ -42,4 +42,15 @@ void launch_seed_advance(const double* t, int n, int m, int L, int kA, int nb, d
 void launch_gather_nn(const int* list, const int* cnt, const unsigned long long* nnkey, double* out,
                       cudaStream_t st);
 
+// heatmap (heatmap_kernels.cu)
+struct HmCol {
+    int64_t index;   // 1-based start index
+    int64_t length;  // first length reaching the column maximum
+    double score;    // column maximum
+};
+void launch_hm_scatter(const int64_t* rows, const int64_t* cols_idx, const double* vals, int64_t count,
+                       int64_t ncols, double* hm, cudaStream_t st);
+void launch_hm_colmax(const double* hm, int64_t nrows, int64_t ncols, int64_t min_len, HmCol* out,
+                      unsigned long long* count, cudaStream_t st);
+
 }  // namespace tsd

@@ -1,0 +1,78 @@
+// Heatmap / ranking of a multi-length discord set on the device (SURVEY §8f
+// rank 2; reference src/heatmap.cpp:18-57, PAPER Eq. 10/11).
+//
+// The score matrix is rows = lengths minL..maxL x cols = start indices
+// 1..n-minL, row-major FP64 (C4: 513 x 999,488 = 4.1 GB, resident in HBM).
+// Building it is a scatter of the (few) records into a zeroed matrix; the
+// ranking needs every column's maximum over the lengths, one HBM-bound pass
+// over the whole matrix (k_hm_colmax), followed by a host sort of the
+// non-zero columns (at most one per record).
+#include <stdint.h>
+
+#include "engine_internal.h"
+
+namespace tsd {
+
+__global__ void k_hm_scatter(const int64_t* __restrict__ rows, const int64_t* __restrict__ cols_idx,
+                             const double* __restrict__ vals, int64_t count, int64_t ncols,
+                             double* __restrict__ hm) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
+         e += (int64_t)gridDim.x * blockDim.x)
+        hm[rows[e] * ncols + cols_idx[e]] = vals[e];
+}
+
+// Per column: the largest score and the first (smallest) length reaching it
+// (heatmap.cpp:37-45 keeps the first strict maximum over ascending lengths).
+// Thread per column; a warp reads 32 consecutive doubles of a row, the row
+// loop is unrolled for memory-level parallelism.
+__global__ void __launch_bounds__(256) k_hm_colmax(const double* __restrict__ hm, int64_t nrows, int64_t ncols,
+                                                   int64_t min_len, HmCol* __restrict__ out,
+                                                   unsigned long long* __restrict__ count) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ncols;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double best = 0.0;
+        int64_t len = 0;
+        int64_t r = 0;
+        for (; r + 8 <= nrows; r += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldcs(&hm[(r + u) * ncols + i]);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (v[u] > best) {
+                    best = v[u];
+                    len = min_len + r + u;
+                }
+        }
+        for (; r < nrows; ++r) {
+            const double v = __ldcs(&hm[r * ncols + i]);
+            if (v > best) {
+                best = v;
+                len = min_len + r;
+            }
+        }
+        if (best > 0.0) {
+            const unsigned long long at = atomicAdd(count, 1ull);
+            out[at] = HmCol{i + 1, len, best};
+        }
+    }
+}
+
+void launch_hm_scatter(const int64_t* rows, const int64_t* cols_idx, const double* vals, int64_t count,
+                       int64_t ncols, double* hm, cudaStream_t st) {
+    if (count <= 0) return;
+    const int64_t b = (count + 255) / 256;
+    k_hm_scatter<<<(int)(b < 4096 ? b : 4096), 256, 0, st>>>(rows, cols_idx, vals, count, ncols, hm);
+}
+
+void launch_hm_colmax(const double* hm, int64_t nrows, int64_t ncols, int64_t min_len, HmCol* out,
+                      unsigned long long* count, cudaStream_t st) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t need = (ncols + 255) / 256;
+    const int64_t grid = need < (int64_t)sms * 8 ? need : (int64_t)sms * 8;
+    k_hm_colmax<<<(int)(grid > 0 ? grid : 1), 256, 0, st>>>(hm, nrows, ncols, min_len, out, count);
+}
+
+}  // namespace tsd

@@ -489,6 +489,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
 
     float4 cr_next = crp[0];  // row operands are prefetched one step ahead
     for (int s0 = 0; s0 < rows_p; s0 += kDiag) {
+        unsigned hit = 0u;  // kPrune: steps of this block whose row is certainly killed
 #pragma unroll
         for (int uu = 0; uu < kDiag; ++uu) {
             const int ss = s0 + uu;
@@ -500,7 +501,17 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
                 cov[j] = fmaf(cr.x, rd[rj].y, cov[j]);
                 cov[j] = fmaf(rd[rj].x, cr.y, cov[j]);
             }
-            if (cr.z != kNoEval) {  // CTA-uniform branch: the row is undecided
+            if (MODE == kPrune) {
+                // band passes evaluate every step branch-free: a decided row has
+                // tc = kNoEval (never exceeded), and the kill stores wait for the
+                // end of the 9-step block.  The max is a depth-2 FMNMX3 tree.
+                float x[kDiag];
+#pragma unroll
+                for (int j = 0; j < kDiag; ++j) x[j] = cov[j] * rn[(j + uu) % kDiag];
+                const float mx = fmaxf(fmaxf(fmaxf(fmaxf(x[0], x[1]), x[2]), fmaxf(fmaxf(x[3], x[4]), x[5])),
+                                       fmaxf(fmaxf(x[6], x[7]), x[8]));
+                hit |= (mx > cr.z ? 1u : 0u) << uu;
+            } else if (cr.z != kNoEval) {  // CTA-uniform branch: the row is undecided
                 float x[kDiag];
                 float mx = -FLT_MAX;
 #pragma unroll
@@ -508,11 +519,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
                     x[j] = cov[j] * rn[(j + uu) % kDiag];
                     mx = fmaxf(mx, x[j]);
                 }
-                if (MODE == kPrune) {
-                    // certain kill of the row candidate (FP32 only; constant rows are
-                    // not evaluated in band passes): a predicated store, no branch
-                    if (mx > cr.z) p.alive[dir > 0 ? td.r0 + ss : r_end - ss] = 0;
-                } else if (MODE == kPruneTrack) {
+                if (MODE == kPruneTrack) {
                     if (mx > cr.z) {
                         // rare: kills, knife edges, constant conventions (out of line)
                         F9 xv, qv;
@@ -551,6 +558,15 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
             // slide: slot kDiag-1 of step ss+1 is u = ss + 1 + ub + kDiag - 1
             rd[uu % kDiag] = qdp[ss + kDiag];
             rn[uu % kDiag] = qnp[ss + kDiag];
+        }
+        if (MODE == kPrune && hit) {
+            // certain kills of the row candidates (FP32 only)
+            do {
+                const int uu = __ffs(hit) - 1;
+                hit &= hit - 1;
+                const int ss = s0 + uu;
+                p.alive[dir > 0 ? td.r0 + ss : r_end - ss] = 0;
+            } while (hit);
         }
     }
 

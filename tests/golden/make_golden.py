@@ -104,6 +104,15 @@ def small(R):
     ]
     fx["csv_acceptance_c2"] = R.merlin_csv(R.gen_randomwalk(3000, 2024), 8, 24, top_k=2,
                                            seglen=128, workers=4)
+    # heatmap / ranking of that discord CSV (the reference CLI's `heatmap` outputs)
+    import hashlib
+    hm = {}
+    for name, csv, n in [("acceptance_c2", fx["csv_acceptance_c2"], 3000)]:
+        hm[name] = dict(n=n, heatmap_csv_sha256=hashlib.sha256(R.heatmap(csv, n, 10, 0)).hexdigest(),
+                        pgm_sha256=hashlib.sha256(R.heatmap(csv, n, 10, 1)).hexdigest(),
+                        ranking_csv=R.heatmap(csv, n, 10, 2).decode(),
+                        ranking_k3=R.heatmap(csv, n, 3, 2).decode())
+    fx["heatmap"] = hm
     with open(os.path.join(HERE, "small.json"), "w") as f:
         json.dump(fx, f, indent=0)
     print("wrote small.json")
