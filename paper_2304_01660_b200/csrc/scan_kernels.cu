@@ -261,7 +261,9 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
         for (int pc = 0; pc < m; pc += kSeedChunk) {
             const int len = min(kSeedChunk, m - pc);
             __syncthreads();
+#pragma unroll 4
             for (int x = tid; x < len; x += kThreads) S.u.seed32.a[x] = (float)(p.t[c_first + pc + x] - mu_c);
+#pragma unroll 4
             for (int x = tid; x < kW + len - 1; x += kThreads) {
                 const int g = qlo + pc + x;
                 const float w = (g >= 0 && g < p.n) ? (float)(p.t[g] - anchor) : 0.f;
@@ -323,7 +325,9 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
     for (int pc = 0; pc < m; pc += kSeedChunk) {
         const int len = min(kSeedChunk, m - pc);
         __syncthreads();
+#pragma unroll 4
         for (int x = tid; x < len; x += kThreads) S.u.seed.a[x] = p.t[c_first + pc + x] - mu_c;
+#pragma unroll 4
         for (int x = tid; x < kW + len - 1; x += kThreads) {
             const int g = qlo + pc + x;
             S.u.seed.win[x] = (g >= 0 && g < p.n) ? p.t[g] : 0.0;
@@ -367,69 +371,71 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
     __syncthreads();  // seed buffers are reused below
 
     // ---- 2. stage the walk operands ---------------------------------------
-    float smax_c = 0.f, smax_q = 0.f, qn_max = 0.f;
+    // Every iteration's global loads are independent (no load behind a
+    // branch on another load) and the loops are unrolled, so a thread keeps
+    // several loads in flight: the prologue is latency-bound otherwise.  The
+    // largest sigma of each side comes from the smallest non-zero norm,
+    // sigma = 1/(sqrt(m) nrm) up to the FP32 rounding of nrm (factor below).
+    float cn_min = FLT_MAX, qn_min = FLT_MAX, qn_max = 0.f;
+#pragma unroll 4
     for (int s = tid; s < rows; s += kThreads) {
         const int c = dir > 0 ? td.r0 + s : r_end - s;
+        const int ci = dir > 0 ? c : min(c + 1, N - 1);  // s == 0 takes no increment
         float4 v;
-        if (s == 0) {
-            v.x = 0.f;
-            v.y = 0.f;
-        } else if (dir > 0) {
-            v.x = p.df[c];
-            v.y = p.dg[c];
-        } else {
-            v.x = -p.df[c + 1];
-            v.y = -p.dg[c + 1];
-        }
+        const float a = p.df[ci], b = p.dg[ci];
+        v.x = s == 0 ? 0.f : (dir > 0 ? a : -a);
+        v.y = s == 0 ? 0.f : (dir > 0 ? b : -b);
         v.w = p.nrm[c];
         v.z = 0.f;
-        if (v.w != 0.f) smax_c = fmaxf(smax_c, (float)p.sig[c]);
+        if (v.w != 0.f) cn_min = fminf(cn_min, v.w);
         S.crow[s] = v;
     }
     const int rows_p = (rows + kDiag - 1) / kDiag * kDiag;
     for (int s = rows + tid; s <= rows_p; s += kThreads) S.crow[s] = make_float4(0.f, 0.f, FLT_MAX, 0.f);
+#pragma unroll 4
     for (int u = tid; u < rows_p + kW + kDiag; u += kThreads) {
         const int q = dir > 0 ? qbase + u : qbase - u;
-        float a = 0.f, b = 0.f, nn = 0.f;
-        if (u < nq && q >= 0 && q < N) {
-            const int qi = dir > 0 ? q : q + 1;
-            if (qi < N) {
-                a = p.df[qi];
-                b = p.dg[qi];
-            }
-            nn = p.nrm[q];
-            if (nn != 0.f) {
-                smax_q = fmaxf(smax_q, (float)p.sig[q]);
-                qn_max = fmaxf(qn_max, nn);
-            }
+        const bool valid = u < nq && q >= 0 && q < N;
+        const int qc = valid ? q : 0;
+        const int qi = dir > 0 ? qc : min(qc + 1, N - 1);
+        float a = p.df[qi], b = p.dg[qi];
+        const float nn = p.nrm[qc];
+        if (!valid || (dir < 0 && qc + 1 >= N)) {
+            a = 0.f;
+            b = 0.f;
+        }
+        if (valid && nn != 0.f) {
+            qn_min = fminf(qn_min, nn);
+            qn_max = fmaxf(qn_max, nn);
         }
         S.u.walk.qd[u] = make_float2(a, b);
         // an invalid q gets a NaN norm: its x = cov*qn is NaN, which never passes a
         // threshold test and is ignored by fmaxf (a constant q keeps qn = 0, x = 0)
-        S.u.walk.qn[u] = (u < nq && q >= 0 && q < N) ? nn : __int_as_float(0x7fffffff);
+        S.u.walk.qn[u] = valid ? nn : __int_as_float(0x7fffffff);
     }
-    smax_c = warp_max(smax_c);
-    smax_q = warp_max(smax_q);
+    cn_min = -warp_max(-cn_min);
+    qn_min = -warp_max(-qn_min);
     qn_max = warp_max(qn_max);
     if ((tid & 31) == 0) {
-        S.red[0][tid >> 5] = smax_c;
-        S.red[1][tid >> 5] = smax_q;
+        S.red[0][tid >> 5] = cn_min;
+        S.red[1][tid >> 5] = qn_min;
         S.red[2][tid >> 5] = qn_max;
     }
     __syncthreads();
-    smax_c = 0.f;
-    smax_q = 0.f;
+    cn_min = FLT_MAX;
+    qn_min = FLT_MAX;
     qn_max = 0.f;
 #pragma unroll
     for (int w = 0; w < kThreads / 32; ++w) {
-        smax_c = fmaxf(smax_c, S.red[0][w]);
-        smax_q = fmaxf(smax_q, S.red[1][w]);
+        cn_min = fminf(cn_min, S.red[0][w]);
+        qn_min = fminf(qn_min, S.red[1][w]);
         qn_max = fmaxf(qn_max, S.red[2][w]);
     }
+    const double inv_sqm = 1.0 / sqrt((double)m);
+    const double smax_c = cn_min < FLT_MAX ? inv_sqm / (double)cn_min * (1.0 + 1e-6) : 0.0;
+    const double smax_q = qn_min < FLT_MAX ? inv_sqm / (double)qn_min * (1.0 + 1e-6) : 0.0;
     // absolute FP32 covariance error bound for every cell of this tile
-    const double E = p.err_k * (double)kEps32 * (double)m * (double)smax_c * (double)smax_q *
-                         (double)(rows + 8) +
-                     e_seed;
+    const double E = p.err_k * (double)kEps32 * (double)m * smax_c * smax_q * (double)(rows + 8) + e_seed;
     const float Ef = (float)E;
     // Row thresholds.  crow.z = tc: a live row's cells with x = cov*qn > tc may be
     // within the error band of d^2 = r^2 (slow path); kNoEval marks rows whose
