@@ -136,6 +136,27 @@ int tsd_merlin(tsd_ctx* ctx, int64_t min_len, int64_t max_len, const tsd_merlin_
  * subsequence (n-m+1 values) with the reference arithmetic. */
 int tsd_brute_force_nn(tsd_ctx* ctx, int64_t m, double* out);
 
+/* ---- in-process rank group (single process, several GPUs) ----------------
+ * The alternative to tsd_ctx_join + NCCL when one process drives several
+ * devices: rank r owns devices[r] (repeats allowed: several ranks may share a
+ * GPU, which is how the sharded path is tested on one device).  The scan tiles
+ * are dealt cyclically over the ranks and the kill flags / route maxima /
+ * exact-nn keys are all-reduced by one kernel per rank reading every rank's
+ * buffer through peer memory.  Results equal the single-rank ones bit for bit;
+ * the group entry points check that every rank produced the same records
+ * (TSD_ERUNTIME "ranks diverged" otherwise). */
+typedef struct tsd_group tsd_group;
+int tsd_group_create(const int* devices, int n, tsd_group** out);
+void tsd_group_destroy(tsd_group* g);
+const char* tsd_group_last_error(const tsd_group* g);
+int tsd_group_size(const tsd_group* g);
+tsd_ctx* tsd_group_ctx(tsd_group* g, int rank); /* per-rank counters / params */
+int tsd_group_series_set(tsd_group* g, const double* values, int64_t n);
+int tsd_group_merlin(tsd_group* g, int64_t min_len, int64_t max_len, const tsd_merlin_opts* opts,
+                     int64_t* counts, tsd_record* recs, double* final_r, int64_t* retries, uint8_t* failed);
+int tsd_group_pardrag(tsd_group* g, int64_t m, double r_sq, int64_t seglen, tsd_record* out, int64_t cap,
+                      int64_t* count);
+
 /* ---- heatmap / ranking on the device (heatmap.hpp) ------------------------
  * One ranked column: replaces tsdiscord::RankedDiscord (include/tsdiscord/heatmap.hpp:35-39). */
 typedef struct {

@@ -31,6 +31,9 @@ EXPORTS = (
     "tsd_init_stats", "tsd_advance_stats", "tsd_compute_layout", "tsd_next_threshold",
     "tsd_pardrag", "tsd_merlin", "tsd_brute_force_nn", "tsd_gen_randomwalk",
     "tsd_get_counters", "tsd_reset_counters", "tsd_set_param", "tsd_fp32_peak_probe",
+    "tsd_heatmap_build", "tsd_heatmap_set", "tsd_heatmap_rank",
+    "tsd_group_create", "tsd_group_destroy", "tsd_group_last_error", "tsd_group_size", "tsd_group_ctx",
+    "tsd_group_series_set", "tsd_group_merlin", "tsd_group_pardrag",
 )
 
 
@@ -103,6 +106,13 @@ def load_library(path: str = LIB_PATH):
     f("tsd_reset_counters", C.c_int, [vp])
     f("tsd_set_param", C.c_int, [vp, C.c_char_p, C.c_double])
     f("tsd_fp32_peak_probe", C.c_int, [C.c_int, C.POINTER(C.c_double)])
+    f("tsd_group_create", C.c_int, [C.POINTER(C.c_int), C.c_int, C.POINTER(vp)])
+    f("tsd_group_destroy", None, [vp])
+    f("tsd_group_last_error", C.c_char_p, [vp])
+    f("tsd_group_ctx", vp, [vp, C.c_int])
+    f("tsd_group_series_set", C.c_int, [vp, _dp, _i64])
+    f("tsd_group_merlin", C.c_int, [vp, _i64, _i64, C.POINTER(_Opts), _ip, vp, _dp, _ip, _u8])
+    f("tsd_group_pardrag", C.c_int, [vp, _i64, C.c_double, _i64, vp, _i64, C.POINTER(_i64)])
     f("tsd_heatmap_build", C.c_int, [vp, _i64, _i64, _i64, _ip, vp, _i64, vp])
     f("tsd_heatmap_set", C.c_int, [vp, _i64, _i64, _i64, _dp])
     f("tsd_heatmap_rank", C.c_int, [vp, _i64, vp, C.POINTER(_i64)])
@@ -326,6 +336,75 @@ class Engine:
 
     def set_param(self, key: str, value: float):
         self._check(self._L.tsd_set_param(self._h, key.encode(), float(value)))
+
+
+class Group:
+    """In-process rank group (tsd_group_*): rank r runs on devices[r] (repeats
+    allowed), tiles are dealt cyclically over the ranks and reductions go
+    through peer memory.  Same results as Engine, bit for bit."""
+
+    def __init__(self, devices):
+        self._L = load_library()
+        devs = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        rc = self._L.tsd_group_create(devs, len(devices), C.byref(h))
+        if rc != TSD_OK:
+            _raise(rc, (self._L.tsd_create_error() or b"").decode())
+        self._h = h
+        self.size = len(devices)
+        self.n = 0
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.tsd_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != TSD_OK:
+            _raise(rc, (self._L.tsd_group_last_error(self._h) or b"").decode())
+
+    def set_series(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        self._check(self._L.tsd_group_series_set(self._h, x, len(x)))
+        self.n = len(x)
+
+    def counters(self, rank: int = 0) -> dict:
+        c = Counters()
+        self._check(self._L.tsd_get_counters(self._L.tsd_group_ctx(self._h, rank), C.byref(c)))
+        return c.as_dict()
+
+    def pardrag(self, m: int, r_sq: float, seglen: int) -> np.ndarray:
+        N = max(self.n - m + 1, 1)
+        out = np.zeros(N, RECORD_DTYPE)
+        cnt = C.c_int64(0)
+        self._check(self._L.tsd_group_pardrag(self._h, m, float(r_sq), seglen, out.ctypes.data, N, C.byref(cnt)))
+        return out[: cnt.value].copy()
+
+    def merlin_full(self, min_len: int, max_len: int, top_k: int = 1, seglen: int = 512,
+                    max_retries: int = 100, reuse_stats: bool = True) -> MerlinReport:
+        Ln = max(max_len - min_len + 1, 1)
+        k = max(top_k, 1)
+        counts = np.zeros(Ln, np.int64)
+        recs = np.zeros((Ln, k), RECORD_DTYPE)
+        final_r = np.zeros(Ln)
+        retries = np.zeros(Ln, np.int64)
+        failed = np.zeros(Ln, np.uint8)
+        o = _Opts(top_k, seglen, 1, max_retries, 1 if reuse_stats else 0)
+        self._check(self._L.tsd_group_merlin(self._h, min_len, max_len, C.byref(o), counts, recs.ctypes.data,
+                                             final_r, retries, failed))
+        rep = MerlinReport(min_len, max_len, final_r=final_r[:Ln], retries=retries[:Ln])
+        for i in range(max_len - min_len + 1):
+            if failed[i]:
+                rep.failed_lengths.append(min_len + i)
+            else:
+                rep.per_length[min_len + i] = recs[i][: counts[i]].copy()
+        return rep
 
 
 _default: Engine | None = None

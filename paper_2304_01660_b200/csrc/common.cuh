@@ -58,6 +58,7 @@ struct TryCtl {
     int cdone;      // compaction: finished CTAs (self-resetting)
     int ctotal;     // compaction: total of the latest launch
     int xdone;      // exact pass: finished CTAs (self-resetting)
+    int stop_why;   // band loop: 1 nothing / few rows left, 2 a pass killed too few
     double lk;      // top-k filter: need_top-th largest nn lower bound
     double cost[6]; // compaction: grouping cost per span (16..512), self-resetting
 };

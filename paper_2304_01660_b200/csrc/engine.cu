@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <random>
+#include <thread>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -31,6 +32,7 @@
 #include "common.cuh"
 #include "engine_internal.h"
 #include "nccl_shim.h"
+#include "peer_group.cuh"
 
 using namespace tsd;
 
@@ -170,18 +172,43 @@ struct tsd_ctx {
         ctr.host_syncs += 1;
     }
 
-    void allreduce_min_u8(uint8_t* p, size_t cnt) {
-        if (world > 1) nccl_allreduce(comm, p, cnt, 0 /*u8 min*/, st);
+    // Reductions across ranks: NCCL (one process per GPU) or the in-process
+    // peer group (peer_group.cuh).  Every rank reaches them in the same order
+    // with identical sizes: the host control flow depends only on reduced data.
+    PeerGroup* group = nullptr;
+    DBuf<unsigned char> red_tmp;
+
+    void allreduce(void* p, size_t cnt, int kind, size_t esize) {
+        if (world <= 1) return;
+        if (group) {
+            peer_allreduce(p, cnt, kind, esize);
+            return;
+        }
+        if (!nccl_allreduce(comm, p, cnt, kind, st)) fail(TSD_ECUDA, "ncclAllReduce failed");
     }
-    void allreduce_max_u32(unsigned* p, size_t cnt) {
-        if (world > 1) nccl_allreduce(comm, p, cnt, 1 /*u32 max*/, st);
+    void peer_allreduce(void* p, size_t cnt, int kind, size_t esize) {
+        PeerGroup& g = *group;
+        g.ptrs[rank] = p;
+        ck(cudaEventRecord(g.ev_in[rank], st), "event");
+        g.bar.wait();  // every rank's input pointer and event are published
+        PeerPtrs in{};
+        for (int r = 0; r < g.n; ++r) {
+            in.p[r] = g.ptrs[r];
+            if (r != rank) ck(cudaStreamWaitEvent(st, g.ev_in[r], 0), "event wait");
+        }
+        red_tmp.ensure(cnt * esize);
+        launch_peer_reduce(kind, in, g.n, red_tmp.p, cnt, st);
+        ck(cudaGetLastError(), "peer reduce");
+        ck(cudaEventRecord(g.ev_red[rank], st), "event");
+        g.bar.wait();  // no rank overwrites its input before every rank has read it
+        for (int r = 0; r < g.n; ++r)
+            if (r != rank) ck(cudaStreamWaitEvent(st, g.ev_red[r], 0), "event wait");
+        ck(cudaMemcpyAsync(p, red_tmp.p, cnt * esize, cudaMemcpyDeviceToDevice, st), "D2D");
+        ctr.kernel_launches += 1;
     }
-    void allreduce_min_u64(unsigned long long* p, size_t cnt) {
-        if (world > 1) nccl_allreduce(comm, p, cnt, 2 /*u64 min*/, st);
-    }
-    void allreduce_sum_i32(int* p, size_t cnt) {
-        if (world > 1) nccl_allreduce(comm, p, cnt, 3 /*i32 sum*/, st);
-    }
+    void allreduce_min_u8(uint8_t* p, size_t cnt) { allreduce(p, cnt, 0 /*u8 min*/, 1); }
+    void allreduce_max_u32(unsigned* p, size_t cnt) { allreduce(p, cnt, 1 /*u32 max*/, 4); }
+    void allreduce_min_u64(unsigned long long* p, size_t cnt) { allreduce(p, cnt, 2 /*u64 min*/, 8); }
 
     // ---- statistics --------------------------------------------------
     void init_stats_dev(int64_t m) {
@@ -512,7 +539,8 @@ struct tsd_ctx {
         last_count = hc.sc;
         if (r_sq > 0.0 && enq_passes > 0) {
             if (hc.stop == INT_MAX) band_hint = enq_passes + 2;  // cut off by the count: allow more
-            else band_hint = std::max(1, hc.passes);             // the break rule fired at pass passes-1
+            else if (hc.stop_why == 2) band_hint = std::max(1, hc.passes);  // passes stopped paying
+            else band_hint = std::max(band_hint, hc.passes);  // ran out of rows: no evidence to shrink
         }
         const int ec = hc.ec;
         if (debug)
@@ -705,6 +733,7 @@ void tsd_ctx_destroy(tsd_ctx* c) {
     c->hm_rows.release();
     c->hm_idx.release();
     c->hm_vals.release();
+    c->red_tmp.release();
     c->ctl.release();
     c->h_ctl.release();
     c->h_ex.release();
@@ -1037,6 +1066,172 @@ int tsd_heatmap_rank(tsd_ctx* c, int64_t k, tsd_ranked* out, int64_t* count) {
         for (int64_t e = 0; e < keep; ++e) out[e] = tsd_ranked{v[e].index, v[e].length, v[e].score};
         *count = keep;
     });
+}
+
+// ---- in-process rank group ---------------------------------------------------
+struct tsd_group {
+    std::vector<tsd_ctx*> ctx;
+    PeerGroup* pg = nullptr;
+    std::string err;
+};
+
+int tsd_group_create(const int* devices, int n, tsd_group** out) {
+    *out = nullptr;
+    if (n < 1 || n > kMaxGroup) {
+        g_create_err = "group size must be 1.." + std::to_string(kMaxGroup);
+        return TSD_EINVAL;
+    }
+    tsd_group* g = new tsd_group();
+    g->pg = new PeerGroup(n);
+    for (int r = 0; r < n; ++r) {
+        tsd_ctx* c = nullptr;
+        const int rc = tsd_ctx_create(devices[r], &c);
+        if (rc != TSD_OK) {
+            tsd_group_destroy(g);
+            return rc;
+        }
+        g->ctx.push_back(c);
+        c->rank = r;
+        c->world = n;
+        c->group = g->pg;
+        cudaSetDevice(c->device);
+        if (cudaEventCreateWithFlags(&g->pg->ev_in[r], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&g->pg->ev_red[r], cudaEventDisableTiming) != cudaSuccess) {
+            g_create_err = "event creation failed";
+            tsd_group_destroy(g);
+            return TSD_ECUDA;
+        }
+    }
+    // peer access between distinct devices (same device: plain pointers)
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < n; ++b) {
+            const int da = g->ctx[a]->device, db = g->ctx[b]->device;
+            if (da == db) continue;
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, da, db);
+            if (!can) {
+                g_create_err = "devices " + std::to_string(da) + " and " + std::to_string(db) + " lack peer access";
+                tsd_group_destroy(g);
+                return TSD_ECUDA;
+            }
+            cudaSetDevice(da);
+            const cudaError_t e = cudaDeviceEnablePeerAccess(db, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+                g_create_err = std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e);
+                tsd_group_destroy(g);
+                return TSD_ECUDA;
+            }
+            cudaGetLastError();
+        }
+    *out = g;
+    return TSD_OK;
+}
+
+void tsd_group_destroy(tsd_group* g) {
+    if (!g) return;
+    for (size_t r = 0; r < g->ctx.size(); ++r) {
+        if (g->pg->ev_in[r]) cudaEventDestroy(g->pg->ev_in[r]);
+        if (g->pg->ev_red[r]) cudaEventDestroy(g->pg->ev_red[r]);
+        tsd_ctx_destroy(g->ctx[r]);
+    }
+    delete g->pg;
+    delete g;
+}
+
+const char* tsd_group_last_error(const tsd_group* g) { return g ? g->err.c_str() : g_create_err.c_str(); }
+int tsd_group_size(const tsd_group* g) { return g ? (int)g->ctx.size() : 0; }
+tsd_ctx* tsd_group_ctx(tsd_group* g, int rank) {
+    return (g && rank >= 0 && rank < (int)g->ctx.size()) ? g->ctx[rank] : nullptr;
+}
+
+}  // extern "C"
+namespace {
+// runs f(rank) on one host thread per rank; a failing rank releases the others
+template <typename F>
+int group_run(tsd_group* g, F&& f) {
+    const int n = (int)g->ctx.size();
+    std::vector<int> rc(n, TSD_OK);
+    g->pg->bar.reset();
+    std::vector<std::thread> th;
+    for (int r = 0; r < n; ++r)
+        th.emplace_back([&, r] {
+            rc[r] = f(r);
+            if (rc[r] != TSD_OK) g->pg->bar.fail();
+        });
+    for (auto& t : th) t.join();
+    for (int r = 0; r < n; ++r)
+        if (rc[r] != TSD_OK) {
+            g->err = "rank " + std::to_string(r) + ": " + tsd_last_error(g->ctx[r]);
+            return rc[r];
+        }
+    g->err.clear();
+    return TSD_OK;
+}
+}  // namespace
+extern "C" {
+
+int tsd_group_series_set(tsd_group* g, const double* v, int64_t n) {
+    return group_run(g, [&](int r) { return tsd_series_set(g->ctx[r], v, n); });
+}
+
+int tsd_group_merlin(tsd_group* g, int64_t min_len, int64_t max_len, const tsd_merlin_opts* o, int64_t* counts,
+                     tsd_record* recs, double* final_r, int64_t* retries, uint8_t* failed) {
+    const int n = (int)g->ctx.size();
+    const int64_t L = std::max<int64_t>(max_len - min_len + 1, 1);
+    const int64_t k = std::max<int64_t>(o ? o->top_k : 1, 1);
+    struct Out {
+        std::vector<int64_t> counts, retries;
+        std::vector<tsd_record> recs;
+        std::vector<double> final_r;
+        std::vector<uint8_t> failed;
+    };
+    std::vector<Out> outs(n);
+    for (auto& x : outs) {
+        x.counts.assign(L, 0);
+        x.retries.assign(L, 0);
+        x.recs.assign(L * k, tsd_record{});
+        x.final_r.assign(L, 0.0);
+        x.failed.assign(L, 0);
+    }
+    const int rc = group_run(g, [&](int r) {
+        Out& x = outs[r];
+        return tsd_merlin(g->ctx[r], min_len, max_len, o, x.counts.data(), x.recs.data(), x.final_r.data(),
+                          x.retries.data(), x.failed.data());
+    });
+    if (rc != TSD_OK) return rc;
+    // every rank holds the same reduced state, hence the same records
+    for (int r = 1; r < n; ++r)
+        if (outs[r].counts != outs[0].counts || outs[r].failed != outs[0].failed ||
+            std::memcmp(outs[r].recs.data(), outs[0].recs.data(), L * k * sizeof(tsd_record)) != 0) {
+            g->err = "ranks diverged";
+            return TSD_ERUNTIME;
+        }
+    std::copy(outs[0].counts.begin(), outs[0].counts.end(), counts);
+    std::copy(outs[0].retries.begin(), outs[0].retries.end(), retries);
+    std::copy(outs[0].final_r.begin(), outs[0].final_r.end(), final_r);
+    std::copy(outs[0].failed.begin(), outs[0].failed.end(), failed);
+    std::copy(outs[0].recs.begin(), outs[0].recs.end(), recs);
+    return TSD_OK;
+}
+
+int tsd_group_pardrag(tsd_group* g, int64_t m, double r_sq, int64_t seglen, tsd_record* out, int64_t cap,
+                      int64_t* count) {
+    const int n = (int)g->ctx.size();
+    std::vector<std::vector<tsd_record>> bufs(n, std::vector<tsd_record>(std::max<int64_t>(cap, 1)));
+    std::vector<int64_t> cnt(n, 0);
+    const int rc = group_run(g, [&](int r) {
+        return tsd_pardrag(g->ctx[r], m, r_sq, seglen, nullptr, nullptr, bufs[r].data(), cap, &cnt[r]);
+    });
+    if (rc != TSD_OK) return rc;
+    for (int r = 1; r < n; ++r)
+        if (cnt[r] != cnt[0] ||
+            std::memcmp(bufs[r].data(), bufs[0].data(), std::min(cnt[0], cap) * sizeof(tsd_record)) != 0) {
+            g->err = "ranks diverged";
+            return TSD_ERUNTIME;
+        }
+    *count = cnt[0];
+    std::copy(bufs[0].begin(), bufs[0].begin() + std::min(cnt[0], cap), out);
+    return TSD_OK;
 }
 
 int tsd_gen_randomwalk(int64_t n, uint64_t seed, double* out) {

@@ -76,3 +76,32 @@ void launch_hm_colmax(const double* hm, int64_t nrows, int64_t ncols, int64_t mi
 }
 
 }  // namespace tsd
+
+// ---------------------------------------------------------------------------
+// peer all-reduce (peer_group.cuh): every rank reads all ranks' buffers
+#include "peer_group.cuh"
+
+namespace tsd {
+
+template <typename T, int KIND>
+__global__ void k_peer_reduce(PeerPtrs in, int nranks, T* __restrict__ out, size_t cnt) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < cnt; i += (size_t)gridDim.x * blockDim.x) {
+        T v = static_cast<const T*>(in.p[0])[i];
+        for (int r = 1; r < nranks; ++r) {
+            const T w = static_cast<const T*>(in.p[r])[i];
+            v = KIND == 1 ? (w > v ? w : v) : (w < v ? w : v);
+        }
+        out[i] = v;
+    }
+}
+
+void launch_peer_reduce(int kind, PeerPtrs in, int nranks, void* out, size_t cnt, cudaStream_t st) {
+    if (cnt == 0) return;
+    size_t b = (cnt + 255) / 256;
+    if (b > 148 * 8) b = 148 * 8;
+    if (kind == 0) k_peer_reduce<uint8_t, 0><<<(int)b, 256, 0, st>>>(in, nranks, (uint8_t*)out, cnt);
+    else if (kind == 1) k_peer_reduce<unsigned, 1><<<(int)b, 256, 0, st>>>(in, nranks, (unsigned*)out, cnt);
+    else k_peer_reduce<unsigned long long, 2><<<(int)b, 256, 0, st>>>(in, nranks, (unsigned long long*)out, cnt);
+}
+
+}  // namespace tsd

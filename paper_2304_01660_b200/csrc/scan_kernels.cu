@@ -727,6 +727,7 @@ __global__ void k_try_init(uint8_t* __restrict__ alive, unsigned* __restrict__ y
         ctl->ec = 0;
         ctl->passes = 0;
         ctl->span = 0;
+        ctl->stop_why = 0;
         ctl->lk = 0.0;
         acc[0] = acc[1] = acc[2] = 0ull;
     }
@@ -1083,8 +1084,13 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
             const int prev = ctl->alive;
             ctl->prev = prev;
             ctl->passes = gate + 1;
-            if (total == 0 || total <= max(64, n / 4096) || (double)total > (double)band_keep * (double)prev)
+            if (total == 0 || total <= max(64, n / 4096)) {
                 ctl->stop = gate;
+                ctl->stop_why = 1;
+            } else if ((double)total > (double)band_keep * (double)prev) {
+                ctl->stop = gate;
+                ctl->stop_why = 2;
+            }
         }
         ctl->alive = total;
         int k = 5;  // dense lists (>= 1 row in 64 undecided): whole 512-row blocks

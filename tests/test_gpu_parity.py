@@ -172,3 +172,35 @@ def test_merlin_constant_series_fails_lengths(engine):
     engine.set_series(np.full(400, 2.5))
     rep = engine.merlin_full(8, 12)
     assert rep.failed_lengths == list(range(8, 13))
+
+
+# ---- sharded path (segment-sharded tiles + reductions) on one device -----------
+@pytest.mark.parametrize("ranks", [2, 3])
+def test_group_sharded_merlin_equals_single(engine, ranks):
+    # ranks contexts on cuda:0: tiles dealt cyclically, kill flags / route maxima /
+    # exact-nn keys all-reduced through peer memory -> identical records
+    import paper_2304_01660_b200 as P
+    g = P.Group([0] * ranks)
+    for fx in (load_golden("c1.json"), load_golden("small.json")["merlin"][1]):
+        x = series_of(fx["input"])
+        g.set_series(x)
+        rep = g.merlin_full(fx["min_len"], fx["max_len"], top_k=fx["top_k"], seglen=fx["seglen"])
+        check_merlin(rep, fx)
+    # every rank swept only its share of the tiles
+    cells = [g.counters(r)["cells"] for r in range(ranks)]
+    assert all(c > 0 for c in cells)
+    g.close()
+
+
+def test_group_sharded_range_sets(engine, oracle):
+    import paper_2304_01660_b200 as P
+    g = P.Group([0, 0])
+    x = oracle.gen_randomwalk(2500, 77)
+    g.set_series(x)
+    for m in (8, 33):
+        s = np.sort(oracle.brute_force_nn(x, m))
+        for q in (0.5, 0.99):
+            r_sq = float(s[int(len(s) * q)])
+            assert recs_list(g.pardrag(m, r_sq, seglen=max(2 * m, 64))) == \
+                recs_list(oracle.range_discords(x, m, r_sq))
+    g.close()
