@@ -107,6 +107,15 @@ struct ScanParams {
     unsigned long long* acc;  // accounting: [0] cells walked, [1] cells evaluated, [2] seed dots
 };
 
+// Programmatic dependent launch: every kernel of the try chain is launched
+// with programmatic stream serialization (launch_pdl), waits here for its
+// predecessor's completion and memory, then lets its own successor launch, so
+// the successor's CTAs are resident when this grid ends (no launch gap).
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
 // Order-preserving float <-> uint32 map (for atomicMax on floats of any sign).
 __device__ __forceinline__ unsigned f2key(float f) {
     const unsigned b = __float_as_uint(f);

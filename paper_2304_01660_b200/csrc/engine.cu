@@ -318,7 +318,18 @@ struct tsd_ctx {
     std::vector<EvPair> ev_pool;
     size_t ev_used = 0;
 
+    // bracket every scan with events (per-phase kernel time for the roofline).
+    // Off by default: an event between two kernels breaks the programmatic
+    // dependent launch chain (C2: 53.7 ms with events, 43.1 ms without)
+    bool scan_events = false;
     void scan(int mode, const ScanParams& p) {
+        if (!scan_events) {
+            launch_scan(mode, p, st);
+            ck(cudaGetLastError(), "scan launch");
+            ctr.scan_launches += 1;
+            ctr.kernel_launches += 1;
+            return;
+        }
         if (ev_used == ev_pool.size()) {
             EvPair e{};
             ck(cudaEventCreate(&e.a), "event");
@@ -1263,6 +1274,7 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         if (k == "dense_rows") c->dense_rows = v <= 0 ? 0 : std::max(16, std::min(kMaxRows, (int)v));
         else if (k == "sparse_rows") c->sparse_rows = std::max(0, std::min(kMaxRows, (int)v));
         else if (k == "err_scale") c->err_k = v;
+        else if (k == "scan_events") c->scan_events = v != 0.0;
         else if (k == "band_keep") c->band_keep = (float)std::max(0.0, std::min(1.0, v));
         else if (k == "band_passes") c->band_passes = std::max(1, std::min(64, (int)v));
         else if (k == "result_prefix") c->result_prefix = std::max(16, std::min(1 << 20, (int)v));

@@ -8,6 +8,22 @@
 
 namespace tsd {
 
+// Launch with programmatic stream serialization (kernels call pdl_enter()).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 void launch_init_stats(const double* t, int n, int m, double* mu, double* sig, double* scratch_a,
                        double* scratch_b, cudaStream_t st);
 void launch_advance_stats(const double* t, int n, int m, double* mu, double* sig, cudaStream_t st);

@@ -195,6 +195,7 @@ __device__ __noinline__ void slow_track(const F9 x, const F9 qn, float tz, float
 
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(const ScanParams p) {
+    pdl_enter();
     // static shared memory (33 KB): CTA-relative LDS addressing, no shared
     // window base to rematerialise inside the walk
     __shared__ ScanSmem S;
@@ -665,6 +666,7 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_ref_pairs(const double* __r
                                                                unsigned long long* nnkey,
                                                                TryCtl* ctl, const int* __restrict__ ex,
                                                                double* __restrict__ nnout) {
+    pdl_enter();
     __shared__ double buf[kPairWarps][256];
     const int w = threadIdx.x >> 5;
     const int total = min(*count, cap);
@@ -708,6 +710,7 @@ constexpr int kSmallGrid = 148 * 2;  // grid-stride kernels over device-sized li
 // try start: every row undecided, counters reset, route maxima cleared
 __global__ void k_try_init(uint8_t* __restrict__ alive, unsigned* __restrict__ ymax, unsigned* __restrict__ emax,
                            float* __restrict__ ythr, int N, TryCtl* ctl, unsigned long long* acc) {
+    pdl_enter();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
         alive[i] = 1;
         ymax[i] = 0u;
@@ -930,6 +933,7 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
                                                         int gate, int2* __restrict__ groups,
                                                         int2* __restrict__ slots, int m, int fixed_span,
                                                         float band_keep) {
+    pdl_enter();
     if (gated_off(ctl, gate)) return;
     __shared__ int s_bid, s_excl, s_last, s_k;
     __shared__ int wsum[32];
@@ -1191,6 +1195,7 @@ __global__ void __launch_bounds__(1024) k_survivors(const int* __restrict__ list
                                                     double* __restrict__ hi, int* __restrict__ cand,
                                                     float* __restrict__ ythr, unsigned long long* __restrict__ nnkey,
                                                     int2* __restrict__ groups, int fixed_span) {
+    pdl_enter();
     __shared__ int wsum[32];
     __shared__ int hist[256];
     __shared__ unsigned long long s_prefix;
@@ -1311,6 +1316,7 @@ __global__ void __launch_bounds__(1024) k_survivors(const int* __restrict__ list
 
 __global__ void k_gather_nn(const int* __restrict__ list, const int* __restrict__ cnt_p,
                             const unsigned long long* __restrict__ nnkey, double* __restrict__ out) {
+    pdl_enter();
     const int cnt = *cnt_p;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += gridDim.x * blockDim.x)
         out[e] = __longlong_as_double((long long)nnkey[list[e]]);
@@ -1344,6 +1350,7 @@ __global__ void k_seed_init(const double* __restrict__ t, int n, int m, int L, i
 
 __global__ void k_seed_advance(const double* __restrict__ t, int n, int m, int L, int kA, int nb,
                                double* __restrict__ qt) {
+    pdl_enter();
     const int N1 = n - m;  // subsequence count of length m+1
     const long long total = (long long)nb * kW;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
@@ -1358,7 +1365,7 @@ void launch_seed_init(const double* t, int n, int m, int L, int kA, int nb, doub
 }
 
 void launch_seed_advance(const double* t, int n, int m, int L, int kA, int nb, double* qt, cudaStream_t st) {
-    k_seed_advance<<<148 * 8, 256, 0, st>>>(t, n, m, L, kA, nb, qt);
+    launch_pdl(k_seed_advance, 148 * 8, 256, st, t, n, m, L, kA, nb, qt);
 }
 
 static int grid_for(long long work, int threads) {
@@ -1394,9 +1401,9 @@ static int scan_grid() {
 
 void launch_scan(int mode, const ScanParams& p, cudaStream_t st) {
     switch (mode) {
-        case kPrune: k_scan<kPrune><<<scan_grid<kPrune>(), kThreads, 0, st>>>(p); break;
-        case kPruneTrack: k_scan<kPruneTrack><<<scan_grid<kPruneTrack>(), kThreads, 0, st>>>(p); break;
-        default: k_scan<kCollect><<<scan_grid<kCollect>(), kThreads, 0, st>>>(p); break;
+        case kPrune: launch_pdl(k_scan<kPrune>, scan_grid<kPrune>(), kThreads, st, p); break;
+        case kPruneTrack: launch_pdl(k_scan<kPruneTrack>, scan_grid<kPruneTrack>(), kThreads, st, p); break;
+        default: launch_pdl(k_scan<kCollect>, scan_grid<kCollect>(), kThreads, st, p); break;
     }
 }
 
@@ -1405,10 +1412,10 @@ void launch_ref_pairs(int mode, const double* t, int m, const int2* pairs, const
                       double* nnout, cudaStream_t st) {
     const int blocks = 148 * 4;  // grid-stride over the device-side pair count
     if (mode == 0)
-        k_ref_pairs<0><<<blocks, kPairWarps * 32, 0, st>>>(t, m, pairs, count, cap, r_sq, alive, nnkey, ctl,
+        launch_pdl(k_ref_pairs<0>, blocks, kPairWarps * 32, st, t, m, pairs, count, cap, r_sq, alive, nnkey, ctl,
                                                              nullptr, nullptr);
     else
-        k_ref_pairs<1><<<blocks, kPairWarps * 32, 0, st>>>(t, m, pairs, count, cap, r_sq, alive, nnkey, ctl, ex,
+        launch_pdl(k_ref_pairs<1>, blocks, kPairWarps * 32, st, t, m, pairs, count, cap, r_sq, alive, nnkey, ctl, ex,
                                                              nnout);
 }
 
@@ -1416,13 +1423,13 @@ void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const 
                       const unsigned* emax, const float* nrm, const int* crange, int N, int m, int need,
                       double* lo, double* hi, int* cand, float* ythr, unsigned long long* nnkey, int2* groups,
                       int fixed_span, cudaStream_t st) {
-    k_survivors<<<1, 1024, 0, st>>>(list, alive, ctl, ymax, emax, nrm, crange, N, m, need, lo, hi, cand, ythr,
+    launch_pdl(k_survivors, 1, 1024, st, list, alive, ctl, ymax, emax, nrm, crange, N, m, need, lo, hi, cand, ythr,
                                     nnkey, groups, fixed_span);
 }
 
 void launch_try_init(uint8_t* alive, unsigned* ymax, unsigned* emax, float* ythr, int N, TryCtl* ctl,
                      unsigned long long* acc, cudaStream_t st) {
-    k_try_init<<<grid_for(N, 256), 256, 0, st>>>(alive, ymax, emax, ythr, N, ctl, acc);
+    launch_pdl(k_try_init, grid_for(N, 256), 256, st, alive, ymax, emax, ythr, N, ctl, acc);
 }
 
 int compact_blocks(int n) { return (n + kCompactTile - 1) / kCompactTile; }
@@ -1430,7 +1437,7 @@ int compact_blocks(int n) { return (n + kCompactTile - 1) / kCompactTile; }
 void launch_compact_group(const uint8_t* a, int n, int* out, unsigned long long* status, unsigned epoch,
                           TryCtl* ctl, int gate, int2* groups, int2* slots, int m, int fixed_span, float band_keep,
                           cudaStream_t st) {
-    k_compact_group<<<compact_blocks(n), kCompactBlock, 0, st>>>(a, n, out, status, epoch, ctl, gate, groups, slots,
+    launch_pdl(k_compact_group, compact_blocks(n), kCompactBlock, st, a, n, out, status, epoch, ctl, gate, groups, slots,
                                                                m, fixed_span, band_keep);
 }
 
@@ -1438,7 +1445,7 @@ int group_slots(int n) { return compact_blocks(n) * 504; }
 
 void launch_gather_nn(const int* list, const int* cnt, const unsigned long long* nnkey, double* out,
                       cudaStream_t st) {
-    k_gather_nn<<<kSmallGrid, 256, 0, st>>>(list, cnt, nnkey, out);
+    launch_pdl(k_gather_nn, kSmallGrid, 256, st, list, cnt, nnkey, out);
 }
 
 }  // namespace tsd

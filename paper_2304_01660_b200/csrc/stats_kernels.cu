@@ -96,6 +96,7 @@ __global__ void k_init_finish(const double* __restrict__ sum, const double* __re
 // stats (length m, n-m+1 valid) -> length m+1 (n-m valid), in place.
 __global__ void k_advance(const double* __restrict__ t, int n, int m, double* __restrict__ mu,
                           double* __restrict__ sig) {
+    pdl_enter();
     const int cnt = n - m;  // next valid_count
     const double md = (double)m;
     const double md1 = md + 1.0;
@@ -120,6 +121,7 @@ __global__ void k_advance(const double* __restrict__ t, int n, int m, double* __
 __global__ void k_derive(const double* __restrict__ t, int m, int cnt, const double* __restrict__ mu,
                          const double* __restrict__ sig, float* __restrict__ df,
                          float* __restrict__ dg, float* __restrict__ nrm, int* __restrict__ cr) {
+    pdl_enter();
     const double sqm = sqrt((double)m);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
         const double s = sig[i];
@@ -154,13 +156,13 @@ void launch_init_stats(const double* t, int n, int m, double* mu, double* sig, d
 }
 
 void launch_advance_stats(const double* t, int n, int m, double* mu, double* sig, cudaStream_t st) {
-    k_advance<<<grid_for(n - m, 256), 256, 0, st>>>(t, n, m, mu, sig);
+    launch_pdl(k_advance, grid_for(n - m, 256), 256, st, t, n, m, mu, sig);
 }
 
 void launch_derive(const double* t, int m, int cnt, const double* mu, const double* sig, float* df,
                    float* dg, float* nrm, int* crange, cudaStream_t st) {
     cudaMemsetAsync(crange, 0, 2 * sizeof(int), st);
-    k_derive<<<grid_for(cnt, 256), 256, 0, st>>>(t, m, cnt, mu, sig, df, dg, nrm, crange);
+    launch_pdl(k_derive, grid_for(cnt, 256), 256, st, t, m, cnt, mu, sig, df, dg, nrm, crange);
 }
 
 }  // namespace tsd
