@@ -58,7 +58,9 @@ struct TryCtl {
     int cdone;      // compaction: finished CTAs (self-resetting)
     int ctotal;     // compaction: total of the latest launch
     int xdone;      // exact pass: finished CTAs (self-resetting)
-    int stop_why;   // band loop: 1 nothing / few rows left, 2 a pass killed too few
+    int stop_why;   // band loop: 1 nothing / few rows / no diagonals left, 2 a pass killed too few
+    int bK0;        // band passes >= 1: first diagonal of the next pass
+    int bnb;        // ... and its number of kW-wide bands (set by the compaction before it)
     double lk;      // top-k filter: need_top-th largest nn lower bound
     double cost[6]; // compaction: grouping cost per span (16..512), self-resetting
 };
@@ -100,7 +102,7 @@ struct ScanParams {
     const int2* groups;  // kSpaceBand / kSpaceFull: (first, last) row of each group
     int space;           // TileSpace
     int pass;            // band pass index (kSpaceBand: skipped when ctl->stop < pass)
-    int K0, nb;          // band: diagonals [K0, K0 + nb*kW) on both sides
+    int K0, nb;          // kSpaceBlocks: diagonals [K0, K0 + nb*kW) on both sides (kSpaceBand: TryCtl)
     int L, kA;           // kSpaceSeed / kSpaceBlocks: block rows; kSpaceSeed: band offset
     int rank, world;     // tiles are dealt cyclically across ranks
     const double* seedqt;  // resident raw dot products QT(i, i+k) of the band-0 tiles (kW per tile)

@@ -448,7 +448,12 @@ struct tsd_ctx {
         ev_used = 0;
         ctr.pardrag_calls += 1;
         TryCtl* C = ctl.p;
-        launch_try_init(alive.p, ymax.p, emax.p, ythr.p, N, C, acc.p, st);
+        // band 0 is the band at kA (resident seed rows) or at m; later passes
+        // continue from its end, with the device choosing their widths
+        const bool seeded = seed_m == m;
+        const long long k_max = (long long)N - 1;
+        const long long K1 = seeded ? (long long)seed_kA + kW : (long long)m + kW;
+        launch_try_init(alive.p, ymax.p, emax.p, ythr.p, N, C, acc.p, (int)std::min<long long>(K1, INT_MAX), st);
         ck(cudaGetLastError(), "try init");
         ctr.kernel_launches += 1;
         const ScanParams P = params(m, r_sq);
@@ -457,39 +462,32 @@ struct tsd_ctx {
         // ---- band passes (PD3 selection): diagonals |k| in [K0, K0 + nb*kW) on
         // both sides of every undecided row; only certain FP32 kills.  Pass 0
         // tiles all rows in aligned blocks; later passes tile the device-built
-        // groups of the remaining rows.  The break rule (nothing / few left, or
-        // < 15% killed) is applied on the device; passes after it are no-ops.
+        // groups of the remaining rows over a device-chosen number of bands.  The
+        // break rule (nothing / few left, < 15% killed, no diagonals left) is
+        // applied on the device; passes after it are no-ops.
         if (r_sq > 0.0) {
-            long long K0 = m;
-            const long long k_max = (long long)N - 1;
             // passes after the device-side break rule are no-ops but still cost
             // their launches: enqueue what the previous try needed (consecutive
             // lengths behave alike), growing while the cap is what stopped it
             const int want = band_hint > 0 ? std::min(band_hint, band_passes) : std::min(4, band_passes);
             enq_passes = 0;
-            for (int pass = 0; K0 <= k_max && pass < want; ++pass) {
+            for (int pass = 0; pass < want && (pass == 0 || K1 <= k_max); ++pass) {
                 ++enq_passes;
                 ScanParams q = P;
                 q.pass = pass;
-                if (pass == 0 && seed_m == m) {
+                if (pass == 0 && seeded) {
                     // band 0 at the fixed offset kA (>= m for every length of the run)
                     // seeded from the resident rows: no direct dot products
                     q.space = kSpaceSeed;
                     q.L = seed_L;
                     q.kA = seed_kA;
-                    K0 = (long long)seed_kA + kW;
+                } else if (pass == 0) {
+                    q.space = kSpaceBlocks;
+                    q.L = block_rows(N);
+                    q.K0 = (int)m;
+                    q.nb = 1;
                 } else {
-                    const long long nb =
-                        std::min<long long>(1ll << std::min(pass, 5), (k_max - K0 + kW) / kW);
-                    if (pass == 0) {
-                        q.space = kSpaceBlocks;
-                        q.L = block_rows(N);
-                    } else {
-                        q.space = kSpaceBand;  // groups built by the previous compaction
-                    }
-                    q.K0 = (int)K0;
-                    q.nb = (int)nb;
-                    K0 += nb * kW;
+                    q.space = kSpaceBand;  // groups and bands set by the previous compaction
                 }
                 scan(kPrune, q);
                 allreduce_min_u8(alive.p, N);

@@ -44,7 +44,7 @@ void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const 
                       double* lo, double* hi, int* cand, float* ythr, unsigned long long* nnkey, int2* groups,
                       int fixed_span, cudaStream_t st);
 void launch_try_init(uint8_t* alive, unsigned* ymax, unsigned* emax, float* ythr, int N, TryCtl* ctl,
-                     unsigned long long* acc, cudaStream_t st);
+                     unsigned long long* acc, int band_k0, cudaStream_t st);
 int compact_blocks(int n);
 // gate: band pass index (>= 0), kGateNone or kGateQueue (common.cuh)
 // compaction + break rule + grouping in one kernel (status: >= compact_blocks(n)

@@ -73,7 +73,7 @@ __device__ __forceinline__ long long tile_slots(const ScanParams& p) {
     switch (p.space) {
         case kSpaceSeed: return 2ll * ((p.N + p.L - 1) / p.L);
         case kSpaceBlocks: return 2ll * p.nb * ((p.N + p.L - 1) / p.L);
-        case kSpaceBand: return ctl->stop < p.pass ? 0 : 2ll * p.nb * ctl->G;
+        case kSpaceBand: return ctl->stop < p.pass ? 0 : 2ll * ctl->bnb * ctl->G;
         default: {  // full rows: the farthest group needs ceil((N - m) / kW) tiles a side
             const long long maxc = ((long long)p.N - p.m + kW - 1) / kW;
             return maxc > 0 ? 2ll * maxc * ctl->G : 0;
@@ -122,7 +122,7 @@ __device__ __forceinline__ bool tile_decode(const ScanParams& p, long long t, Ti
         const int2 gr = p.groups[(t >> 1) % G];
         a = gr.x;
         e = gr.y;
-        k0 = (long long)p.K0 + b * kW;
+        k0 = (long long)p.ctl->bK0 + b * kW;
     } else {
         G = p.ctl->G;
         const long long i = t / (2 * G);
@@ -709,7 +709,7 @@ constexpr int kSmallGrid = 148 * 2;  // grid-stride kernels over device-sized li
 
 // try start: every row undecided, counters reset, route maxima cleared
 __global__ void k_try_init(uint8_t* __restrict__ alive, unsigned* __restrict__ ymax, unsigned* __restrict__ emax,
-                           float* __restrict__ ythr, int N, TryCtl* ctl, unsigned long long* acc) {
+                           float* __restrict__ ythr, int N, TryCtl* ctl, unsigned long long* acc, int band_k0) {
     pdl_enter();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
         alive[i] = 1;
@@ -731,6 +731,8 @@ __global__ void k_try_init(uint8_t* __restrict__ alive, unsigned* __restrict__ y
         ctl->passes = 0;
         ctl->span = 0;
         ctl->stop_why = 0;
+        ctl->bK0 = band_k0;
+        ctl->bnb = 0;
         ctl->lk = 0.0;
         acc[0] = acc[1] = acc[2] = 0ull;
     }
@@ -932,7 +934,7 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
                                                         unsigned long long* status, unsigned epoch, TryCtl* ctl,
                                                         int gate, int2* __restrict__ groups,
                                                         int2* __restrict__ slots, int m, int fixed_span,
-                                                        float band_keep) {
+                                                        float band_keep, int scan_slots) {
     pdl_enter();
     if (gated_off(ctl, gate)) return;
     __shared__ int s_bid, s_excl, s_last, s_k;
@@ -1095,6 +1097,8 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
                 ctl->stop = gate;
                 ctl->stop_why = 2;
             }
+            // next band pass (gate + 1): starts where this one ended
+            if (gate >= 1) ctl->bK0 += ctl->bnb * kW;
         }
         ctl->alive = total;
         int k = 5;  // dense lists (>= 1 row in 64 undecided): whole 512-row blocks
@@ -1130,7 +1134,26 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
         if (ff) groups[p2] = v;
         carry += t2;
     }
-    if (threadIdx.x == 0) ctl->G = carry;
+    if (threadIdx.x == 0) {
+        ctl->G = carry;
+        if (gate >= 0 && ctl->stop == INT_MAX) {
+            // Bands of the next pass: at least 2^p (the doubling schedule), and
+            // enough to fill one wave of the persistent scan grid — a pass with
+            // fewer tiles than CTAs costs one tile's latency anyway, so the
+            // extra bands come free and kill more rows before the full rows.
+            const long long k_max = (long long)n - 1, K0 = ctl->bK0;
+            const long long left = K0 <= k_max ? (k_max - K0 + kW) / kW : 0;
+            if (left <= 0 || carry == 0) {
+                ctl->stop = gate;
+                ctl->stop_why = 1;
+            } else {
+                long long nb = 1ll << min(gate + 1, 5);
+                const long long fill = (scan_slots + 2ll * carry - 1) / (2ll * carry);
+                if (fill > nb) nb = fill;
+                ctl->bnb = (int)(nb < left ? nb : left);
+            }
+        }
+    }
 }
 
 // per-survivor interval [lo, hi] of the exact nn^2 from the tracked route maxima
@@ -1428,17 +1451,19 @@ void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const 
 }
 
 void launch_try_init(uint8_t* alive, unsigned* ymax, unsigned* emax, float* ythr, int N, TryCtl* ctl,
-                     unsigned long long* acc, cudaStream_t st) {
-    launch_pdl(k_try_init, grid_for(N, 256), 256, st, alive, ymax, emax, ythr, N, ctl, acc);
+                     unsigned long long* acc, int band_k0, cudaStream_t st) {
+    launch_pdl(k_try_init, grid_for(N, 256), 256, st, alive, ymax, emax, ythr, N, ctl, acc, band_k0);
 }
 
 int compact_blocks(int n) { return (n + kCompactTile - 1) / kCompactTile; }
+
+int scan_slots_prune() { return scan_grid<kPrune>(); }
 
 void launch_compact_group(const uint8_t* a, int n, int* out, unsigned long long* status, unsigned epoch,
                           TryCtl* ctl, int gate, int2* groups, int2* slots, int m, int fixed_span, float band_keep,
                           cudaStream_t st) {
     launch_pdl(k_compact_group, compact_blocks(n), kCompactBlock, st, a, n, out, status, epoch, ctl, gate, groups, slots,
-                                                               m, fixed_span, band_keep);
+                                                               m, fixed_span, band_keep, scan_slots_prune());
 }
 
 int group_slots(int n) { return compact_blocks(n) * 504; }
