@@ -180,6 +180,14 @@ int tsd_heatmap_set(tsd_ctx* ctx, int64_t min_len, int64_t max_len, int64_t n, c
  * k, non-zero only.  k < 1 -> TSD_EINVAL.  `out` must hold min(k, n-minL). */
 int tsd_heatmap_rank(tsd_ctx* ctx, int64_t k, tsd_ranked* out, int64_t* count);
 
+/* ---- independent FP64 matrix profile (checker) ----------------------------
+ * nn^2 of every subsequence (n-m+1 values, +inf without a non-self match) by
+ * a different algorithm than the product path: the FP64 STOMP diagonal
+ * recurrence over every cell, no pruning.  Agrees with brute_force_nn to
+ * ~1e-10 relative; meant for parity checks at sizes where the reference's
+ * O(N^2 m) brute_force_nn (src/drag.cpp:137-149) is out of reach. */
+int tsd_matrix_profile_fp64(tsd_ctx* ctx, int64_t m, double* out);
+
 /* ---- host utilities the reference API also exposes (io.hpp) --------------
  * gen_randomwalk: src/io.cpp:110-119 (libstdc++ mt19937_64 + normal_distribution). */
 int tsd_gen_randomwalk(int64_t n, uint64_t seed, double* out);

@@ -33,7 +33,7 @@ EXPORTS = (
     "tsd_get_counters", "tsd_reset_counters", "tsd_set_param", "tsd_fp32_peak_probe",
     "tsd_heatmap_build", "tsd_heatmap_set", "tsd_heatmap_rank",
     "tsd_group_create", "tsd_group_destroy", "tsd_group_last_error", "tsd_group_size", "tsd_group_ctx",
-    "tsd_group_series_set", "tsd_group_merlin", "tsd_group_pardrag",
+    "tsd_group_series_set", "tsd_group_merlin", "tsd_group_pardrag", "tsd_matrix_profile_fp64",
 )
 
 
@@ -101,6 +101,7 @@ def load_library(path: str = LIB_PATH):
     f("tsd_pardrag", C.c_int, [vp, _i64, C.c_double, _i64, vp, vp, vp, _i64, C.POINTER(_i64)])
     f("tsd_merlin", C.c_int, [vp, _i64, _i64, C.POINTER(_Opts), _ip, vp, _dp, _ip, _u8])
     f("tsd_brute_force_nn", C.c_int, [vp, _i64, _dp])
+    f("tsd_matrix_profile_fp64", C.c_int, [vp, _i64, _dp])
     f("tsd_gen_randomwalk", C.c_int, [_i64, C.c_uint64, _dp])
     f("tsd_get_counters", C.c_int, [vp, C.POINTER(Counters)])
     f("tsd_reset_counters", C.c_int, [vp])
@@ -263,6 +264,12 @@ class Engine:
     def brute_force_nn(self, m: int) -> np.ndarray:
         out = np.empty(max(self.n - m + 1, 1))
         self._check(self._L.tsd_brute_force_nn(self._h, m, out))
+        return out
+
+    def matrix_profile_fp64(self, m: int) -> np.ndarray:
+        """Independent FP64 matrix profile (checker; ~1e-10 relative to brute_force_nn)."""
+        out = np.empty(max(self.n - m + 1, 1))
+        self._check(self._L.tsd_matrix_profile_fp64(self._h, m, out))
         return out
 
     def merlin_full(self, min_len: int, max_len: int, top_k: int = 1, seglen: int = 512,

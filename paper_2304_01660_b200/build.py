@@ -27,7 +27,7 @@ CU_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xc
 CXX_FLAGS = ["-O3", "-std=gnu++20", "-fPIC", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC,
              "-I/usr/local/cuda/include"]
 
-SOURCES = ["stats_kernels.cu", "scan_kernels.cu", "heatmap_kernels.cu", "probe.cu", "engine.cu", "api.cpp"]
+SOURCES = ["stats_kernels.cu", "scan_kernels.cu", "heatmap_kernels.cu", "mp_fp64.cu", "probe.cu", "engine.cu", "api.cpp"]
 HEADERS = ["common.cuh", "engine_internal.h", "nccl_shim.h", "peer_group.cuh"]
 
 

@@ -17,6 +17,8 @@
 #include <ostream>
 #include <sstream>
 #include <string>
+#include <string_view>
+#include <thread>
 
 #include "tsdiscord/drag.hpp"
 #include "tsdiscord/heatmap.hpp"
@@ -387,47 +389,133 @@ void write_ranking_csv(const std::vector<RankedDiscord>& ranking, std::ostream& 
             << '\n';
 }
 
+// load_series (src/io.cpp:48-104) with the reference's semantics and messages,
+// parallel: the file is read once, split into lines, and the data lines are
+// parsed by all host threads in contiguous chunks; the first error by line
+// number is the one reported (the reference stops at it).
+namespace {
+std::string_view trim_ref(std::string_view s) {  // " \t\r" only, as src/io.cpp:24-29
+    const auto b = s.find_first_not_of(" \t\r");
+    if (b == std::string_view::npos) return {};
+    const auto e = s.find_last_not_of(" \t\r");
+    return s.substr(b, e - b + 1);
+}
+bool parse_ref(std::string_view tok, double& out) {  // src/io.cpp:31-38
+    const std::string_view t = trim_ref(tok);
+    if (t.empty()) return false;
+    auto res = std::from_chars(t.data(), t.data() + t.size(), out);
+    return res.ec == std::errc() && res.ptr == t.data() + t.size();
+}
+// field f of a CSV line (split on ',', a trailing ',' adds an empty field);
+// false when the line has fewer fields
+bool csv_field(std::string_view line, long f, std::string_view& out) {
+    size_t a = 0;
+    for (long k = 0; k < f; ++k) {
+        const size_t c = line.find(',', a);
+        if (c == std::string_view::npos) return false;
+        a = c + 1;
+    }
+    const size_t c = line.find(',', a);
+    out = line.substr(a, c == std::string_view::npos ? std::string_view::npos : c - a);
+    return true;
+}
+}  // namespace
+
 TimeSeries load_series(const std::string& path, const std::string& column) {
-    std::ifstream in(path);
+    std::ifstream in(path, std::ios::binary);
     if (!in) throw std::runtime_error("cannot open input file: " + path);
+    const std::string buf((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    // lines as std::getline splits them (no empty line after a final '\n')
+    std::vector<std::string_view> lines;
+    {
+        size_t a = 0;
+        while (a < buf.size()) {
+            size_t e = buf.find('\n', a);
+            if (e == std::string::npos) e = buf.size();
+            lines.emplace_back(buf.data() + a, e - a);
+            a = e + 1;
+        }
+    }
+    // header / column resolution on the first non-blank line
+    long col = column.empty() ? 0 : -1;
+    size_t first = lines.size();
+    for (size_t i = 0; i < lines.size(); ++i)
+        if (!trim_ref(lines[i]).empty()) {
+            first = i;
+            break;
+        }
+    if (first < lines.size()) {
+        std::string_view f0;
+        csv_field(lines[first], 0, f0);
+        double probe;
+        if (!parse_ref(f0, probe)) {  // header row
+            if (!column.empty()) {
+                for (long f = 0;; ++f) {
+                    std::string_view fv;
+                    if (!csv_field(lines[first], f, fv)) break;
+                    if (trim_ref(fv) == column) col = f;
+                }
+                if (col < 0) {
+                    double idx;
+                    if (parse_ref(column, idx)) col = static_cast<long>(idx);
+                    else throw std::runtime_error("column '" + column + "' not found in header");
+                }
+            }
+            ++first;
+        } else if (!column.empty()) {
+            double idx;
+            if (!parse_ref(column, idx))
+                throw std::runtime_error("column '" + column + "' requested but file has no header");
+            col = static_cast<long>(idx);
+        }
+    }
+    // parallel parse of lines [first, end)
+    const size_t total = lines.size() > first ? lines.size() - first : 0;
+    const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
+    const size_t nchunk = std::max<size_t>(1, std::min<size_t>(hc, total / 65536 + 1));
+    struct Chunk {
+        std::vector<double> v;
+        size_t err_line = SIZE_MAX;
+        std::string err;
+    };
+    std::vector<Chunk> ch(nchunk);
+    auto work = [&](size_t c) {
+        const size_t lo = first + total * c / nchunk, hi = first + total * (c + 1) / nchunk;
+        Chunk& k = ch[c];
+        k.v.reserve(hi - lo);
+        for (size_t i = lo; i < hi; ++i) {
+            const std::string_view line = lines[i];
+            if (trim_ref(line).empty()) continue;
+            std::string_view fv;
+            if (!csv_field(line, col, fv)) {
+                k.err_line = i;
+                k.err = "line " + std::to_string(i + 1) + ": missing column " + std::to_string(col);
+                return;
+            }
+            double v;
+            if (!parse_ref(fv, v)) {
+                k.err_line = i;
+                k.err = "line " + std::to_string(i + 1) + ": non-numeric value '" + std::string(trim_ref(fv)) + "'";
+                return;
+            }
+            k.v.push_back(v);
+        }
+    };
+    if (nchunk == 1) {
+        work(0);
+    } else {
+        std::vector<std::thread> th;
+        for (size_t c = 0; c < nchunk; ++c) th.emplace_back(work, c);
+        for (auto& t : th) t.join();
+    }
     std::vector<double> values;
-    std::string line;
-    long lineno = 0;
-    long col = -1;
-    bool header_seen = false;
-    while (std::getline(in, line)) {
-        ++lineno;
-        if (!line.empty() && line.back() == '\r') line.pop_back();
-        if (strip(line).empty()) continue;
-        const auto fields = split_csv(line);
-        if (col < 0) {
-            // column selection: empty -> first, digits -> position, else header name
-            if (column.empty()) col = 0;
-            else if (std::all_of(column.begin(), column.end(), ::isdigit)) col = std::atol(column.c_str());
-            else {
-                for (size_t i = 0; i < fields.size(); ++i)
-                    if (strip(fields[i]) == column) col = (long)i;
-                if (col < 0) throw std::runtime_error("column not found: " + column);
-                header_seen = true;
-                continue;
-            }
-        }
-        if ((size_t)col >= fields.size())
-            throw std::runtime_error("line " + std::to_string(lineno) + ": missing column");
-        double v;
-        if (!to_double(fields[(size_t)col], v)) {
-            if (!header_seen && values.empty()) {
-                header_seen = true;  // a leading header line
-                continue;
-            }
-            throw std::runtime_error("line " + std::to_string(lineno) + ": not a number: " +
-                                     strip(fields[(size_t)col]));
-        }
-        values.push_back(v);
+    values.reserve(total);
+    for (const Chunk& k : ch) {
+        if (k.err_line != SIZE_MAX) throw std::runtime_error(k.err);
+        values.insert(values.end(), k.v.begin(), k.v.end());
     }
     if (values.size() < 3)
-        throw std::runtime_error("series too short: need at least 3 values, got " +
-                                 std::to_string(values.size()));
+        throw std::runtime_error("series too short: need at least 3 values, got " + std::to_string(values.size()));
     return TimeSeries(std::move(values));
 }
 

@@ -1243,6 +1243,35 @@ int tsd_group_pardrag(tsd_group* g, int64_t m, double r_sq, int64_t seglen, tsd_
     return TSD_OK;
 }
 
+int tsd_matrix_profile_fp64(tsd_ctx* c, int64_t m, double* out) {
+    return guard(c, [&] {
+        need_series(c);
+        if (m < 3 || m > c->n - 2) fail(TSD_EINVAL, "matrix_profile: length out of range");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        const int64_t n = c->n, N = n - m + 1;
+        double gm = 0.0;
+        for (double v : c->h_t) gm += v;
+        gm /= (double)n;
+        DBuf<double> scratch, res;
+        DBuf<unsigned long long> keys;
+        scratch.ensure((size_t)(2 * n + 4 * N));
+        keys.ensure((size_t)(2 * N));
+        res.ensure((size_t)N);
+        ck(cudaEventRecord(c->ev_a, c->st), "event");
+        mp_fp64(c->t.p, (int)n, (int)m, gm, scratch.p, keys.p, res.p, c->st);
+        ck(cudaGetLastError(), "matrix profile");
+        ck(cudaEventRecord(c->ev_b, c->st), "event");
+        ck(cudaMemcpyAsync(out, res.p, (size_t)N * sizeof(double), cudaMemcpyDeviceToHost, c->st), "D2H");
+        c->sync();
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c->ev_a, c->ev_b);
+        c->ctr.total_ms = ms;
+        scratch.release();
+        keys.release();
+        res.release();
+    });
+}
+
 int tsd_gen_randomwalk(int64_t n, uint64_t seed, double* out) {
     return guard(nullptr, [&] {
         // src/io.cpp:110-119 — same engine and distribution (libstdc++)

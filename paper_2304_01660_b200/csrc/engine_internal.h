@@ -58,6 +58,10 @@ void launch_seed_advance(const double* t, int n, int m, int L, int kA, int nb, d
 void launch_gather_nn(const int* list, const int* cnt, const unsigned long long* nnkey, double* out,
                       cudaStream_t st);
 
+// independent FP64 matrix profile (mp_fp64.cu); scratch: 2n + 4N doubles, keys: 2N
+void mp_fp64(const double* t, int n, int m, double gmean, double* scratch,
+             unsigned long long* keys, double* out, cudaStream_t st);
+
 // heatmap (heatmap_kernels.cu)
 struct HmCol {
     int64_t index;   // 1-based start index

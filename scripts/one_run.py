@@ -4,13 +4,13 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2304_01660_b200 as P
-from bench import CONFIGS
+from bench import CONFIGS, make_input
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 n, seed, lo, hi, top_k, _ = CONFIGS[cfg]
 if len(sys.argv) > 2:
     hi = lo + int(sys.argv[2]) - 1
-x = P.gen_randomwalk(n, seed)
+x = make_input(cfg)
 e = P.Engine(0)
 for kv in sys.argv[3:]:
     k, v = kv.split("=")

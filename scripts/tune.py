@@ -5,7 +5,7 @@ import itertools
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2304_01660_b200 as P
-from bench import CONFIGS
+from bench import CONFIGS, make_input
 
 cfg = sys.argv[1]
 n, seed, lo, hi, top_k, _ = CONFIGS[cfg]
@@ -13,7 +13,7 @@ grid = {}
 for a in sys.argv[2:]:
     k, v = a.split("=")
     grid[k] = [float(x) for x in v.split(",")]
-x = P.gen_randomwalk(n, seed)
+x = make_input(cfg)
 e = P.Engine(0)
 e.set_series(x)
 e.merlin_full(lo, hi, top_k=top_k)  # warm

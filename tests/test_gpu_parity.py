@@ -204,3 +204,38 @@ def test_group_sharded_range_sets(engine, oracle):
             assert recs_list(g.pardrag(m, r_sq, seglen=max(2 * m, 64))) == \
                 recs_list(oracle.range_discords(x, m, r_sq))
     g.close()
+
+
+# ---- independent FP64 matrix profile (STOMP recurrence, no pruning) -------------
+def top_k_of(profile, k):
+    order = np.lexsort((np.arange(len(profile)), -profile))  # nn desc, index asc (sort_discords)
+    return order[:k]
+
+
+def test_matrix_profile_fp64_vs_reference_bruteforce(engine, oracle):
+    for n, m, seed in [(1500, 16, 3), (2400, 64, 9), (900, 100, 4)]:
+        x = oracle.gen_randomwalk(n, seed)
+        engine.set_series(x)
+        mp = engine.matrix_profile_fp64(m)
+        bf = oracle.brute_force_nn(x, m)
+        assert np.all(np.isfinite(mp) == np.isfinite(bf))
+        f = np.isfinite(bf)
+        assert np.max(np.abs(mp[f] - bf[f]) / np.maximum(bf[f], 1e-300)) < 1e-9
+
+
+@pytest.mark.parametrize("name,lengths", [("c4.json", (512, 777, 1024)), ("c3s.json", (64, 100, 127)),
+                                          ("c5s.json", (128, 159)), ("c5.json", (384, 640))])
+def test_golden_discords_are_matrix_profile_maxima(engine, name, lengths):
+    # full-size parity by a second, independent route: the reference's discords of
+    # a length are the top-k of the exact nn profile (acceptance criterion 1)
+    fx = load_golden(name)
+    x = series_of(fx["input"])
+    engine.set_series(x)
+    per = {e["m"]: e for e in fx["per_length"]}
+    for m in lengths:
+        e = per[m]
+        mp = engine.matrix_profile_fp64(m)
+        top = top_k_of(mp, fx["top_k"])
+        assert [int(i) + 1 for i in top] == [r[0] for r in e["records"]], m
+        for i, r in zip(top, e["records"]):
+            assert abs(mp[i] - hexf(r[1])) <= 1e-9 * hexf(r[1]), (m, mp[i], hexf(r[1]))
