@@ -34,7 +34,9 @@ enum TileSpace : int {
     kSpaceSeed = 0,    // band 0 at offset kA over aligned L-row blocks, seeded from resident rows
     kSpaceBlocks = 1,  // band [K0, K0 + nb*kW) over aligned L-row blocks (FP32 / FP64 direct seeds)
     kSpaceBand = 2,    // band [K0, K0 + nb*kW) over the device-built groups (TryCtl::G)
-    kSpaceFull = 3     // every diagonal |k| >= m of the device-built groups, near-first
+    kSpaceFull = 3,    // every diagonal |k| >= m of the device-built groups, near-first
+    kSpaceTrack = 4,   // tracked full-row chunk [tK0, tK0 + tnb*kW) over the groups (TryCtl)
+    kSpaceTrackRest = 5  // every tracked chunk not yet run (far rest + near), in one launch
 };
 
 // Device-resident control block of one DRAG try: every count the host used to
@@ -61,6 +63,12 @@ struct TryCtl {
     int stop_why;   // band loop: 1 nothing / few rows / no diagonals left, 2 a pass killed too few
     int bK0;        // band passes >= 1: first diagonal of the next pass
     int bnb;        // ... and its number of kW-wide bands (set by the compaction before it)
+    // full rows as tracked chunks: far chunks [kend, N) first (doubling), then
+    // the near chunk [m, kend) that the band passes covered without tracking
+    int kend;       // end of the band passes' coverage
+    int tK0, tnb;   // next tracked chunk
+    int tphase;     // 0 far chunks, 1 near chunk, 2 done
+    int tpasses;    // tracked chunks that ran
     double lk;      // top-k filter: need_top-th largest nn lower bound
     double cost[6]; // compaction: grouping cost per span (16..512), self-resetting
 };
@@ -69,6 +77,7 @@ struct TryCtl {
 // passes stopped before it), or one of these
 constexpr int kGateNone = -1;   // always runs
 constexpr int kGateQueue = -2;  // skipped when no knife edge was queued (or nothing is alive)
+constexpr int kGateTrack = -3;  // tracked chunks: skipped once the chunks are done
 
 enum ScanMode : int {
     kPrune = 0,       // dense band: kill both ends of any pair with d^2 < r^2

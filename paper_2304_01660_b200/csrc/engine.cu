@@ -140,6 +140,8 @@ struct tsd_ctx {
     int sparse_rows = 0;   // 0: choose by cost model (on the device)
     int band_passes = 40;  // cap on band passes (incl. pass 0) enqueued per try; full rows cover the rest
     int band_hint = 0;     // adaptive count: passes the previous try needed (0: none yet)
+    int track_hint = 0;    // ... and tracked chunks (plus the catch-all launch)
+    int track_chunks = 1;  // cap on tracked launches per try (1: the catch-all alone)
     float band_keep = 0.85f;  // band loop stops when a pass leaves more than this fraction alive
     int result_prefix = 1024;  // records copied back with the try's single round trip
     double err_k = 4.0;
@@ -235,11 +237,41 @@ struct tsd_ctx {
         df.ensure(N);
         dg.ensure(N);
         nrm.ensure(N);
-        crange.ensure(2);
-        launch_derive(t.p, (int)m, (int)N, mu.p, sig.p, df.p, dg.p, nrm.p, crange.p, st);
+        crange.ensure(4);
+        // both parity slots cleared: the fused length step after this one uses the other
+        ck(cudaMemsetAsync(crange.p, 0, 4 * sizeof(int), st), "memset");
+        cr_cur = crange.p + 2 * (m & 1);
+        launch_derive(t.p, (int)m, (int)N, mu.p, sig.p, df.p, dg.p, nrm.p, cr_cur, st);
         ctr.kernel_launches += 1;
         ck(cudaGetLastError(), "derive");
         derived_m = m;
+    }
+    // MERLIN length step m -> m+1 in one launch: stats (ping-pong buffers),
+    // derived operands of m+1 and, when resident, the seed rows
+    int* cr_cur = nullptr;  // constant-row range of derived_m
+    DBuf<double> mu2, sig2;
+    void next_length(bool with_seed) {
+        const int64_t m = stats_m, m1 = m + 1, N1 = n - m;
+        mu2.ensure(n);
+        sig2.ensure(n);
+        df.ensure(N1);
+        dg.ensure(N1);
+        nrm.ensure(N1);
+        if (derived_m != m || !cr_cur) derive(m);  // establishes the parity slots
+        int* cr = crange.p + 2 * (m1 & 1);
+        int* crn = crange.p + 2 * ((m1 + 1) & 1);
+        launch_next_length(t.p, (int)n, (int)m, mu.p, sig.p, mu2.p, sig2.p, df.p, dg.p, nrm.p, cr, crn, seed_L, seed_kA,
+                           seed_nb, with_seed ? seedqt.p : nullptr, st);
+        ck(cudaGetLastError(), "next length");
+        ctr.kernel_launches += 1;
+        std::swap(mu.p, mu2.p);
+        std::swap(mu.cap, mu2.cap);
+        std::swap(sig.p, sig2.p);
+        std::swap(sig.cap, sig2.cap);
+        stats_m = m1;
+        derived_m = m1;
+        cr_cur = cr;
+        if (with_seed) seed_m = m1;
     }
 
     // Rows per band-0 block: 512 when the blocks fill the persistent grid, else
@@ -384,8 +416,11 @@ struct tsd_ctx {
         ck(cudaMemcpyAsync(h_ctl.p, ctl.p, sizeof(TryCtl), cudaMemcpyDeviceToHost, st), "D2H");
         sync();
         const TryCtl& c = *h_ctl.p;
-        fprintf(stderr, "[tsd] m=%lld r2=%.6g %s pass=%d groups=%d span=%d alive=%d stop=%d queue=%d\n",
-                (long long)m, r_sq, what, pass, c.G, c.span, c.alive, c.stop == INT_MAX ? -1 : c.stop, c.queue);
+        fprintf(stderr,
+                "[tsd] m=%lld r2=%.6g %s pass=%d groups=%d span=%d alive=%d stop=%d queue=%d band=[%d,+%d) "
+                "track=[%d,+%d) phase=%d\n",
+                (long long)m, r_sq, what, pass, c.G, c.span, c.alive, c.stop == INT_MAX ? -1 : c.stop, c.queue,
+                c.bK0, c.bnb * kW, c.tK0, c.tnb * kW, c.tphase);
     }
 
     void ensure_scan_buffers(int N) {
@@ -465,12 +500,12 @@ struct tsd_ctx {
         // groups of the remaining rows over a device-chosen number of bands.  The
         // break rule (nothing / few left, < 15% killed, no diagonals left) is
         // applied on the device; passes after it are no-ops.
+        enq_passes = 0;
         if (r_sq > 0.0) {
             // passes after the device-side break rule are no-ops but still cost
             // their launches: enqueue what the previous try needed (consecutive
             // lengths behave alike), growing while the cap is what stopped it
             const int want = band_hint > 0 ? std::min(band_hint, band_passes) : std::min(4, band_passes);
-            enq_passes = 0;
             for (int pass = 0; pass < want && (pass == 0 || K1 <= k_max); ++pass) {
                 ++enq_passes;
                 ScanParams q = P;
@@ -499,10 +534,29 @@ struct tsd_ctx {
         }
 
         // ---- full rows (PD3 refinement) for every remaining candidate: prune,
-        // queue knife edges, and track a lower bound of each row's best corr
-        // (groups of the list come from the last compaction)
+        // queue knife edges, and track a lower bound of each row's best corr.
+        // The diagonals are swept as tracked chunks with a compaction (and new
+        // groups) after each: first the far diagonals the band passes never
+        // reached, doubling, where the remaining non-discords die, then the
+        // near chunk [m, kend) for the rows still undecided.  The last launch
+        // covers whatever chunks the enqueued count did not reach.
         ScanParams q = P;
-        q.space = kSpaceFull;
+        launch_track_init(C, N, (int)m, r_sq > 0.0 && enq_passes > 0, st);
+        ck(cudaGetLastError(), "track init");
+        ctr.kernel_launches += 1;
+        // Measured: separate tracked chunks cost a launch latency each (C4:
+        // 505 us per try in 6 chunks vs 346 us in one launch), so by default
+        // the whole stage is the single catch-all launch; track_chunks > 1
+        // enables the chunked schedule (experiments).
+        const int twant = track_chunks <= 1 ? 1 : std::max(1, std::min(track_hint > 0 ? track_hint : 4, track_chunks));
+        for (int j = 0; j + 1 < twant; ++j) {
+            q.space = kSpaceTrack;
+            scan(kPruneTrack, q);
+            allreduce_min_u8(alive.p, N);
+            compact(N, kGateTrack, m);
+            trace("tracked", m, r_sq, j);
+        }
+        q.space = kSpaceTrackRest;
         scan(kPruneTrack, q);
         allreduce_min_u8(alive.p, N);
         allreduce_max_u32(ymax.p, N);
@@ -516,10 +570,11 @@ struct tsd_ctx {
         // ---- survivors: exact nearest neighbours (pardrag.cpp:378-416).  One
         // CTA filters the list to the survivors, applies the MERLIN top-k
         // filter, resets their keys and groups them.
-        launch_survivors(list.p, alive.p, C, ymax.p, emax.p, nrm.p, crange.p, N, (int)m, (int)need_top, bnd_lo.p,
+        launch_survivors(list.p, alive.p, C, ymax.p, emax.p, nrm.p, cr_cur, N, (int)m, (int)need_top, bnd_lo.p,
                          bnd_hi.p, cand.p, ythr.p, nnkey.p, groups.p, sparse_rows, st);
         ck(cudaGetLastError(), "survivors");
         const int* ex = cand.p;  // rows whose exact nn is computed (count: C->ec)
+        q.space = kSpaceFull;  // every diagonal of the exact-nn rows' groups
         scan(kCollect, q);
         launch_ref_pairs(1, t.p, (int)m, coll.p, &C->coll, kCollCap, r_sq, alive.p, nnkey.p, C,
                          world == 1 ? ex : nullptr, nnout.p, st);
@@ -546,6 +601,8 @@ struct tsd_ctx {
         ctr.rechecks += (unsigned long long)hc.queue;
         ctr.exact_pairs += (unsigned long long)hc.coll;
         last_count = hc.sc;
+        // tracked chunks: run them one by one next time as far as this try needed
+        track_hint = hc.tphase >= 2 ? hc.tpasses + 1 : std::min(16, std::max(track_hint, 4) + 2);
         if (r_sq > 0.0 && enq_passes > 0) {
             if (hc.stop == INT_MAX) band_hint = enq_passes + 2;  // cut off by the count: allow more
             else if (hc.stop_why == 2) band_hint = std::max(1, hc.passes);  // passes stopped paying
@@ -718,6 +775,8 @@ void tsd_ctx_destroy(tsd_ctx* c) {
     c->dg.release();
     c->nrm.release();
     c->crange.release();
+    c->mu2.release();
+    c->sig2.release();
     c->lbstat.release();
     c->alive.release();
     c->queue.release();
@@ -919,9 +978,12 @@ int tsd_merlin(tsd_ctx* c, int64_t min_len, int64_t max_len, const tsd_merlin_op
             counts[k] = 0;
             failed[k] = 0;
             if (m > min_len) {
-                if (reuse) c->advance_stats_dev();
-                else c->init_stats_dev(m);
-                if (c->seed_m == m - 1) c->seed_advance();
+                if (reuse) {
+                    c->next_length(c->seed_m == m - 1);
+                } else {
+                    c->init_stats_dev(m);
+                    if (c->seed_m == m - 1) c->seed_advance();
+                }
             }
             const int phase = m == min_len ? 0 : (m < min_len + 5 ? 1 : 2);
             if (phase != 0 && history.empty()) {
@@ -1302,6 +1364,7 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "sparse_rows") c->sparse_rows = std::max(0, std::min(kMaxRows, (int)v));
         else if (k == "err_scale") c->err_k = v;
         else if (k == "scan_events") c->scan_events = v != 0.0;
+        else if (k == "track_chunks") c->track_chunks = std::max(1, std::min(16, (int)v));
         else if (k == "band_keep") c->band_keep = (float)std::max(0.0, std::min(1.0, v));
         else if (k == "band_passes") c->band_passes = std::max(1, std::min(64, (int)v));
         else if (k == "result_prefix") c->result_prefix = std::max(16, std::min(1 << 20, (int)v));

@@ -30,6 +30,11 @@ void launch_advance_stats(const double* t, int n, int m, double* mu, double* sig
 void launch_derive(const double* t, int m, int cnt, const double* mu, const double* sig, float* df,
                    float* dg, float* nrm, int* crange, cudaStream_t st);
 
+// advance + derive (+ seed rows when qt != nullptr) of one MERLIN length step
+void launch_next_length(const double* t, int n, int m, const double* mu_in, const double* sig_in, double* mu_out,
+                        double* sig_out, float* df, float* dg, float* nrm, int* cr, int* cr_next, int L, int kA,
+                        int nb, double* qt, cudaStream_t st);
+
 size_t scan_smem_bytes();
 void scan_configure();
 // persistent tile scan over the launch's tile space (ScanParams::space)
@@ -53,6 +58,8 @@ void launch_compact_group(const uint8_t* a, int n, int* out, unsigned long long*
                           TryCtl* ctl, int gate, int2* groups, int2* slots, int m, int fixed_span, float band_keep,
                           cudaStream_t st);
 int group_slots(int n);
+// tracked full-row chunks: schedule of the first chunk (after the band passes)
+void launch_track_init(TryCtl* ctl, int N, int m, bool bands_ran, cudaStream_t st);
 void launch_seed_init(const double* t, int n, int m, int L, int kA, int nb, double* qt, cudaStream_t st);
 void launch_seed_advance(const double* t, int n, int m, int L, int kA, int nb, double* qt, cudaStream_t st);
 void launch_gather_nn(const int* list, const int* cnt, const unsigned long long* nnkey, double* out,

@@ -66,6 +66,20 @@ __device__ __forceinline__ float warp_max(float v) {
     return v;
 }
 
+// Bands left for the catch-all tracked launch: the far rest [tK0, N) when the
+// far chunks are unfinished, and the near chunk [m, kend) unless it ran.
+__device__ __forceinline__ void track_rest(const TryCtl* ctl, int N, int m, long long& nf, long long& nn) {
+    const long long k_max = (long long)N - 1;
+    nf = nn = 0;
+    if (ctl->tphase >= 2) return;
+    if (ctl->tphase == 0) {
+        if ((long long)ctl->tK0 <= k_max) nf = (k_max - ctl->tK0 + kW) / kW;
+        if (ctl->kend > m) nn = ((long long)ctl->kend - m + kW - 1) / kW;
+    } else {
+        nn = ctl->tnb;  // the pending near chunk starts at m
+    }
+}
+
 // Number of tile slots of a launch's tile space (device-side: the group count
 // of kSpaceBand / kSpaceFull is only known on the device).
 __device__ __forceinline__ long long tile_slots(const ScanParams& p) {
@@ -74,6 +88,12 @@ __device__ __forceinline__ long long tile_slots(const ScanParams& p) {
         case kSpaceSeed: return 2ll * ((p.N + p.L - 1) / p.L);
         case kSpaceBlocks: return 2ll * p.nb * ((p.N + p.L - 1) / p.L);
         case kSpaceBand: return ctl->stop < p.pass ? 0 : 2ll * ctl->bnb * ctl->G;
+        case kSpaceTrack: return ctl->tphase >= 2 ? 0 : 2ll * ctl->tnb * ctl->G;
+        case kSpaceTrackRest: {
+            long long nf, nn;
+            track_rest(ctl, p.N, p.m, nf, nn);
+            return 2ll * (nf + nn) * ctl->G;
+        }
         default: {  // full rows: the farthest group needs ceil((N - m) / kW) tiles a side
             const long long maxc = ((long long)p.N - p.m + kW - 1) / kW;
             return maxc > 0 ? 2ll * maxc * ctl->G : 0;
@@ -116,13 +136,19 @@ __device__ __forceinline__ bool tile_decode(const ScanParams& p, long long t, Ti
         a = g * p.L;
         e = min(N, a + p.L) - 1;
         k0 = (long long)p.K0 + b * kW;
-    } else if (p.space == kSpaceBand) {
+    } else if (p.space == kSpaceBand || p.space == kSpaceTrack || p.space == kSpaceTrackRest) {
         G = p.ctl->G;
         const long long b = t / (2 * G);
         const int2 gr = p.groups[(t >> 1) % G];
         a = gr.x;
         e = gr.y;
-        k0 = (long long)p.ctl->bK0 + b * kW;
+        if (p.space == kSpaceTrackRest) {
+            long long nf, nn;
+            track_rest(p.ctl, N, p.m, nf, nn);
+            k0 = b < nf ? (long long)p.ctl->tK0 + b * kW : (long long)p.m + (b - nf) * kW;
+        } else {
+            k0 = (long long)(p.space == kSpaceBand ? p.ctl->bK0 : p.ctl->tK0) + b * kW;
+        }
     } else {
         G = p.ctl->G;
         const long long i = t / (2 * G);
@@ -740,6 +766,7 @@ __global__ void k_try_init(uint8_t* __restrict__ alive, unsigned* __restrict__ y
 
 __device__ __forceinline__ bool gated_off(const TryCtl* ctl, int gate) {
     if (gate >= 0) return ctl->stop < gate;
+    if (gate == kGateTrack) return ctl->tphase >= 2;
     if (gate == kGateQueue) return ctl->queue == 0 || ctl->alive == 0;
     return false;
 }
@@ -783,6 +810,9 @@ __device__ __forceinline__ int block_exscan(int v, int* wsum, int* total) {
 // sum over groups of (2m seed work + 3 per walked row and diagonal).  Dense
 // lists (>= 1 row in 64 undecided) take aligned 512-row blocks instead.
 constexpr int kSpans = 6;  // 16, 32, ..., 512
+// a list is "dense" (whole 512-row blocks, no cost model) only when it is long
+// and >= 1 row in 64 is listed; a handful of clustered rows gets small spans
+constexpr int kDenseMin = 4096;
 
 // walks the segment starting at list index e (a segment start for `span`);
 // calls emit(first_index, last_index) for each group
@@ -821,7 +851,8 @@ __device__ void group_body(const int* __restrict__ list_g, const int cnt, int2* 
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
         int sp = fixed_span;
-        if (sp <= 0 && (long long)cnt * 64 >= (long long)(list[cnt - 1] - list[0] + 1)) sp = -kMaxRows;
+        if (sp <= 0 && cnt >= kDenseMin && (long long)cnt * 64 >= (long long)(list[cnt - 1] - list[0] + 1))
+            sp = -kMaxRows;
         s_span = sp;
     }
     __syncthreads();
@@ -929,6 +960,56 @@ __device__ __forceinline__ unsigned long long lb_word(unsigned epoch, unsigned s
 }
 // offset of span k's slot region (tile b's span-blocks at + b * (256 >> k))
 __device__ __forceinline__ long long slot_region(int k, int nb) { return (long long)nb * (512 - (512 >> k)); }
+
+// Tracked-chunk schedule (one thread).  Far chunks start at the end of the
+// band passes' coverage and double (at least enough bands to fill one wave of
+// the scan grid); when they reach the last diagonal, the near chunk
+// [m, kend) follows, for the rows still undecided; then done.
+__device__ void track_schedule(TryCtl* ctl, int N, int m, int G, int scan_slots) {
+    const long long k_max = (long long)N - 1;
+    if (G == 0) {
+        ctl->tphase = 2;
+        return;
+    }
+    if (ctl->tphase == 0 && (long long)ctl->tK0 <= k_max) {
+        const long long left = (k_max - ctl->tK0 + kW) / kW;
+        long long nb = 2ll * ctl->tnb;
+        const long long fill = (scan_slots + 2ll * G - 1) / (2ll * G);
+        if (fill > nb) nb = fill;
+        if (nb < 1) nb = 1;
+        ctl->tnb = (int)(nb < left ? nb : left);
+        return;
+    }
+    if (ctl->tphase == 0 && ctl->kend > m) {
+        ctl->tphase = 1;
+        ctl->tK0 = m;
+        ctl->tnb = (int)(((long long)ctl->kend - m + kW - 1) / kW);
+        return;
+    }
+    ctl->tphase = 2;
+}
+
+// after the chunk that just ran: advance, then schedule the next one
+__device__ void track_next(TryCtl* ctl, int N, int m, int G, int scan_slots) {
+    ctl->tpasses += 1;
+    if (ctl->tphase == 1) {
+        ctl->tphase = 2;
+        return;
+    }
+    ctl->tK0 += ctl->tnb * kW;
+    track_schedule(ctl, N, m, G, scan_slots);
+}
+
+__global__ void k_track_init(TryCtl* ctl, int N, int m, int bands_ran, int scan_slots) {
+    pdl_enter();
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    ctl->kend = bands_ran ? ctl->bK0 : m;
+    ctl->tK0 = ctl->kend;
+    ctl->tnb = 0;
+    ctl->tphase = 0;
+    ctl->tpasses = 0;
+    track_schedule(ctl, N, m, ctl->alive == 0 ? 0 : ctl->G, scan_slots);
+}
 
 __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restrict__ a, int n, int* __restrict__ out,
                                                         unsigned long long* status, unsigned epoch, TryCtl* ctl,
@@ -1105,7 +1186,8 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
         if (fixed_span > 0) {
             k = 0;
             while (k < 5 && (16 << k) < fixed_span) ++k;
-        } else if (total > 0 && (long long)total * 64 < (long long)(__ldcg(&out[total - 1]) - __ldcg(&out[0]) + 1)) {
+        } else if (total > 0 && (total < kDenseMin ||
+                                 (long long)total * 64 < (long long)(__ldcg(&out[total - 1]) - __ldcg(&out[0]) + 1))) {
             double best = 1e300;
             for (int x = 0; x < kSpans; ++x) {
                 const double v = *(volatile double*)&ctl->cost[x];
@@ -1136,6 +1218,7 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
     }
     if (threadIdx.x == 0) {
         ctl->G = carry;
+        if (gate == kGateTrack) track_next(ctl, n, m, carry, scan_slots);
         if (gate >= 0 && ctl->stop == INT_MAX) {
             // Bands of the next pass: at least 2^p (the doubling schedule), and
             // enough to fill one wave of the persistent scan grid — a pass with
@@ -1459,11 +1542,17 @@ int compact_blocks(int n) { return (n + kCompactTile - 1) / kCompactTile; }
 
 int scan_slots_prune() { return scan_grid<kPrune>(); }
 
+void launch_track_init(TryCtl* ctl, int N, int m, bool bands_ran, cudaStream_t st) {
+    launch_pdl(k_track_init, 1, 32, st, ctl, N, m, bands_ran ? 1 : 0, scan_grid<kPruneTrack>());
+}
+
 void launch_compact_group(const uint8_t* a, int n, int* out, unsigned long long* status, unsigned epoch,
                           TryCtl* ctl, int gate, int2* groups, int2* slots, int m, int fixed_span, float band_keep,
                           cudaStream_t st) {
     launch_pdl(k_compact_group, compact_blocks(n), kCompactBlock, st, a, n, out, status, epoch, ctl, gate, groups, slots,
-                                                               m, fixed_span, band_keep, scan_slots_prune());
+                                                               m, fixed_span, band_keep,
+                                                               gate == kGateTrack ? scan_grid<kPruneTrack>()
+                                                                                  : scan_slots_prune());
 }
 
 int group_slots(int n) { return compact_blocks(n) * 504; }

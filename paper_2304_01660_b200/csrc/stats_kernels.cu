@@ -141,6 +141,72 @@ __global__ void k_derive(const double* __restrict__ t, int m, int cnt, const dou
     }
 }
 
+// One MERLIN length step in one launch (north_star (a)): Eq. 7-8 advance of
+// mu/sigma from length m to m+1 (ping-pong buffers, the same rounding as
+// k_advance), the derived FP32 walk operands and constant-row range of length
+// m+1 (as k_derive), and the resident seed rows' length recurrence
+// QT_{m+1}(i,q) = QT_m(i,q) + t[i+m] t[q+m] (as k_seed_advance).  cr must be
+// zero on entry; cr_next (the other parity) is cleared for the next step.
+__device__ __forceinline__ void advance1(const double* __restrict__ t, int m, int i, const double* __restrict__ mu,
+                                         const double* __restrict__ sig, double& mu1, double& sg1) {
+    const double md = (double)m;
+    const double md1 = md + 1.0;
+    const double u = mu[i];
+    const double sg = sig[i];
+    const double in = t[i + m];
+    const double delta = __dsub_rn(u, in);
+    mu1 = __ddiv_rn(__dadd_rn(__dmul_rn(md, u), in), md1);
+    const double var =
+        __dmul_rn(__ddiv_rn(md, md1), __dadd_rn(__dmul_rn(sg, sg), __ddiv_rn(__dmul_rn(delta, delta), md1)));
+    sg1 = __dsqrt_rn(var > 0.0 ? var : 0.0);
+}
+
+__global__ void k_next_length(const double* __restrict__ t, int n, int m, const double* __restrict__ mu_in,
+                              const double* __restrict__ sig_in, double* __restrict__ mu_out,
+                              double* __restrict__ sig_out, float* __restrict__ df, float* __restrict__ dg,
+                              float* __restrict__ nrm, int* __restrict__ cr, int* __restrict__ cr_next, int L, int kA,
+                              int nb, double* __restrict__ qt) {
+    pdl_enter();
+    const int m1 = m + 1, cnt = n - m;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        cr_next[0] = 0;
+        cr_next[1] = 0;
+    }
+    const double sqm = sqrt((double)m1);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+        double u, s;
+        advance1(t, m, i, mu_in, sig_in, u, s);
+        mu_out[i] = u;
+        sig_out[i] = s;
+        nrm[i] = s < kSigmaEps ? 0.f : (float)(1.0 / (sqm * s));
+        if (s < kSigmaEps) {
+            atomicMax(&cr[0], cnt - i);
+            atomicMax(&cr[1], i + 1);
+        }
+        if (i == 0) {
+            df[0] = 0.f;
+            dg[0] = 0.f;
+        } else {
+            double up, sp;
+            advance1(t, m, i - 1, mu_in, sig_in, up, sp);  // mu_{i-1} of length m+1 (same rounding)
+            const double a = t[i + m1 - 1], b = t[i - 1];
+            df[i] = (float)((a - b) * 0.5);
+            dg[i] = (float)((a - u) + (b - up));
+        }
+    }
+    if (qt != nullptr) {
+        const long long total = (long long)nb * kW;
+        for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+             e += (long long)gridDim.x * blockDim.x) {
+            const int b = (int)(e / kW), u = (int)(e % kW);
+            const int j = b >> 1;
+            const int i = (b & 1) ? j * L + L - 1 : j * L;
+            const int q = (b & 1) ? i - kA - u : i + kA + u;
+            if (i < cnt && q >= 0 && q < cnt) qt[e] = fma(t[i + m], t[q + m], qt[e]);
+        }
+    }
+}
+
 static int grid_for(long long work, int threads) {
     long long b = (work + threads - 1) / threads;
     if (b < 1) b = 1;
@@ -163,6 +229,13 @@ void launch_derive(const double* t, int m, int cnt, const double* mu, const doub
                    float* dg, float* nrm, int* crange, cudaStream_t st) {
     cudaMemsetAsync(crange, 0, 2 * sizeof(int), st);
     launch_pdl(k_derive, grid_for(cnt, 256), 256, st, t, m, cnt, mu, sig, df, dg, nrm, crange);
+}
+
+void launch_next_length(const double* t, int n, int m, const double* mu_in, const double* sig_in, double* mu_out,
+                        double* sig_out, float* df, float* dg, float* nrm, int* cr, int* cr_next, int L, int kA,
+                        int nb, double* qt, cudaStream_t st) {
+    launch_pdl(k_next_length, grid_for(n - m, 256), 256, st, t, n, m, mu_in, sig_in, mu_out, sig_out, df, dg, nrm, cr,
+               cr_next, L, kA, nb, qt);
 }
 
 }  // namespace tsd
