@@ -142,6 +142,7 @@ struct tsd_ctx {
     int band_hint = 0;     // adaptive count: passes the previous try needed (0: none yet)
     int track_hint = 0;    // ... and tracked chunks (plus the catch-all launch)
     int track_chunks = 1;  // cap on tracked launches per try (1: the catch-all alone)
+    int band0_sides = 2;   // band 0 on both sides of every row, or the positive side only
     float band_keep = 0.85f;  // band loop stops when a pass leaves more than this fraction alive
     int result_prefix = 1024;  // records copied back with the try's single round trip
     double err_k = 4.0;
@@ -516,6 +517,7 @@ struct tsd_ctx {
                     q.space = kSpaceSeed;
                     q.L = seed_L;
                     q.kA = seed_kA;
+                    q.nb = band0_sides;
                 } else if (pass == 0) {
                     q.space = kSpaceBlocks;
                     q.L = block_rows(N);
@@ -1364,6 +1366,7 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "sparse_rows") c->sparse_rows = std::max(0, std::min(kMaxRows, (int)v));
         else if (k == "err_scale") c->err_k = v;
         else if (k == "scan_events") c->scan_events = v != 0.0;
+        else if (k == "band0_sides") c->band0_sides = v <= 1.0 ? 1 : 2;
         else if (k == "track_chunks") c->track_chunks = std::max(1, std::min(16, (int)v));
         else if (k == "band_keep") c->band_keep = (float)std::max(0.0, std::min(1.0, v));
         else if (k == "band_passes") c->band_passes = std::max(1, std::min(64, (int)v));

@@ -85,7 +85,7 @@ __device__ __forceinline__ void track_rest(const TryCtl* ctl, int N, int m, long
 __device__ __forceinline__ long long tile_slots(const ScanParams& p) {
     const TryCtl* ctl = p.ctl;
     switch (p.space) {
-        case kSpaceSeed: return 2ll * ((p.N + p.L - 1) / p.L);
+        case kSpaceSeed: return (long long)p.nb * ((p.N + p.L - 1) / p.L);  // nb = sides (1 or 2)
         case kSpaceBlocks: return 2ll * p.nb * ((p.N + p.L - 1) / p.L);
         case kSpaceBand: return ctl->stop < p.pass ? 0 : 2ll * ctl->bnb * ctl->G;
         case kSpaceTrack: return ctl->tphase >= 2 ? 0 : 2ll * ctl->tnb * ctl->G;
@@ -110,6 +110,7 @@ __device__ __forceinline__ bool tile_decode(const ScanParams& p, long long t, Ti
     int a, e;
     long long G, k0;
     if (p.space == kSpaceSeed) {
+        if (p.nb == 1) t <<= 1;  // one-sided band 0: positive side only
         const int j = (int)(t >> 1);
         a = j * p.L;
         e = min(N, a + p.L) - 1;
@@ -1204,17 +1205,40 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
     __syncthreads();
     const int k = s_k;
     const int nslot = nb * (256 >> k);
-    const int2* sl = slots + slot_region(k, nb);
     int carry = 0;
-    for (int b0 = 0; b0 < nslot; b0 += blockDim.x) {
-        const int e = b0 + threadIdx.x;
-        int2 v = make_int2(0, -1);
-        if (e < nslot) v = __ldcg(&sl[e]);
-        const int ff = v.y >= 0 ? 1 : 0;
-        int t2;
-        const int p2 = carry + block_exscan(ff, wsum, &t2);
-        if (ff) groups[p2] = v;
-        carry += t2;
+    if (total <= nslot) {
+        // short list (the usual case after pass 0): the groups straight from the
+        // list — an entry starts a group when its span-block differs from its
+        // predecessor's — instead of a sweep over every span-block slot
+        const int sh = 4 + k;
+        for (int b0 = 0; b0 < total; b0 += blockDim.x) {
+            const int e = b0 + threadIdx.x;
+            int r = 0, st = 0, en = 0;
+            if (e < total) {
+                r = __ldcg(&out[e]);
+                st = e == 0 || (__ldcg(&out[e - 1]) >> sh) != (r >> sh);
+                en = e + 1 == total || (__ldcg(&out[e + 1]) >> sh) != (r >> sh);
+            }
+            int t2;
+            const int g = carry + block_exscan(st, wsum, &t2) + st - 1;
+            if (e < total) {
+                if (st) groups[g].x = r;
+                if (en) groups[g].y = r;
+            }
+            carry += t2;
+        }
+    } else {
+        const int2* sl = slots + slot_region(k, nb);
+        for (int b0 = 0; b0 < nslot; b0 += blockDim.x) {
+            const int e = b0 + threadIdx.x;
+            int2 v = make_int2(0, -1);
+            if (e < nslot) v = __ldcg(&sl[e]);
+            const int ff = v.y >= 0 ? 1 : 0;
+            int t2;
+            const int p2 = carry + block_exscan(ff, wsum, &t2);
+            if (ff) groups[p2] = v;
+            carry += t2;
+        }
     }
     if (threadIdx.x == 0) {
         ctl->G = carry;
