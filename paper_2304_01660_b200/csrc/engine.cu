@@ -109,7 +109,8 @@ struct tsd_ctx {
     DBuf<double> mu, sig, scr_a, scr_b;
     int64_t derived_m = -1;
     DBuf<float> df, dg, nrm;
-    DBuf<int> crange;  // constant-row range of the derived length (k_derive)
+    DBuf<int> crange;  // constant-row range and count of the derived length (k_derive), two parity slots
+    DBuf<int> deg;     // degenerate rows (sigma < eps) of the derived length
 
     // scan state
     DBuf<uint8_t> alive;
@@ -144,6 +145,7 @@ struct tsd_ctx {
     int track_chunks = 1;  // cap on tracked launches per try (1: the catch-all alone)
     int band0_sides = 2;   // band 0 on both sides of every row, or the positive side only
     float band_keep = 0.85f;  // band loop stops when a pass leaves more than this fraction alive
+    int band_few = 256;       // ... or when at most max(band_few, N/4096) rows are left (C2: 64 -> 41.8 ms, 256 -> 41.2 ms)
     int result_prefix = 1024;  // records copied back with the try's single round trip
     double err_k = 4.0;
 
@@ -238,11 +240,12 @@ struct tsd_ctx {
         df.ensure(N);
         dg.ensure(N);
         nrm.ensure(N);
-        crange.ensure(4);
+        crange.ensure(6);
+        deg.ensure(N);
         // both parity slots cleared: the fused length step after this one uses the other
-        ck(cudaMemsetAsync(crange.p, 0, 4 * sizeof(int), st), "memset");
-        cr_cur = crange.p + 2 * (m & 1);
-        launch_derive(t.p, (int)m, (int)N, mu.p, sig.p, df.p, dg.p, nrm.p, cr_cur, st);
+        ck(cudaMemsetAsync(crange.p, 0, 6 * sizeof(int), st), "memset");
+        cr_cur = crange.p + 3 * (m & 1);
+        launch_derive(t.p, (int)m, (int)N, mu.p, sig.p, df.p, dg.p, nrm.p, cr_cur, deg.p, st);
         ctr.kernel_launches += 1;
         ck(cudaGetLastError(), "derive");
         derived_m = m;
@@ -259,10 +262,11 @@ struct tsd_ctx {
         dg.ensure(N1);
         nrm.ensure(N1);
         if (derived_m != m || !cr_cur) derive(m);  // establishes the parity slots
-        int* cr = crange.p + 2 * (m1 & 1);
-        int* crn = crange.p + 2 * ((m1 + 1) & 1);
+        int* cr = crange.p + 3 * (m1 & 1);
+        int* crn = crange.p + 3 * ((m1 + 1) & 1);
+        deg.ensure(N1);
         launch_next_length(t.p, (int)n, (int)m, mu.p, sig.p, mu2.p, sig2.p, df.p, dg.p, nrm.p, cr, crn, seed_L, seed_kA,
-                           seed_nb, with_seed ? seedqt.p : nullptr, st);
+                           seed_nb, with_seed ? seedqt.p : nullptr, deg.p, st);
         ck(cudaGetLastError(), "next length");
         ctr.kernel_launches += 1;
         std::swap(mu.p, mu2.p);
@@ -280,10 +284,7 @@ struct tsd_ctx {
     // (measured at C2: 256 rows 55.5 ms, 128 rows 56.8 ms, 512 rows 57.8 ms).
     int block_rows(int64_t N) const {
         if (dense_rows > 0) return dense_rows;
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int64_t want = (4 * 6 * (int64_t)sms) / 5;  // ~one wave of the 6-CTA/SM scan grid
+        const int64_t want = (4 * (int64_t)scan_slots_prune()) / 5;  // ~one wave of the band-pass scan grid
         for (int L = kMaxRows; L > 128; L /= 2)
             if (2 * ((N + L - 1) / L) >= want) return L;
         return 128;
@@ -406,7 +407,7 @@ struct tsd_ctx {
         }
         slots.ensure(group_slots(N));
         launch_compact_group(alive.p, N, list.p, lbstat.p, epoch, ctl.p, gate, groups.p, slots.p, (int)m,
-                             sparse_rows, band_keep, st);
+                             sparse_rows, band_keep, band_few, st);
         ck(cudaGetLastError(), "compact");
         ctr.kernel_launches += 1;
     }
@@ -489,7 +490,8 @@ struct tsd_ctx {
         const bool seeded = seed_m == m;
         const long long k_max = (long long)N - 1;
         const long long K1 = seeded ? (long long)seed_kA + kW : (long long)m + kW;
-        launch_try_init(alive.p, ymax.p, emax.p, ythr.p, N, C, acc.p, (int)std::min<long long>(K1, INT_MAX), st);
+        launch_try_init(alive.p, ymax.p, emax.p, ythr.p, nnkey.p, N, C, acc.p, (int)std::min<long long>(K1, INT_MAX),
+                        st);
         ck(cudaGetLastError(), "try init");
         ctr.kernel_launches += 1;
         const ScanParams P = params(m, r_sq);
@@ -568,6 +570,12 @@ struct tsd_ctx {
                          nullptr, st);
         ck(cudaGetLastError(), "recheck");
         allreduce_min_u8(alive.p, N);
+
+        // degenerate rows: every pair with one is decided exactly
+        launch_degenerate_pairs(t.p, (int)m, N, list.p, C, cr_cur, deg.p, r_sq, alive.p, nnkey.p, rank, world, st);
+        ck(cudaGetLastError(), "degenerate pairs");
+        allreduce_min_u8(alive.p, N);
+        ctr.kernel_launches += 1;
 
         // ---- survivors: exact nearest neighbours (pardrag.cpp:378-416).  One
         // CTA filters the list to the survivors, applies the MERLIN top-k
@@ -777,6 +785,7 @@ void tsd_ctx_destroy(tsd_ctx* c) {
     c->dg.release();
     c->nrm.release();
     c->crange.release();
+    c->deg.release();
     c->mu2.release();
     c->sig2.release();
     c->lbstat.release();
@@ -1368,6 +1377,7 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "scan_events") c->scan_events = v != 0.0;
         else if (k == "band0_sides") c->band0_sides = v <= 1.0 ? 1 : 2;
         else if (k == "track_chunks") c->track_chunks = std::max(1, std::min(16, (int)v));
+        else if (k == "band_few") c->band_few = std::max(0, (int)v);
         else if (k == "band_keep") c->band_keep = (float)std::max(0.0, std::min(1.0, v));
         else if (k == "band_passes") c->band_passes = std::max(1, std::min(64, (int)v));
         else if (k == "result_prefix") c->result_prefix = std::max(16, std::min(1 << 20, (int)v));

@@ -28,12 +28,12 @@ void launch_init_stats(const double* t, int n, int m, double* mu, double* sig, d
                        double* scratch_b, cudaStream_t st);
 void launch_advance_stats(const double* t, int n, int m, double* mu, double* sig, cudaStream_t st);
 void launch_derive(const double* t, int m, int cnt, const double* mu, const double* sig, float* df,
-                   float* dg, float* nrm, int* crange, cudaStream_t st);
+                   float* dg, float* nrm, int* crange, int* deg, cudaStream_t st);
 
 // advance + derive (+ seed rows when qt != nullptr) of one MERLIN length step
 void launch_next_length(const double* t, int n, int m, const double* mu_in, const double* sig_in, double* mu_out,
                         double* sig_out, float* df, float* dg, float* nrm, int* cr, int* cr_next, int L, int kA,
-                        int nb, double* qt, cudaStream_t st);
+                        int nb, double* qt, int* deg, cudaStream_t st);
 
 size_t scan_smem_bytes();
 void scan_configure();
@@ -48,16 +48,22 @@ void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const 
                       const unsigned* emax, const float* nrm, const int* crange, int N, int m, int need,
                       double* lo, double* hi, int* cand, float* ythr, unsigned long long* nnkey, int2* groups,
                       int fixed_span, cudaStream_t st);
-void launch_try_init(uint8_t* alive, unsigned* ymax, unsigned* emax, float* ythr, int N, TryCtl* ctl,
-                     unsigned long long* acc, int band_k0, cudaStream_t st);
+// degenerate rows (sigma < eps): every (alive row, degenerate row) and
+// (degenerate row, any q) pair by the exact distance — kills and exact-nn keys
+void launch_degenerate_pairs(const double* t, int m, int N, const int* list, const TryCtl* ctl, const int* crange,
+                             const int* deg, double r_sq, uint8_t* alive, unsigned long long* nnkey, int rank,
+                             int world, cudaStream_t st);
+void launch_try_init(uint8_t* alive, unsigned* ymax, unsigned* emax, float* ythr, unsigned long long* nnkey, int N,
+                     TryCtl* ctl, unsigned long long* acc, int band_k0, cudaStream_t st);
 int compact_blocks(int n);
 // gate: band pass index (>= 0), kGateNone or kGateQueue (common.cuh)
 // compaction + break rule + grouping in one kernel (status: >= compact_blocks(n)
 // words; slots: group_slots(n) entries)
 void launch_compact_group(const uint8_t* a, int n, int* out, unsigned long long* status, unsigned epoch,
                           TryCtl* ctl, int gate, int2* groups, int2* slots, int m, int fixed_span, float band_keep,
-                          cudaStream_t st);
+                          int band_few, cudaStream_t st);
 int group_slots(int n);
+int scan_slots_prune();  // persistent grid of the band-pass scan (SMs x resident CTAs)
 // tracked full-row chunks: schedule of the first chunk (after the band passes)
 void launch_track_init(TryCtl* ctl, int N, int m, bool bands_ran, cudaStream_t st);
 void launch_seed_init(const double* t, int n, int m, int L, int kA, int nb, double* qt, cudaStream_t st);

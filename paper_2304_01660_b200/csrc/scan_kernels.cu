@@ -24,6 +24,9 @@
 // terms are computed in parallel.
 #include <float.h>
 #include <limits.h>
+#include <stdlib.h>
+
+#include <algorithm>
 
 #include "common.cuh"
 #include "engine_internal.h"
@@ -38,10 +41,13 @@ constexpr double kSlack = 1e-9;           // absolute corr slack around the thre
 constexpr int kRowsPad = kMaxRows + kDiag + 1;
 constexpr int kQPad = kMaxRows + kDiag + kW + kDiag;
 
+// Per-mode shared memory: the band passes need neither the collection
+// thresholds nor the row-max keys, which frees 4 KB per CTA (7 CTAs per SM).
+template <int MODE>
 struct __align__(16) ScanSmem {
-    float4 crow[kRowsPad];  // per row: {cdf, cdg, tc, cn}
-    float cy[kRowsPad];     // kCollect: per-row collection threshold
-    unsigned ykey[kRowsPad];
+    float4 crow[kRowsPad];                           // per row: {cdf, cdg, tc, cn}
+    float cy[MODE == kCollect ? kRowsPad : 1];       // kCollect: per-row collection threshold
+    unsigned ykey[MODE == kPruneTrack ? kRowsPad : 1];  // kPruneTrack: row max keys
     union {
         struct {
             float2 qd[kQPad];  // (df, dg) of the q side
@@ -225,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
     pdl_enter();
     // static shared memory (33 KB): CTA-relative LDS addressing, no shared
     // window base to rematerialise inside the walk
-    __shared__ ScanSmem S;
+    __shared__ ScanSmem<MODE> S;
     const int tid = threadIdx.x;
     const long long slots = tile_slots(p);
     // persistent CTAs: slots are fetched dynamically; rank r owns slots r, r+world, ...
@@ -439,7 +445,9 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
         S.u.walk.qd[u] = make_float2(a, b);
         // an invalid q gets a NaN norm: its x = cov*qn is NaN, which never passes a
         // threshold test and is ignored by fmaxf (a constant q keeps qn = 0, x = 0)
-        S.u.walk.qn[u] = valid ? nn : __int_as_float(0x7fffffff);
+        // (a degenerate q, sigma < eps, is NaN too: its reference distances are
+        // not what the FP32 model predicts, every pair with it is decided exactly)
+        S.u.walk.qn[u] = (valid && nn != 0.f) ? nn : __int_as_float(0x7fffffff);
     }
     cn_min = -warp_max(-cn_min);
     qn_min = -warp_max(-qn_min);
@@ -481,9 +489,9 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
         } else if (!live) {
             tc = kNoEval;
         } else if (cn == 0.f) {
-            // constant row: full rows take the exact-convention slow path on every
-            // cell; band passes leave it to them
-            tc = MODE == kPrune ? kNoEval : -FLT_MAX;
+            // degenerate row (sigma < eps): decided exactly against every q
+            // (k_degenerate_pairs), never by the FP32 walk
+            tc = kNoEval;
         } else if (MODE == kPrune) {
             // band passes only make certain kills: every cell with x > tk has
             // corr - eps_cell > thr0 (eps_cell <= eps_row); knife edges are left
@@ -728,6 +736,49 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_ref_pairs(const double* __r
     }
 }
 
+// Degenerate rows (sigma < eps by the rolling statistics): the reference's
+// distance for such a window depends on its own one-pass statistics
+// (znormalize: all-zero z -> the 0 / 2m conventions, else tiny equal z), so
+// every pair that involves one is decided by the exact routine:
+//   A: every listed row still alive x every degenerate q (|c - q| >= m);
+//   B: every degenerate row x every q (|c - q| >= m).
+// d < r^2 kills the row; every d feeds its exact-nn key.  One warp per pair.
+__global__ void __launch_bounds__(kPairWarps * 32) k_degenerate_pairs(const double* __restrict__ t, int m, int N,
+                                                                      const int* __restrict__ list,
+                                                                      const TryCtl* __restrict__ ctl,
+                                                                      const int* __restrict__ cr,
+                                                                      const int* __restrict__ deg, double r_sq,
+                                                                      uint8_t* alive,
+                                                                      unsigned long long* nnkey, int rank,
+                                                                      int world) {
+    pdl_enter();
+    __shared__ double buf[kPairWarps][256];
+    const int D = cr[2];
+    if (D == 0) return;
+    const long long nl = ctl->alive;
+    const long long totA = nl * D, tot = totA + (long long)D * N;
+    const int w = threadIdx.x >> 5;
+    for (long long e = ((long long)blockIdx.x * kPairWarps + w) * world + rank; e < tot;
+         e += (long long)gridDim.x * kPairWarps * world) {
+        int c, q;
+        if (e < totA) {
+            c = list[e / D];
+            q = deg[e % D];
+            if (!alive[c]) continue;
+        } else {
+            const long long f = e - totA;
+            c = deg[f / N];
+            q = (int)(f % N);
+        }
+        if (abs(c - q) < m) continue;
+        const double d = ref_dist_warp(t, m, c, q, buf[w]);
+        if ((threadIdx.x & 31) == 0) {
+            if (d < r_sq) alive[c] = 0;
+            atomicMin(&nnkey[c], (unsigned long long)__double_as_longlong(d));
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // flags / compaction / grouping / survivor kernels.  None of them takes a
 // count from the host: counts live in TryCtl, so one DRAG try is a single
@@ -736,13 +787,15 @@ constexpr int kSmallGrid = 148 * 2;  // grid-stride kernels over device-sized li
 
 // try start: every row undecided, counters reset, route maxima cleared
 __global__ void k_try_init(uint8_t* __restrict__ alive, unsigned* __restrict__ ymax, unsigned* __restrict__ emax,
-                           float* __restrict__ ythr, int N, TryCtl* ctl, unsigned long long* acc, int band_k0) {
+                           float* __restrict__ ythr, unsigned long long* __restrict__ nnkey, int N, TryCtl* ctl,
+                           unsigned long long* acc, int band_k0) {
     pdl_enter();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
         alive[i] = 1;
         ymax[i] = 0u;
         emax[i] = 0u;
         ythr[i] = FLT_MAX;  // collection off unless the row gets exact nn this try
+        nnkey[i] = 0x7ff0000000000000ull;  // exact nn^2 (+inf), min-reduced by every exact pair
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         ctl->alive = N;
@@ -1016,7 +1069,7 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
                                                         unsigned long long* status, unsigned epoch, TryCtl* ctl,
                                                         int gate, int2* __restrict__ groups,
                                                         int2* __restrict__ slots, int m, int fixed_span,
-                                                        float band_keep, int scan_slots) {
+                                                        float band_keep, int scan_slots, int band_few) {
     pdl_enter();
     if (gated_off(ctl, gate)) return;
     __shared__ int s_bid, s_excl, s_last, s_k;
@@ -1172,7 +1225,7 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
             const int prev = ctl->alive;
             ctl->prev = prev;
             ctl->passes = gate + 1;
-            if (total == 0 || total <= max(64, n / 4096)) {
+            if (total == 0 || total <= max(band_few, n / 4096)) {
                 ctl->stop = gate;
                 ctl->stop_why = 1;
             } else if ((double)total > (double)band_keep * (double)prev) {
@@ -1347,8 +1400,9 @@ __global__ void __launch_bounds__(1024) k_survivors(const int* __restrict__ list
     }
     __syncthreads();
     int ec = sc;
-    // 2. top-k filter
-    if (need > 0 && sc > need) {
+    // 2. top-k filter (the nn intervals come from the FP32 route maxima over
+    // regular q only: with degenerate rows present every survivor gets exact nn)
+    if (need > 0 && sc > need && cr_raw[2] == 0) {
         for (int e = threadIdx.x; e < sc; e += blockDim.x) {
             double l, h;
             nn_interval(cand[e], ymax, emax, nrm, cr, N, m, l, h);
@@ -1422,10 +1476,7 @@ __global__ void __launch_bounds__(1024) k_survivors(const int* __restrict__ list
     // it may be the reference's minimiser.
     for (int e = threadIdx.x; e < ec; e += blockDim.x) {
         const int c = cand[e];
-        if (nrm[c] == 0.f) {
-            nnkey[c] = (unsigned long long)__double_as_longlong(const_nn(c, cr, N, m));
-            continue;  // never collected (cn == 0 rows are not evaluated)
-        }
+        if (nrm[c] == 0.f) continue;  // degenerate: exact nn from k_degenerate_pairs, never collected
         const unsigned k = ymax[c];
         float th = -FLT_MAX;  // no tracked data: collect everything
         if (k > 1u) {
@@ -1434,7 +1485,6 @@ __global__ void __launch_bounds__(1024) k_survivors(const int* __restrict__ list
             th = nextafterf(nextafterf(l - fabsf(l) * 2.4e-7f, -FLT_MAX), -FLT_MAX);
         }
         ythr[c] = th;
-        nnkey[c] = 0x7ff0000000000000ull;  // +inf
     }
     if (threadIdx.x == 0) {
         ctl->sc = sc;
@@ -1505,7 +1555,7 @@ static int grid_for(long long work, int threads) {
     return (int)b;
 }
 
-size_t scan_smem_bytes() { return sizeof(ScanSmem); }
+size_t scan_smem_bytes() { return sizeof(ScanSmem<kPruneTrack>); }
 
 void scan_configure() {
     // the walk kernels want the largest shared-memory carveout (6 CTAs x 33 KB)
@@ -1524,6 +1574,7 @@ static int scan_grid() {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_scan<MODE>, kThreads, 0);
+        if (const char* e = std::getenv("TSD_SCAN_CTAS")) per = std::min(per, std::max(1, std::atoi(e)));
         g_scan_grid[MODE] = sms * (per > 0 ? per : 1);
     }
     return g_scan_grid[MODE];
@@ -1549,6 +1600,13 @@ void launch_ref_pairs(int mode, const double* t, int m, const int2* pairs, const
                                                              nnout);
 }
 
+void launch_degenerate_pairs(const double* t, int m, int N, const int* list, const TryCtl* ctl, const int* crange,
+                             const int* deg, double r_sq, uint8_t* alive, unsigned long long* nnkey, int rank,
+                             int world, cudaStream_t st) {
+    launch_pdl(k_degenerate_pairs, 148 * 4, kPairWarps * 32, st, t, m, N, list, ctl, crange, deg, r_sq, alive,
+               nnkey, rank, world);
+}
+
 void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const unsigned* ymax,
                       const unsigned* emax, const float* nrm, const int* crange, int N, int m, int need,
                       double* lo, double* hi, int* cand, float* ythr, unsigned long long* nnkey, int2* groups,
@@ -1557,9 +1615,9 @@ void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const 
                                     nnkey, groups, fixed_span);
 }
 
-void launch_try_init(uint8_t* alive, unsigned* ymax, unsigned* emax, float* ythr, int N, TryCtl* ctl,
-                     unsigned long long* acc, int band_k0, cudaStream_t st) {
-    launch_pdl(k_try_init, grid_for(N, 256), 256, st, alive, ymax, emax, ythr, N, ctl, acc, band_k0);
+void launch_try_init(uint8_t* alive, unsigned* ymax, unsigned* emax, float* ythr, unsigned long long* nnkey, int N,
+                     TryCtl* ctl, unsigned long long* acc, int band_k0, cudaStream_t st) {
+    launch_pdl(k_try_init, grid_for(N, 256), 256, st, alive, ymax, emax, ythr, nnkey, N, ctl, acc, band_k0);
 }
 
 int compact_blocks(int n) { return (n + kCompactTile - 1) / kCompactTile; }
@@ -1572,11 +1630,12 @@ void launch_track_init(TryCtl* ctl, int N, int m, bool bands_ran, cudaStream_t s
 
 void launch_compact_group(const uint8_t* a, int n, int* out, unsigned long long* status, unsigned epoch,
                           TryCtl* ctl, int gate, int2* groups, int2* slots, int m, int fixed_span, float band_keep,
-                          cudaStream_t st) {
+                          int band_few, cudaStream_t st) {
     launch_pdl(k_compact_group, compact_blocks(n), kCompactBlock, st, a, n, out, status, epoch, ctl, gate, groups, slots,
                                                                m, fixed_span, band_keep,
                                                                gate == kGateTrack ? scan_grid<kPruneTrack>()
-                                                                                  : scan_slots_prune());
+                                                                                  : scan_slots_prune(),
+                                                               band_few);
 }
 
 int group_slots(int n) { return compact_blocks(n) * 504; }

@@ -116,11 +116,13 @@ __global__ void k_advance(const double* __restrict__ t, int n, int m, double* __
 // (centered-covariance diagonal step: cov(i,j) = cov(i-1,j-1) + df_i dg_j + df_j dg_i)
 // nrm[i] = 1 / (sqrt(m) sigma_i), 0 for a constant subsequence.
 // Per-length FP32 walk operands and the constant-row range
-// (cr[0] = max(N - i), cr[1] = max(i + 1) over rows with sigma < eps; cleared
+// (cr[0] = max(N - i), cr[1] = max(i + 1) over rows with sigma < eps, cr[2] their
+// count, listed in deg; cleared
 // to 0 before the launch, 0 meaning none).
 __global__ void k_derive(const double* __restrict__ t, int m, int cnt, const double* __restrict__ mu,
                          const double* __restrict__ sig, float* __restrict__ df,
-                         float* __restrict__ dg, float* __restrict__ nrm, int* __restrict__ cr) {
+                         float* __restrict__ dg, float* __restrict__ nrm, int* __restrict__ cr,
+                         int* __restrict__ deg) {
     pdl_enter();
     const double sqm = sqrt((double)m);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
@@ -129,6 +131,7 @@ __global__ void k_derive(const double* __restrict__ t, int m, int cnt, const dou
         if (s < kSigmaEps) {
             atomicMax(&cr[0], cnt - i);
             atomicMax(&cr[1], i + 1);
+            deg[atomicAdd(&cr[2], 1)] = i;  // decided exactly, against every q
         }
         if (i == 0) {
             df[0] = 0.f;
@@ -165,12 +168,13 @@ __global__ void k_next_length(const double* __restrict__ t, int n, int m, const 
                               const double* __restrict__ sig_in, double* __restrict__ mu_out,
                               double* __restrict__ sig_out, float* __restrict__ df, float* __restrict__ dg,
                               float* __restrict__ nrm, int* __restrict__ cr, int* __restrict__ cr_next, int L, int kA,
-                              int nb, double* __restrict__ qt) {
+                              int nb, double* __restrict__ qt, int* __restrict__ deg) {
     pdl_enter();
     const int m1 = m + 1, cnt = n - m;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         cr_next[0] = 0;
         cr_next[1] = 0;
+        cr_next[2] = 0;
     }
     const double sqm = sqrt((double)m1);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
@@ -182,6 +186,7 @@ __global__ void k_next_length(const double* __restrict__ t, int n, int m, const 
         if (s < kSigmaEps) {
             atomicMax(&cr[0], cnt - i);
             atomicMax(&cr[1], i + 1);
+            deg[atomicAdd(&cr[2], 1)] = i;  // decided exactly, against every q
         }
         if (i == 0) {
             df[0] = 0.f;
@@ -226,16 +231,15 @@ void launch_advance_stats(const double* t, int n, int m, double* mu, double* sig
 }
 
 void launch_derive(const double* t, int m, int cnt, const double* mu, const double* sig, float* df,
-                   float* dg, float* nrm, int* crange, cudaStream_t st) {
-    cudaMemsetAsync(crange, 0, 2 * sizeof(int), st);
-    launch_pdl(k_derive, grid_for(cnt, 256), 256, st, t, m, cnt, mu, sig, df, dg, nrm, crange);
+                   float* dg, float* nrm, int* crange, int* deg, cudaStream_t st) {
+    launch_pdl(k_derive, grid_for(cnt, 256), 256, st, t, m, cnt, mu, sig, df, dg, nrm, crange, deg);
 }
 
 void launch_next_length(const double* t, int n, int m, const double* mu_in, const double* sig_in, double* mu_out,
                         double* sig_out, float* df, float* dg, float* nrm, int* cr, int* cr_next, int L, int kA,
-                        int nb, double* qt, cudaStream_t st) {
+                        int nb, double* qt, int* deg, cudaStream_t st) {
     launch_pdl(k_next_length, grid_for(n - m, 256), 256, st, t, n, m, mu_in, sig_in, mu_out, sig_out, df, dg, nrm, cr,
-               cr_next, L, kA, nb, qt);
+               cr_next, L, kA, nb, qt, deg);
 }
 
 }  // namespace tsd

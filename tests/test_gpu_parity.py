@@ -239,3 +239,44 @@ def test_golden_discords_are_matrix_profile_maxima(engine, name, lengths):
         assert [int(i) + 1 for i in top] == [r[0] for r in e["records"]], m
         for i, r in zip(top, e["records"]):
             assert abs(mp[i] - hexf(r[1])) <= 1e-9 * hexf(r[1]), (m, mp[i], hexf(r[1]))
+
+
+# ---- constant stretches: the sigma < eps conventions of reference_sq_dist ------
+def flat_series(oracle, n, seed, flats):
+    x = oracle.gen_randomwalk(n, seed).copy()
+    for a, length, level in flats:
+        x[a:a + length] = level
+    return x
+
+
+@pytest.mark.parametrize("case", range(4))
+def test_constant_stretches_range_sets(engine, oracle, case):
+    # exactly constant windows (nrm = 0): d = 0 between two of them, 2m against
+    # anything else; they never enter the FP32 band passes and are decided in
+    # the full-row stage / survivors with the exact conventions
+    rng = np.random.default_rng(40 + case)
+    n = int(rng.integers(800, 2500))
+    flats = [(int(rng.integers(0, n - 200)), int(rng.integers(20, 120)), float(rng.normal() * 5))
+             for _ in range(int(rng.integers(1, 4)))]
+    x = flat_series(oracle, n, 900 + case, flats)
+    engine.set_series(x)
+    for m in (8, 16, 40):
+        nn = oracle.brute_force_nn(x, m)
+        s = np.sort(nn[np.isfinite(nn)])
+        assert np.array_equal(engine.brute_force_nn(m), nn), (case, m)
+        for r_sq in (float(s[len(s) // 2]), float(s[-3]), 2.0 * m, 2.0 * m + 1e-9, 1e-12):
+            got = engine.pardrag(m, r_sq, seglen=max(2 * m, 64))
+            assert recs_list(got) == recs_list(oracle.range_discords(x, m, r_sq)), (case, m, r_sq)
+
+
+def test_constant_stretches_merlin(engine, oracle):
+    x = flat_series(oracle, 3000, 77, [(500, 150, 3.0), (2000, 90, -1.0)])
+    engine.set_series(x)
+    for top_k in (1, 3):
+        rep = engine.merlin_full(8, 24, top_k=top_k, seglen=128)
+        exp = oracle.merlin(x, 8, 24, top_k=top_k, seglen=128)
+        for k, m in enumerate(range(8, 25)):
+            assert (m in rep.failed_lengths) == bool(exp["failed"][k]), m
+            if m not in rep.failed_lengths:
+                assert recs_list(rep.per_length[m]) == recs_list(exp["recs"][k][: exp["counts"][k]]), m
+        assert np.array_equal(rep.final_r, exp["final_r"]) and np.array_equal(rep.retries, exp["retries"])
