@@ -76,7 +76,6 @@ struct TryCtl {
 // compaction / grouping gates: a band pass index (>= 0: skipped once the band
 // passes stopped before it), or one of these
 constexpr int kGateNone = -1;   // always runs
-constexpr int kGateQueue = -2;  // skipped when no knife edge was queued (or nothing is alive)
 constexpr int kGateTrack = -3;  // tracked chunks: skipped once the chunks are done
 
 enum ScanMode : int {

@@ -56,7 +56,7 @@ void launch_degenerate_pairs(const double* t, int m, int N, const int* list, con
 void launch_try_init(uint8_t* alive, unsigned* ymax, unsigned* emax, float* ythr, unsigned long long* nnkey, int N,
                      TryCtl* ctl, unsigned long long* acc, int band_k0, cudaStream_t st);
 int compact_blocks(int n);
-// gate: band pass index (>= 0), kGateNone or kGateQueue (common.cuh)
+// gate: band pass index (>= 0), kGateNone or kGateTrack (common.cuh)
 // compaction + break rule + grouping in one kernel (status: >= compact_blocks(n)
 // words; slots: group_slots(n) entries)
 void launch_compact_group(const uint8_t* a, int n, int* out, unsigned long long* status, unsigned epoch,

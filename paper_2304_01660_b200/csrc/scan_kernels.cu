@@ -821,7 +821,6 @@ __global__ void k_try_init(uint8_t* __restrict__ alive, unsigned* __restrict__ y
 __device__ __forceinline__ bool gated_off(const TryCtl* ctl, int gate) {
     if (gate >= 0) return ctl->stop < gate;
     if (gate == kGateTrack) return ctl->tphase >= 2;
-    if (gate == kGateQueue) return ctl->queue == 0 || ctl->alive == 0;
     return false;
 }
 
@@ -1351,14 +1350,6 @@ __device__ __forceinline__ unsigned long long dkey(double d) {  // order-preserv
 __device__ __forceinline__ void crange_decode(const int* cr, int N, int out[2]) {
     out[0] = N - cr[0];
     out[1] = cr[1] - 1;
-}
-
-// nn by the constant conventions of reference_sq_dist for a constant row c:
-// 0 with an admissible constant partner, else 2m, else inf
-__device__ __forceinline__ double const_nn(int c, const int cr[2], int N, int m) {
-    if (c - cr[0] >= m || cr[1] - c >= m) return 0.0;
-    if (c - m >= 0 || c + m <= N - 1) return 2.0 * (double)m;
-    return __longlong_as_double(0x7ff0000000000000ll);
 }
 
 // The survivors stage of a try in one CTA (1024 threads):
