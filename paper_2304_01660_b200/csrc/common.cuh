@@ -113,6 +113,7 @@ struct ScanParams {
     int K0, nb;          // kSpaceBlocks: diagonals [K0, K0 + nb*kW) on both sides (kSpaceBand: TryCtl)
     int L, kA;           // kSpaceSeed / kSpaceBlocks: block rows; kSpaceSeed: band offset
     int rank, world;     // tiles are dealt cyclically across ranks
+    int seed32;          // FP32 direct seeds (with their error term in E) outside the band passes too
     const double* seedqt;  // resident raw dot products QT(i, i+k) of the band-0 tiles (kW per tile)
     unsigned long long* acc;  // accounting: [0] cells walked, [1] cells evaluated, [2] seed dots
 };

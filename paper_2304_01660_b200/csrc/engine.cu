@@ -144,6 +144,8 @@ struct tsd_ctx {
     int track_hint = 0;    // ... and tracked chunks (plus the catch-all launch)
     int track_chunks = 1;  // cap on tracked launches per try (1: the catch-all alone)
     int band0_sides = 2;   // band 0 on both sides of every row, or the positive side only
+    int seed32_track = 0;    // FP32 seeds in the full-row launch (wider error band, half the seed cost)
+    int seed32_collect = 0;  // ... and in the collection launch
     float band_keep = 0.85f;  // band loop stops when a pass leaves more than this fraction alive
     int band_few = 256;       // ... or when at most max(band_few, N/4096) rows are left (C2: 64 -> 41.8 ms, 256 -> 41.2 ms)
     int result_prefix = 1024;  // records copied back with the try's single round trip
@@ -545,6 +547,7 @@ struct tsd_ctx {
         // near chunk [m, kend) for the rows still undecided.  The last launch
         // covers whatever chunks the enqueued count did not reach.
         ScanParams q = P;
+        q.seed32 = seed32_track;
         launch_track_init(C, N, (int)m, r_sq > 0.0 && enq_passes > 0, st);
         ck(cudaGetLastError(), "track init");
         ctr.kernel_launches += 1;
@@ -585,6 +588,7 @@ struct tsd_ctx {
         ck(cudaGetLastError(), "survivors");
         const int* ex = cand.p;  // rows whose exact nn is computed (count: C->ec)
         q.space = kSpaceFull;  // every diagonal of the exact-nn rows' groups
+        q.seed32 = seed32_collect;
         scan(kCollect, q);
         launch_ref_pairs(1, t.p, (int)m, coll.p, &C->coll, kCollCap, r_sq, alive.p, nnkey.p, C,
                          world == 1 ? ex : nullptr, nnout.p, st);
@@ -1375,6 +1379,8 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "sparse_rows") c->sparse_rows = std::max(0, std::min(kMaxRows, (int)v));
         else if (k == "err_scale") c->err_k = v;
         else if (k == "scan_events") c->scan_events = v != 0.0;
+        else if (k == "seed32_track") c->seed32_track = v != 0.0;
+        else if (k == "seed32_collect") c->seed32_collect = v != 0.0;
         else if (k == "band0_sides") c->band0_sides = v <= 1.0 ? 1 : 2;
         else if (k == "track_chunks") c->track_chunks = std::max(1, std::min(16, (int)v));
         else if (k == "band_few") c->band_few = std::max(0, (int)v);

@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
             const int q = dir > 0 ? qbase + u : qbase - u;
             cov[j] = (q >= 0 && q < N) ? (float)(qt[j] - mmu * p.mu[q]) : 0.f;
         }
-    } else if (MODE == kPrune) {
+    } else if (MODE == kPrune || p.seed32) {
         // band passes only make certain kills, so their seeds may be FP32: the
         // rounding of a = t[c+p]-mu_c, w = t[q+p]-anchor and of the m-term sums is
         // bounded by E_seed (added to the tile's error bound below)
