@@ -132,6 +132,15 @@ def test_merlin_golden_c3s(engine):
     check_merlin(rep, fx)
 
 
+def test_merlin_golden_c3(engine):
+    # BASELINE config 3 in full: ECG-like n=500,000, lengths 64..512 (449 lengths;
+    # the reference needed 21 min on 6 threads)
+    fx = load_golden("c3.json")
+    engine.set_series(series_of(fx["input"]))
+    rep = engine.merlin_full(fx["min_len"], fx["max_len"], top_k=fx["top_k"], seglen=fx["seglen"])
+    check_merlin(rep, fx)
+
+
 def test_merlin_golden_c5s(engine):
     # BASELINE config 5 (n=2,000,000 random walk, top-3), its first 32 lengths
     fx = load_golden("c5s.json")
@@ -224,6 +233,7 @@ def test_matrix_profile_fp64_vs_reference_bruteforce(engine, oracle):
 
 
 @pytest.mark.parametrize("name,lengths", [("c4.json", (512, 777, 1024)), ("c3s.json", (64, 100, 127)),
+                                          ("c3.json", (300, 512)),
                                           ("c5s.json", (128, 159)), ("c5.json", (384, 640))])
 def test_golden_discords_are_matrix_profile_maxima(engine, name, lengths):
     # full-size parity by a second, independent route: the reference's discords of
