@@ -157,6 +157,19 @@ int tsd_group_merlin(tsd_group* g, int64_t min_len, int64_t max_len, const tsd_m
 int tsd_group_pardrag(tsd_group* g, int64_t m, double r_sq, int64_t seglen, tsd_record* out, int64_t cap,
                       int64_t* count);
 
+/* ---- cross-process ranks over CUDA IPC (one process per GPU) ---------------
+ * The fused peer-store transport of tsd_group_* between processes: every rank
+ *  1. calls tsd_ipc_export(ctx, rows, h) after tsd_series_set (rows >= the series
+ *     length; the shared kill-flag / row-max / exact-nn arrays are allocated
+ *     once at that size) and gets 320 bytes of CUDA IPC handles;
+ *  2. gathers all ranks' 320-byte blocks in rank order (e.g. all_gather_object);
+ *  3. rank 0 calls tsd_ipc_join first (it creates the shared-memory barrier
+ *     `shm_name`), then the others, with identical shm_name;
+ *  4. runs tsd_merlin / tsd_pardrag with identical arguments on every rank.
+ * Ranks may share a GPU.  tsd_ctx_join (NCCL) is the alternative transport. */
+int tsd_ipc_export(tsd_ctx* ctx, int64_t rows, uint8_t out_handles[320]);
+int tsd_ipc_join(tsd_ctx* ctx, int rank, int world, const uint8_t* all_handles, const char* shm_name);
+
 /* ---- heatmap / ranking on the device (heatmap.hpp) ------------------------
  * One ranked column: replaces tsdiscord::RankedDiscord (include/tsdiscord/heatmap.hpp:35-39). */
 typedef struct {

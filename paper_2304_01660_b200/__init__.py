@@ -34,6 +34,7 @@ EXPORTS = (
     "tsd_heatmap_build", "tsd_heatmap_set", "tsd_heatmap_rank",
     "tsd_group_create", "tsd_group_destroy", "tsd_group_last_error", "tsd_group_size", "tsd_group_ctx",
     "tsd_group_series_set", "tsd_group_merlin", "tsd_group_pardrag", "tsd_matrix_profile_fp64",
+    "tsd_ipc_export", "tsd_ipc_join",
 )
 
 
@@ -102,6 +103,8 @@ def load_library(path: str = LIB_PATH):
     f("tsd_merlin", C.c_int, [vp, _i64, _i64, C.POINTER(_Opts), _ip, vp, _dp, _ip, _u8])
     f("tsd_brute_force_nn", C.c_int, [vp, _i64, _dp])
     f("tsd_matrix_profile_fp64", C.c_int, [vp, _i64, _dp])
+    f("tsd_ipc_export", C.c_int, [vp, _i64, C.c_char_p])
+    f("tsd_ipc_join", C.c_int, [vp, C.c_int, C.c_int, C.c_char_p, C.c_char_p])
     f("tsd_gen_randomwalk", C.c_int, [_i64, C.c_uint64, _dp])
     f("tsd_get_counters", C.c_int, [vp, C.POINTER(Counters)])
     f("tsd_reset_counters", C.c_int, [vp])
@@ -216,6 +219,19 @@ class Engine:
         buf = C.create_string_buffer(128)
         _host_check(load_library().tsd_nccl_unique_id(buf))
         return buf.raw
+
+    def ipc_export(self, rows: int) -> bytes:
+        """Cross-process ranks, step 1: allocate the shared arrays (rows >= series
+        length) and return this rank's 320 bytes of CUDA IPC handles."""
+        buf = C.create_string_buffer(320)
+        self._check(self._L.tsd_ipc_export(self._h, rows, buf))
+        return buf.raw
+
+    def ipc_join(self, rank: int, world: int, handles: list, shm_name: str):
+        """Step 2: join with every rank's handles (rank order); rank 0 first."""
+        blob = b"".join(handles)
+        assert len(blob) == 320 * world
+        self._check(self._L.tsd_ipc_join(self._h, rank, world, blob, shm_name.encode()))
 
     def join(self, rank: int, world: int, nccl_id: bytes | None = None):
         idb = C.create_string_buffer(nccl_id or b"\0" * 128, 128)
@@ -385,6 +401,14 @@ class Group:
         c = Counters()
         self._check(self._L.tsd_get_counters(self._L.tsd_group_ctx(self._h, rank), C.byref(c)))
         return c.as_dict()
+
+    def set_param(self, key: str, value: float):
+        """Tuning knob on every rank (e.g. fused_peers=0: all-reduce kernels
+        instead of fused peer stores)."""
+        for r in range(self.size):
+            rc = self._L.tsd_set_param(self._L.tsd_group_ctx(self._h, r), key.encode(), float(value))
+            if rc != TSD_OK:
+                _raise(rc, "set_param failed")
 
     def pardrag(self, m: int, r_sq: float, seglen: int) -> np.ndarray:
         N = max(self.n - m + 1, 1)

@@ -84,6 +84,39 @@ enum ScanMode : int {
     kCollect = 2      // survivors: push every pair that may attain the row's exact minimum
 };
 
+// Fused rank reduction over peer memory (in-process rank group): a kernel that
+// kills a row, or raises a row maximum, stores into EVERY rank's array (peer
+// stores / atomics over NVLink, plain ones on a shared device).  Kills are
+// monotone byte stores and maxima are atomicMax, so the stores themselves are
+// the AND / MAX all-reduce; the ranks only meet at an event barrier afterwards.
+constexpr int kMaxPeers = 8;
+struct Peers {
+    uint8_t* alive[kMaxPeers];
+    unsigned* ymax[kMaxPeers];
+    unsigned* emax[kMaxPeers];
+    unsigned long long* nnkey[kMaxPeers];
+    int n;  // 0: local only
+};
+
+__device__ __forceinline__ void peer_min_key(const Peers& P, unsigned long long* local, int c,
+                                             unsigned long long v) {
+    if (P.n > 1) {
+#pragma unroll 1
+        for (int r = 0; r < P.n; ++r) atomicMin(&P.nnkey[r][c], v);
+    } else {
+        atomicMin(&local[c], v);
+    }
+}
+
+__device__ __forceinline__ void peer_kill(const Peers& P, uint8_t* local, int c) {
+    if (P.n > 1) {
+#pragma unroll 1
+        for (int r = 0; r < P.n; ++r) P.alive[r][c] = 0;
+    } else {
+        local[c] = 0;
+    }
+}
+
 struct ScanParams {
     const double* t;     // series (n)
     const double* mu;    // FP64 rolling mean, length m (N)
@@ -114,6 +147,7 @@ struct ScanParams {
     int L, kA;           // kSpaceSeed / kSpaceBlocks: block rows; kSpaceSeed: band offset
     int rank, world;     // tiles are dealt cyclically across ranks
     int seed32;          // FP32 direct seeds (with their error term in E) outside the band passes too
+    Peers peers;         // fused cross-rank kills / maxima (n > 1), else local
     const double* seedqt;  // resident raw dot products QT(i, i+k) of the band-0 tiles (kW per tile)
     unsigned long long* acc;  // accounting: [0] cells walked, [1] cells evaluated, [2] seed dots
 };

@@ -213,6 +213,64 @@ struct tsd_ctx {
         ck(cudaMemcpyAsync(p, red_tmp.p, cnt * esize, cudaMemcpyDeviceToDevice, st), "D2D");
         ctr.kernel_launches += 1;
     }
+    // Fused transport (peer group): the kernels store kills and row maxima into
+    // every rank's arrays (Peers), so an "all-reduce" of alive / ymax / emax is
+    // only an event barrier between the ranks' streams.
+    bool fused = true;
+    Peers peers{};
+    // cross-process ranks (tsd_ipc_*): peers fixed at join, barrier in shared memory
+    ShmBarrier* ipc_bar = nullptr;
+    cudaEvent_t ipc_ev = nullptr;                  // this rank's exported barrier event
+    std::vector<cudaEvent_t> ipc_peer_ev;          // every rank's event (own included)
+    std::vector<void*> ipc_opened;                 // peer mappings to close
+    int64_t ipc_rows = 0;                          // capacity of the shared arrays
+    bool ipc_host_sync = std::getenv("TSD_IPC_SYNC") != nullptr;
+    void peer_publish() {
+        if (ipc_bar) return;  // fixed at join
+        peers.n = 0;
+        if (!group || !fused || world <= 1) return;
+        PeerGroup& g = *group;
+        g.p_alive[rank] = alive.p;
+        g.p_ymax[rank] = ymax.p;
+        g.p_emax[rank] = emax.p;
+        g.p_nnkey[rank] = nnkey.p;
+        g.bar.wait();
+        peers.n = g.n;
+        for (int r = 0; r < g.n; ++r) {
+            peers.alive[r] = static_cast<uint8_t*>(g.p_alive[r]);
+            peers.ymax[r] = static_cast<unsigned*>(g.p_ymax[r]);
+            peers.emax[r] = static_cast<unsigned*>(g.p_emax[r]);
+            peers.nnkey[r] = static_cast<unsigned long long*>(g.p_nnkey[r]);
+        }
+        g.bar.wait();  // the tables stay put until every rank has read them
+    }
+    void peer_barrier() {  // every rank's preceding kernels (and their remote stores) are done
+        if (ipc_bar) {
+            ck(cudaEventRecord(ipc_ev, st), "event");
+            if (ipc_host_sync) sync();  // this rank's work done on the device before the host barrier
+            ipc_bar->wait();
+            if (!ipc_host_sync)
+                for (int r = 0; r < world; ++r)
+                    if (r != rank) ck(cudaStreamWaitEvent(st, ipc_peer_ev[r], 0), "event wait");
+            ipc_bar->wait();
+            return;
+        }
+        PeerGroup& g = *group;
+        ck(cudaEventRecord(g.ev_in[rank], st), "event");
+        g.bar.wait();
+        for (int r = 0; r < g.n; ++r)
+            if (r != rank) ck(cudaStreamWaitEvent(st, g.ev_in[r], 0), "event wait");
+        g.bar.wait();  // nobody re-records its event before every rank has waited on it
+    }
+    void reduce_alive(int64_t N) {
+        if (peers.n > 1) peer_barrier();
+        else allreduce_min_u8(alive.p, N);
+    }
+    void reduce_maxima(int64_t N) {  // after reduce_alive of the same scan
+        if (peers.n > 1) return;
+        allreduce_max_u32(ymax.p, N);
+        allreduce_max_u32(emax.p, N);
+    }
     void allreduce_min_u8(uint8_t* p, size_t cnt) { allreduce(p, cnt, 0 /*u8 min*/, 1); }
     void allreduce_max_u32(unsigned* p, size_t cnt) { allreduce(p, cnt, 1 /*u32 max*/, 4); }
     void allreduce_min_u64(unsigned long long* p, size_t cnt) { allreduce(p, cnt, 2 /*u64 min*/, 8); }
@@ -342,6 +400,7 @@ struct tsd_ctx {
         p.rank = rank;
         p.world = world;
         p.acc = acc.p;
+        p.peers = peers;
         return p;
     }
 
@@ -412,6 +471,9 @@ struct tsd_ctx {
                              sparse_rows, band_keep, band_few, st);
         ck(cudaGetLastError(), "compact");
         ctr.kernel_launches += 1;
+        // fused peers: no rank's next scan may store kills into this rank's
+        // flags before this compaction has read them (the lists must agree)
+        if (peers.n > 1) peer_barrier();
     }
 
     // debug trace: one host round trip per stage (TSD_DEBUG only)
@@ -428,6 +490,7 @@ struct tsd_ctx {
     }
 
     void ensure_scan_buffers(int N) {
+        if (ipc_bar && N > ipc_rows) fail(TSD_EINVAL, "ipc group: series longer than at tsd_ipc_export");
         alive.ensure(N);
         queue.ensure(kQueueCap);
         coll.ensure(kCollCap);
@@ -486,6 +549,7 @@ struct tsd_ctx {
         ensure_scan_buffers(N);
         ev_used = 0;
         ctr.pardrag_calls += 1;
+        peer_publish();
         TryCtl* C = ctl.p;
         // band 0 is the band at kA (resident seed rows) or at m; later passes
         // continue from its end, with the device choosing their widths
@@ -496,6 +560,8 @@ struct tsd_ctx {
                         st);
         ck(cudaGetLastError(), "try init");
         ctr.kernel_launches += 1;
+        // fused peers: another rank's kills must not land before this rank's reset
+        if (peers.n > 1) peer_barrier();
         const ScanParams P = params(m, r_sq);
         std::vector<tsd_record> out;
 
@@ -531,7 +597,7 @@ struct tsd_ctx {
                     q.space = kSpaceBand;  // groups and bands set by the previous compaction
                 }
                 scan(kPrune, q);
-                allreduce_min_u8(alive.p, N);
+                reduce_alive(N);
                 compact(N, pass, m);
                 trace("band", m, r_sq, pass);
             }
@@ -559,25 +625,25 @@ struct tsd_ctx {
         for (int j = 0; j + 1 < twant; ++j) {
             q.space = kSpaceTrack;
             scan(kPruneTrack, q);
-            allreduce_min_u8(alive.p, N);
+            reduce_alive(N);
             compact(N, kGateTrack, m);
             trace("tracked", m, r_sq, j);
         }
         q.space = kSpaceTrackRest;
         scan(kPruneTrack, q);
-        allreduce_min_u8(alive.p, N);
-        allreduce_max_u32(ymax.p, N);
-        allreduce_max_u32(emax.p, N);
+        reduce_alive(N);
+        reduce_maxima(N);
         // knife edges: the reference's FP64 distance decides (pardrag.cpp:255)
         launch_ref_pairs(0, t.p, (int)m, queue.p, &C->queue, kQueueCap, r_sq, alive.p, nnkey.p, C, nullptr,
-                         nullptr, st);
+                         nullptr, peers, st);
         ck(cudaGetLastError(), "recheck");
-        allreduce_min_u8(alive.p, N);
+        reduce_alive(N);
 
         // degenerate rows: every pair with one is decided exactly
-        launch_degenerate_pairs(t.p, (int)m, N, list.p, C, cr_cur, deg.p, r_sq, alive.p, nnkey.p, rank, world, st);
+        launch_degenerate_pairs(t.p, (int)m, N, list.p, C, cr_cur, deg.p, r_sq, alive.p, nnkey.p, rank, world, peers,
+                                st);
         ck(cudaGetLastError(), "degenerate pairs");
-        allreduce_min_u8(alive.p, N);
+        reduce_alive(N);
         ctr.kernel_launches += 1;
 
         // ---- survivors: exact nearest neighbours (pardrag.cpp:378-416).  One
@@ -591,10 +657,11 @@ struct tsd_ctx {
         q.seed32 = seed32_collect;
         scan(kCollect, q);
         launch_ref_pairs(1, t.p, (int)m, coll.p, &C->coll, kCollCap, r_sq, alive.p, nnkey.p, C,
-                         world == 1 ? ex : nullptr, nnout.p, st);
+                         world == 1 ? ex : nullptr, nnout.p, peers, st);
         ck(cudaGetLastError(), "exact");
         if (world > 1) {
-            allreduce_min_u64(nnkey.p, N);
+            if (peers.n > 1) peer_barrier();  // every rank's exact pairs reached every nnkey
+            else allreduce_min_u64(nnkey.p, N);
             launch_gather_nn(ex, &C->ec, nnkey.p, nnout.p, st);
             ck(cudaGetLastError(), "gather");
             ctr.kernel_launches += 1;
@@ -780,6 +847,11 @@ void tsd_ctx_destroy(tsd_ctx* c) {
         fprintf(stderr, "[tsd] host ms: wall %.1f wait %.1f\n", c->ctr.host_wall_ms, c->ctr.host_wait_ms);
     cudaSetDevice(c->device);
     if (c->comm) nccl_destroy(c->comm);
+    for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+    for (int r = 0; r < (int)c->ipc_peer_ev.size(); ++r)
+        if (r != c->rank && c->ipc_peer_ev[r]) cudaEventDestroy(c->ipc_peer_ev[r]);
+    if (c->ipc_ev) cudaEventDestroy(c->ipc_ev);
+    delete c->ipc_bar;
     c->t.release();
     c->mu.release();
     c->sig.release();
@@ -1154,6 +1226,74 @@ int tsd_heatmap_rank(tsd_ctx* c, int64_t k, tsd_ranked* out, int64_t* count) {
     });
 }
 
+// ---- cross-process ranks over CUDA IPC -------------------------------------------
+int tsd_ipc_export(tsd_ctx* c, int64_t rows, uint8_t out[5 * 64]) {
+    return guard(c, [&] {
+        if (rows < 1) fail(TSD_EINVAL, "ipc export: rows must be positive");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        // the shared arrays are allocated once, at their final size
+        c->alive.release();
+        c->ymax.release();
+        c->emax.release();
+        c->nnkey.release();
+        c->alive.ensure(rows);
+        c->ymax.ensure(rows);
+        c->emax.ensure(rows);
+        c->nnkey.ensure(rows);
+        c->ipc_rows = rows;
+        if (!c->ipc_ev)
+            ck(cudaEventCreateWithFlags(&c->ipc_ev, cudaEventDisableTiming | cudaEventInterprocess), "ipc event");
+        void* ptrs[4] = {c->alive.p, c->ymax.p, c->emax.p, c->nnkey.p};
+        for (int k = 0; k < 4; ++k) {
+            cudaIpcMemHandle_t h;
+            ck(cudaIpcGetMemHandle(&h, ptrs[k]), "cudaIpcGetMemHandle");
+            std::memcpy(out + 64 * k, &h, sizeof(h) < 64 ? sizeof(h) : 64);
+        }
+        cudaIpcEventHandle_t eh;
+        ck(cudaIpcGetEventHandle(&eh, c->ipc_ev), "cudaIpcGetEventHandle");
+        std::memcpy(out + 256, &eh, sizeof(eh) < 64 ? sizeof(eh) : 64);
+    });
+}
+
+int tsd_ipc_join(tsd_ctx* c, int rank, int world, const uint8_t* handles, const char* shm_name) {
+    return guard(c, [&] {
+        if (world < 2 || world > kMaxPeers || rank < 0 || rank >= world) fail(TSD_EINVAL, "bad rank/world");
+        if (c->ipc_rows == 0 || !c->ipc_ev) fail(TSD_EINVAL, "ipc join: call tsd_ipc_export first");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        c->rank = rank;
+        c->world = world;
+        c->peers = Peers{};
+        c->peers.n = world;
+        c->ipc_peer_ev.assign(world, nullptr);
+        for (int r = 0; r < world; ++r) {
+            const uint8_t* h = handles + (size_t)r * 320;
+            void* p[4];
+            if (r == rank) {
+                p[0] = c->alive.p;
+                p[1] = c->ymax.p;
+                p[2] = c->emax.p;
+                p[3] = c->nnkey.p;
+                c->ipc_peer_ev[r] = c->ipc_ev;
+            } else {
+                for (int k = 0; k < 4; ++k) {
+                    cudaIpcMemHandle_t mh;
+                    std::memcpy(&mh, h + 64 * k, sizeof(mh) < 64 ? sizeof(mh) : 64);
+                    ck(cudaIpcOpenMemHandle(&p[k], mh, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+                    c->ipc_opened.push_back(p[k]);
+                }
+                cudaIpcEventHandle_t eh;
+                std::memcpy(&eh, h + 256, sizeof(eh) < 64 ? sizeof(eh) : 64);
+                ck(cudaIpcOpenEventHandle(&c->ipc_peer_ev[r], eh), "cudaIpcOpenEventHandle");
+            }
+            c->peers.alive[r] = static_cast<uint8_t*>(p[0]);
+            c->peers.ymax[r] = static_cast<unsigned*>(p[1]);
+            c->peers.emax[r] = static_cast<unsigned*>(p[2]);
+            c->peers.nnkey[r] = static_cast<unsigned long long*>(p[3]);
+        }
+        c->ipc_bar = new ShmBarrier(shm_name ? shm_name : "/tsd_ipc", world, rank == 0);
+    });
+}
+
 // ---- in-process rank group ---------------------------------------------------
 struct tsd_group {
     std::vector<tsd_ctx*> ctx;
@@ -1379,6 +1519,7 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "sparse_rows") c->sparse_rows = std::max(0, std::min(kMaxRows, (int)v));
         else if (k == "err_scale") c->err_k = v;
         else if (k == "scan_events") c->scan_events = v != 0.0;
+        else if (k == "fused_peers") c->fused = v != 0.0;
         else if (k == "seed32_track") c->seed32_track = v != 0.0;
         else if (k == "seed32_collect") c->seed32_collect = v != 0.0;
         else if (k == "band0_sides") c->band0_sides = v <= 1.0 ? 1 : 2;

@@ -43,7 +43,7 @@ void launch_scan(int mode, const ScanParams& p, cudaStream_t st);
 // gathers nnout[e] = nn(ex[e]) for e < ctl->ec — single rank only)
 void launch_ref_pairs(int mode, const double* t, int m, const int2* pairs, const int* count, int cap,
                       double r_sq, uint8_t* alive, unsigned long long* nnkey, TryCtl* ctl, const int* ex,
-                      double* nnout, cudaStream_t st);
+                      double* nnout, const Peers& peers, cudaStream_t st);
 void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const unsigned* ymax,
                       const unsigned* emax, const float* nrm, const int* crange, int N, int m, int need,
                       double* lo, double* hi, int* cand, float* ythr, unsigned long long* nnkey, int2* groups,
@@ -52,7 +52,7 @@ void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const 
 // (degenerate row, any q) pair by the exact distance — kills and exact-nn keys
 void launch_degenerate_pairs(const double* t, int m, int N, const int* list, const TryCtl* ctl, const int* crange,
                              const int* deg, double r_sq, uint8_t* alive, unsigned long long* nnkey, int rank,
-                             int world, cudaStream_t st);
+                             int world, const Peers& peers, cudaStream_t st);
 void launch_try_init(uint8_t* alive, unsigned* ymax, unsigned* emax, float* ythr, unsigned long long* nnkey, int N,
                      TryCtl* ctl, unsigned long long* acc, int band_k0, cudaStream_t st);
 int compact_blocks(int n);

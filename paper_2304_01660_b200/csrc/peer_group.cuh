@@ -10,6 +10,7 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <condition_variable>
 #include <mutex>
 #include <stdexcept>
@@ -40,7 +41,13 @@ public:
             cv_.notify_all();
             return;
         }
-        cv_.wait(lk, [&] { return gen != gen_ || broken_; });
+        // a rank that never arrives (diverged control flow) must fail the call,
+        // not hang it
+        if (!cv_.wait_for(lk, std::chrono::seconds(120), [&] { return gen != gen_ || broken_; })) {
+            broken_ = true;
+            cv_.notify_all();
+            throw std::runtime_error("peer group: barrier timeout");
+        }
         if (broken_) throw std::runtime_error("peer group: another rank failed");
     }
     void fail() {
@@ -66,8 +73,95 @@ struct PeerGroup {
     int n = 0;
     HostBarrier bar;
     std::vector<const void*> ptrs;
+    std::vector<void*> p_alive, p_ymax, p_emax, p_nnkey;  // fused transport: every rank's arrays
     std::vector<cudaEvent_t> ev_in, ev_red;
-    explicit PeerGroup(int ranks) : n(ranks), bar(ranks), ptrs(ranks), ev_in(ranks), ev_red(ranks) {}
+    explicit PeerGroup(int ranks)
+        : n(ranks), bar(ranks), ptrs(ranks), p_alive(ranks), p_ymax(ranks), p_emax(ranks), p_nnkey(ranks), ev_in(ranks),
+          ev_red(ranks) {}
+};
+
+}  // namespace tsd
+
+// ---------------------------------------------------------------------------
+// Cross-process ranks (one process per GPU, e.g. under torchrun): the same
+// fused peer stores, with the arrays shared through CUDA IPC memory handles,
+// the per-rank barrier events through CUDA IPC event handles, and the host
+// barrier in a POSIX shared-memory segment of the node.
+#include <fcntl.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <unistd.h>
+
+#include <atomic>
+#include <chrono>
+#include <string>
+
+namespace tsd {
+
+struct ShmBarrierState {
+    std::atomic<int> count;
+    std::atomic<int> gen;
+    std::atomic<int> broken;
+};
+
+class ShmBarrier {
+public:
+    ShmBarrier(const std::string& name, int world, bool create) : name_(name), n_(world) {
+        const int fd = shm_open(name.c_str(), O_RDWR | (create ? O_CREAT : 0), 0600);
+        if (fd < 0) throw std::runtime_error("shm_open " + name + " failed");
+        if (create && ftruncate(fd, sizeof(ShmBarrierState)) != 0) {
+            close(fd);
+            throw std::runtime_error("ftruncate " + name + " failed");
+        }
+        void* p = mmap(nullptr, sizeof(ShmBarrierState), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+        close(fd);
+        if (p == MAP_FAILED) throw std::runtime_error("mmap " + name + " failed");
+        st_ = static_cast<ShmBarrierState*>(p);
+        if (create) {
+            st_->count.store(0);
+            st_->gen.store(0);
+            st_->broken.store(0);
+        }
+        owner_ = create;
+    }
+    ~ShmBarrier() {
+        munmap(st_, sizeof(ShmBarrierState));
+        if (owner_) shm_unlink(name_.c_str());
+    }
+    void wait() {
+        static const double timeout_s = std::getenv("TSD_BARRIER_TIMEOUT") ? std::atof(std::getenv("TSD_BARRIER_TIMEOUT"))
+                                                                          : 120.0;
+        ++waits_;
+        if (std::getenv("TSD_DEBUG_BARRIER")) fprintf(stderr, "[ipc] pid %d barrier #%ld\n", (int)getpid(), waits_);
+        if (st_->broken.load()) throw std::runtime_error("ipc group: another rank failed");
+        const int g = st_->gen.load(std::memory_order_acquire);
+        if (st_->count.fetch_add(1) + 1 == n_) {
+            st_->count.store(0);
+            st_->gen.fetch_add(1, std::memory_order_release);
+            return;
+        }
+        const auto t0 = std::chrono::steady_clock::now();
+        for (unsigned spin = 0; st_->gen.load(std::memory_order_acquire) == g; ++spin) {
+            if (st_->broken.load()) throw std::runtime_error("ipc group: another rank failed");
+            if ((spin & 1023u) == 1023u) {
+                sched_yield();
+                if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s) {
+                    st_->broken.store(1);
+                    throw std::runtime_error("ipc group: barrier timeout");
+                }
+            }
+        }
+    }
+    void fail() { st_->broken.store(1); }
+
+private:
+    std::string name_;
+    int n_;
+    long waits_ = 0;
+    ShmBarrierState* st_ = nullptr;
+    bool owner_ = false;
 };
 
 }  // namespace tsd

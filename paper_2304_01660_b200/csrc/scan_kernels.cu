@@ -202,7 +202,8 @@ struct F9 {
 // unrolled walk.
 __device__ __noinline__ void slow_track(const F9 x, const F9 qn, float tz, float cw, int c, int u0, int dir,
                                         int qbase, int N, int m, double r_sq, double thr0, double E,
-                                        uint8_t* alive, int2* queue, int* queue_count, int queue_cap) {
+                                        uint8_t* alive, uint8_t* const* peer_alive, int npeer, int2* queue,
+                                        int* queue_count, int queue_cap) {
 #pragma unroll
     for (int j = 0; j < kDiag; ++j) {
         if (!(x.v[j] > tz)) continue;
@@ -212,13 +213,17 @@ __device__ __noinline__ void slow_track(const F9 x, const F9 qn, float tz, float
         const float qj = qn.v[j];
         if (cw == 0.f || qj == 0.f) {
             const double d = (cw == 0.f && qj == 0.f) ? 0.0 : 2.0 * (double)m;
-            if (d < r_sq) alive[c] = 0;
+            if (d < r_sq) {
+                if (npeer > 1) for (int r = 0; r < npeer; ++r) peer_alive[r][c] = 0;
+                else alive[c] = 0;
+            }
             continue;
         }
         const double corr = (double)x.v[j] * (double)cw;
         const double ec = E * (double)cw * (double)qj + kSlack;
         if (corr - ec > thr0) {
-            alive[c] = 0;
+            if (npeer > 1) for (int r = 0; r < npeer; ++r) peer_alive[r][c] = 0;
+            else alive[c] = 0;
         } else if (corr + ec >= thr0) {
             const int at = atomicAdd(queue_count, 1);
             if (at < queue_cap) queue[at] = make_int2(c, q);
@@ -232,6 +237,8 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
     // static shared memory (33 KB): CTA-relative LDS addressing, no shared
     // window base to rematerialise inside the walk
     __shared__ ScanSmem<MODE> S;
+    __shared__ uint8_t* s_peer_alive[kMaxPeers];  // slow path: peer pointers without a param copy
+    if (threadIdx.x < kMaxPeers) s_peer_alive[threadIdx.x] = p.peers.alive[threadIdx.x];
     const int tid = threadIdx.x;
     const long long slots = tile_slots(p);
     // persistent CTAs: slots are fetched dynamically; rank r owns slots r, r+world, ...
@@ -571,7 +578,8 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
                             qv.v[j] = rn[(j + uu) % kDiag];
                         }
                         slow_track(xv, qv, cr.z, cr.w, dir > 0 ? td.r0 + ss : r_end - ss, ss + ub, dir, qbase, N,
-                                   m, p.r_sq, p.thr0, E, p.alive, p.queue, p.queue_count, p.queue_cap);
+                                   m, p.r_sq, p.thr0, E, p.alive, s_peer_alive, p.peers.n, p.queue,
+                                   p.queue_count, p.queue_cap);
                     }
                     if (S.ykey[ss] != 0u) {
                         // row max of the FP32 route value x = cov*qn over valid q (NaN for
@@ -607,7 +615,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
                 const int uu = __ffs(hit) - 1;
                 hit &= hit - 1;
                 const int ss = s0 + uu;
-                p.alive[dir > 0 ? td.r0 + ss : r_end - ss] = 0;
+                peer_kill(p.peers, p.alive, dir > 0 ? td.r0 + ss : r_end - ss);
             } while (hit);
         }
     }
@@ -619,8 +627,15 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
             const unsigned k = S.ykey[s];
             if (k > 1u) {
                 const int c = dir > 0 ? td.r0 + s : r_end - s;
-                atomicMax(&p.ymax[c], k);
-                atomicMax(&p.emax[c], ekey);
+                if (p.peers.n > 1) {
+                    for (int r = 0; r < p.peers.n; ++r) {
+                        atomicMax(&p.peers.ymax[r][c], k);
+                        atomicMax(&p.peers.emax[r][c], ekey);
+                    }
+                } else {
+                    atomicMax(&p.ymax[c], k);
+                    atomicMax(&p.emax[c], ekey);
+                }
             }
         }
     }
@@ -700,7 +715,7 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_ref_pairs(const double* __r
                                                                uint8_t* alive,
                                                                unsigned long long* nnkey,
                                                                TryCtl* ctl, const int* __restrict__ ex,
-                                                               double* __restrict__ nnout) {
+                                                               double* __restrict__ nnout, const Peers peers) {
     pdl_enter();
     __shared__ double buf[kPairWarps][256];
     const int w = threadIdx.x >> 5;
@@ -712,11 +727,11 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_ref_pairs(const double* __r
         if ((threadIdx.x & 31) == 0) {
             if (MODE == 0) {
                 if (d < r_sq) {
-                    alive[pr.x] = 0;
-                    alive[pr.y] = 0;
+                    peer_kill(peers, alive, pr.x);
+                    peer_kill(peers, alive, pr.y);
                 }
             } else {
-                atomicMin(&nnkey[pr.x], (unsigned long long)__double_as_longlong(d));
+                peer_min_key(peers, nnkey, pr.x, (unsigned long long)__double_as_longlong(d));
             }
         }
     }
@@ -750,7 +765,7 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_degenerate_pairs(const doub
                                                                       const int* __restrict__ deg, double r_sq,
                                                                       uint8_t* alive,
                                                                       unsigned long long* nnkey, int rank,
-                                                                      int world) {
+                                                                      int world, const Peers peers) {
     pdl_enter();
     __shared__ double buf[kPairWarps][256];
     const int D = cr[2];
@@ -773,8 +788,8 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_degenerate_pairs(const doub
         if (abs(c - q) < m) continue;
         const double d = ref_dist_warp(t, m, c, q, buf[w]);
         if ((threadIdx.x & 31) == 0) {
-            if (d < r_sq) alive[c] = 0;
-            atomicMin(&nnkey[c], (unsigned long long)__double_as_longlong(d));
+            if (d < r_sq) peer_kill(peers, alive, c);
+            peer_min_key(peers, nnkey, c, (unsigned long long)__double_as_longlong(d));
         }
     }
 }
@@ -1581,21 +1596,21 @@ void launch_scan(int mode, const ScanParams& p, cudaStream_t st) {
 
 void launch_ref_pairs(int mode, const double* t, int m, const int2* pairs, const int* count, int cap,
                       double r_sq, uint8_t* alive, unsigned long long* nnkey, TryCtl* ctl, const int* ex,
-                      double* nnout, cudaStream_t st) {
+                      double* nnout, const Peers& peers, cudaStream_t st) {
     const int blocks = 148 * 4;  // grid-stride over the device-side pair count
     if (mode == 0)
         launch_pdl(k_ref_pairs<0>, blocks, kPairWarps * 32, st, t, m, pairs, count, cap, r_sq, alive, nnkey, ctl,
-                                                             nullptr, nullptr);
+                   (const int*)nullptr, (double*)nullptr, peers);
     else
         launch_pdl(k_ref_pairs<1>, blocks, kPairWarps * 32, st, t, m, pairs, count, cap, r_sq, alive, nnkey, ctl, ex,
-                                                             nnout);
+                   nnout, peers);
 }
 
 void launch_degenerate_pairs(const double* t, int m, int N, const int* list, const TryCtl* ctl, const int* crange,
                              const int* deg, double r_sq, uint8_t* alive, unsigned long long* nnkey, int rank,
-                             int world, cudaStream_t st) {
+                             int world, const Peers& peers, cudaStream_t st) {
     launch_pdl(k_degenerate_pairs, 148 * 4, kPairWarps * 32, st, t, m, N, list, ctl, crange, deg, r_sq, alive,
-               nnkey, rank, world);
+               nnkey, rank, world, peers);
 }
 
 void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const unsigned* ymax,

@@ -184,12 +184,14 @@ def test_merlin_constant_series_fails_lengths(engine):
 
 
 # ---- sharded path (segment-sharded tiles + reductions) on one device -----------
-@pytest.mark.parametrize("ranks", [2, 3])
-def test_group_sharded_merlin_equals_single(engine, ranks):
-    # ranks contexts on cuda:0: tiles dealt cyclically, kill flags / route maxima /
-    # exact-nn keys all-reduced through peer memory -> identical records
+@pytest.mark.parametrize("ranks,fused", [(2, 1), (3, 1), (2, 0)])
+def test_group_sharded_merlin_equals_single(engine, ranks, fused):
+    # ranks contexts on cuda:0: tiles dealt cyclically; kills and route maxima go
+    # to every rank's arrays from inside the kernels (fused) or through peer
+    # all-reduce kernels; exact-nn keys all-reduced -> identical records
     import paper_2304_01660_b200 as P
     g = P.Group([0] * ranks)
+    g.set_param("fused_peers", fused)
     for fx in (load_golden("c1.json"), load_golden("small.json")["merlin"][1]):
         x = series_of(fx["input"])
         g.set_series(x)
