@@ -147,6 +147,7 @@ struct tsd_ctx {
     int seed32_track = 1;    // FP32 seeds in the full-row launch (wider error band, half the seed cost; C4 -3.4%)
     int seed32_collect = 1;  // ... and in the collection launch
     float band_keep = 0.85f;  // band loop stops when a pass leaves more than this fraction alive
+    float seed_w = 0.25f;  // grouping cost: one group-diagonal seed = seed_w*m walked row-diagonals (FP32 seeds)
     int band_few = 256;       // ... or when at most max(band_few, N/4096) rows are left (C2: 64 -> 41.8 ms, 256 -> 41.2 ms)
     int result_prefix = 1024;  // records copied back with the try's single round trip
     double err_k = 4.0;
@@ -468,7 +469,7 @@ struct tsd_ctx {
         }
         slots.ensure(group_slots(N));
         launch_compact_group(alive.p, N, list.p, lbstat.p, epoch, ctl.p, gate, groups.p, slots.p, (int)m,
-                             sparse_rows, band_keep, band_few, st);
+                             sparse_rows, band_keep, band_few, seed_w, st);
         ck(cudaGetLastError(), "compact");
         ctr.kernel_launches += 1;
         // fused peers: no rank's next scan may store kills into this rank's
@@ -650,7 +651,7 @@ struct tsd_ctx {
         // CTA filters the list to the survivors, applies the MERLIN top-k
         // filter, resets their keys and groups them.
         launch_survivors(list.p, alive.p, C, ymax.p, emax.p, nrm.p, cr_cur, N, (int)m, (int)need_top, bnd_lo.p,
-                         bnd_hi.p, cand.p, ythr.p, nnkey.p, groups.p, sparse_rows, st);
+                         bnd_hi.p, cand.p, ythr.p, nnkey.p, groups.p, sparse_rows, seed_w, st);
         ck(cudaGetLastError(), "survivors");
         const int* ex = cand.p;  // rows whose exact nn is computed (count: C->ec)
         q.space = kSpaceFull;  // every diagonal of the exact-nn rows' groups
@@ -1525,6 +1526,7 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "band0_sides") c->band0_sides = v <= 1.0 ? 1 : 2;
         else if (k == "track_chunks") c->track_chunks = std::max(1, std::min(16, (int)v));
         else if (k == "band_few") c->band_few = std::max(0, (int)v);
+        else if (k == "seed_w") c->seed_w = (float)std::max(0.01, v);
         else if (k == "band_keep") c->band_keep = (float)std::max(0.0, std::min(1.0, v));
         else if (k == "band_passes") c->band_passes = std::max(1, std::min(64, (int)v));
         else if (k == "result_prefix") c->result_prefix = std::max(16, std::min(1 << 20, (int)v));

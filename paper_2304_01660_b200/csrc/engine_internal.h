@@ -47,7 +47,7 @@ void launch_ref_pairs(int mode, const double* t, int m, const int2* pairs, const
 void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const unsigned* ymax,
                       const unsigned* emax, const float* nrm, const int* crange, int N, int m, int need,
                       double* lo, double* hi, int* cand, float* ythr, unsigned long long* nnkey, int2* groups,
-                      int fixed_span, cudaStream_t st);
+                      int fixed_span, float seed_w, cudaStream_t st);
 // degenerate rows (sigma < eps): every (alive row, degenerate row) and
 // (degenerate row, any q) pair by the exact distance — kills and exact-nn keys
 void launch_degenerate_pairs(const double* t, int m, int N, const int* list, const TryCtl* ctl, const int* crange,
@@ -61,7 +61,7 @@ int compact_blocks(int n);
 // words; slots: group_slots(n) entries)
 void launch_compact_group(const uint8_t* a, int n, int* out, unsigned long long* status, unsigned epoch,
                           TryCtl* ctl, int gate, int2* groups, int2* slots, int m, int fixed_span, float band_keep,
-                          int band_few, cudaStream_t st);
+                          int band_few, float seed_w, cudaStream_t st);
 int group_slots(int n);
 int scan_slots_prune();  // persistent grid of the band-pass scan (SMs x resident CTAs)
 // tracked full-row chunks: schedule of the first chunk (after the band passes)

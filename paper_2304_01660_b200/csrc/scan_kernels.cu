@@ -900,7 +900,7 @@ __device__ __forceinline__ void walk_segment(const int* __restrict__ list, int c
 constexpr int kGroupStage = 8192;  // list entries staged in smem (32 KB)
 // whole-CTA (1024 threads) body; every thread must call it
 __device__ void group_body(const int* __restrict__ list_g, const int cnt, int2* __restrict__ groups, TryCtl* ctl,
-                           int m, int fixed_span) {
+                           int m, int fixed_span, float seed_w) {
     __shared__ double costs[32][kSpans];
     __shared__ int wsum[32];
     __shared__ int s_span;
@@ -961,7 +961,7 @@ __device__ void group_body(const int* __restrict__ list_g, const int cnt, int2* 
                 if (gap < span) continue;
                 double acc = 0.0;
                 walk_segment(list, cnt, e, span, [&](int i0, int i1) {
-                    acc += 2.0 * m + 3.0 * (double)(list[i1] - list[i0] + 1 + kDiag);
+                    acc += seed_w * m + (double)(list[i1] - list[i0] + 1 + kDiag);
                 });
                 c[k] += acc;
             }
@@ -1083,7 +1083,8 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
                                                         unsigned long long* status, unsigned epoch, TryCtl* ctl,
                                                         int gate, int2* __restrict__ groups,
                                                         int2* __restrict__ slots, int m, int fixed_span,
-                                                        float band_keep, int scan_slots, int band_few) {
+                                                        float band_keep, int scan_slots, int band_few,
+                                                        float seed_w) {
     pdl_enter();
     if (gated_off(ctl, gate)) return;
     __shared__ int s_bid, s_excl, s_last, s_k;
@@ -1120,7 +1121,7 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
     }
     // ---- span-blocks: spans 16..128 within a warp, 256 / 512 across warps
     {
-        const double cm = 2.0 * (double)m + 3.0 * (double)(1 + kDiag);
+        const double cm = (double)seed_w * (double)m + (double)(1 + kDiag);
         int mn = fa, mx = la;
         mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, 1));
         mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
@@ -1134,7 +1135,7 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
             if ((lane & ((4 << k) - 1)) == 0) {
                 const int j = threadIdx.x >> (2 + k);
                 slots[slot_region(k, nb) + (long long)bid * (256 >> k) + j] = make_int2(mn, mx);
-                if (mx >= 0) cst[k] = cm + 3.0 * (double)(mx - mn);
+                if (mx >= 0) cst[k] = cm + (double)(mx - mn);
             }
         }
         if (lane == 0) {
@@ -1147,13 +1148,13 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
             const int j = threadIdx.x;
             const int x = min(s_fa[2 * j], s_fa[2 * j + 1]), y = max(s_la[2 * j], s_la[2 * j + 1]);
             slots[slot_region(4, nb) + (long long)bid * 16 + j] = make_int2(x, y);
-            if (y >= 0) cst[4] = cm + 3.0 * (double)(y - x);
+            if (y >= 0) cst[4] = cm + (double)(y - x);
         } else if (threadIdx.x >= 32 && threadIdx.x < 40) {  // span 512: 4 warps each
             const int j = threadIdx.x - 32;
             const int x = min(min(s_fa[4 * j], s_fa[4 * j + 1]), min(s_fa[4 * j + 2], s_fa[4 * j + 3]));
             const int y = max(max(s_la[4 * j], s_la[4 * j + 1]), max(s_la[4 * j + 2], s_la[4 * j + 3]));
             slots[slot_region(5, nb) + (long long)bid * 8 + j] = make_int2(x, y);
-            if (y >= 0) cst[5] = cm + 3.0 * (double)(y - x);
+            if (y >= 0) cst[5] = cm + (double)(y - x);
         }
 #pragma unroll
         for (int k = 0; k < kSpans; ++k) {
@@ -1383,7 +1384,7 @@ __global__ void __launch_bounds__(1024) k_survivors(const int* __restrict__ list
                                                     int N, int m, int need, double* __restrict__ lo,
                                                     double* __restrict__ hi, int* __restrict__ cand,
                                                     float* __restrict__ ythr, unsigned long long* __restrict__ nnkey,
-                                                    int2* __restrict__ groups, int fixed_span) {
+                                                    int2* __restrict__ groups, int fixed_span, float seed_w) {
     pdl_enter();
     __shared__ int wsum[32];
     __shared__ int hist[256];
@@ -1497,7 +1498,7 @@ __global__ void __launch_bounds__(1024) k_survivors(const int* __restrict__ list
         ctl->ec = ec;
     }
     // 4. groups of the rows that get exact distances
-    group_body(cand, ec, groups, ctl, m, fixed_span);
+    group_body(cand, ec, groups, ctl, m, fixed_span, seed_w);
 }
 
 __global__ void k_gather_nn(const int* __restrict__ list, const int* __restrict__ cnt_p,
@@ -1616,9 +1617,9 @@ void launch_degenerate_pairs(const double* t, int m, int N, const int* list, con
 void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const unsigned* ymax,
                       const unsigned* emax, const float* nrm, const int* crange, int N, int m, int need,
                       double* lo, double* hi, int* cand, float* ythr, unsigned long long* nnkey, int2* groups,
-                      int fixed_span, cudaStream_t st) {
+                      int fixed_span, float seed_w, cudaStream_t st) {
     launch_pdl(k_survivors, 1, 1024, st, list, alive, ctl, ymax, emax, nrm, crange, N, m, need, lo, hi, cand, ythr,
-                                    nnkey, groups, fixed_span);
+               nnkey, groups, fixed_span, seed_w);
 }
 
 void launch_try_init(uint8_t* alive, unsigned* ymax, unsigned* emax, float* ythr, unsigned long long* nnkey, int N,
@@ -1636,12 +1637,12 @@ void launch_track_init(TryCtl* ctl, int N, int m, bool bands_ran, cudaStream_t s
 
 void launch_compact_group(const uint8_t* a, int n, int* out, unsigned long long* status, unsigned epoch,
                           TryCtl* ctl, int gate, int2* groups, int2* slots, int m, int fixed_span, float band_keep,
-                          int band_few, cudaStream_t st) {
+                          int band_few, float seed_w, cudaStream_t st) {
     launch_pdl(k_compact_group, compact_blocks(n), kCompactBlock, st, a, n, out, status, epoch, ctl, gate, groups, slots,
                                                                m, fixed_span, band_keep,
                                                                gate == kGateTrack ? scan_grid<kPruneTrack>()
                                                                                   : scan_slots_prune(),
-                                                               band_few);
+                                                               band_few, seed_w);
 }
 
 int group_slots(int n) { return compact_blocks(n) * 504; }
