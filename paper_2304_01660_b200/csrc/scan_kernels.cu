@@ -62,7 +62,7 @@ struct __align__(16) ScanSmem {
             float win[kW + kSeedChunk];
         } seed32;
     } u;
-    float red[3][kThreads / 32];
+    float red[7][kThreads / 32];
     int flag;
 };
 
@@ -418,6 +418,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
     // largest sigma of each side comes from the smallest non-zero norm,
     // sigma = 1/(sqrt(m) nrm) up to the FP32 rounding of nrm (factor below).
     float cn_min = FLT_MAX, qn_min = FLT_MAX, qn_max = 0.f;
+    float dc = 0.f, gc = 0.f, dq = 0.f, gq = 0.f;  // max |df|, |dg| walked on each side
 #pragma unroll 4
     for (int s = tid; s < rows; s += kThreads) {
         const int c = dir > 0 ? td.r0 + s : r_end - s;
@@ -429,6 +430,8 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
         v.w = p.nrm[c];
         v.z = 0.f;
         if (v.w != 0.f) cn_min = fminf(cn_min, v.w);
+        dc = fmaxf(dc, fabsf(v.x));
+        gc = fmaxf(gc, fabsf(v.y));
         S.crow[s] = v;
     }
     const int rows_p = (rows + kDiag - 1) / kDiag * kDiag;
@@ -449,6 +452,8 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
             qn_min = fminf(qn_min, nn);
             qn_max = fmaxf(qn_max, nn);
         }
+        dq = fmaxf(dq, fabsf(a));
+        gq = fmaxf(gq, fabsf(b));
         S.u.walk.qd[u] = make_float2(a, b);
         // an invalid q gets a NaN norm: its x = cov*qn is NaN, which never passes a
         // threshold test and is ignored by fmaxf (a constant q keeps qn = 0, x = 0)
@@ -459,10 +464,18 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
     cn_min = -warp_max(-cn_min);
     qn_min = -warp_max(-qn_min);
     qn_max = warp_max(qn_max);
+    dc = warp_max(dc);
+    gc = warp_max(gc);
+    dq = warp_max(dq);
+    gq = warp_max(gq);
     if ((tid & 31) == 0) {
         S.red[0][tid >> 5] = cn_min;
         S.red[1][tid >> 5] = qn_min;
         S.red[2][tid >> 5] = qn_max;
+        S.red[3][tid >> 5] = dc;
+        S.red[4][tid >> 5] = gc;
+        S.red[5][tid >> 5] = dq;
+        S.red[6][tid >> 5] = gq;
     }
     __syncthreads();
     cn_min = FLT_MAX;
@@ -473,12 +486,25 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
         cn_min = fminf(cn_min, S.red[0][w]);
         qn_min = fminf(qn_min, S.red[1][w]);
         qn_max = fmaxf(qn_max, S.red[2][w]);
+        dc = fmaxf(dc, S.red[3][w]);
+        gc = fmaxf(gc, S.red[4][w]);
+        dq = fmaxf(dq, S.red[5][w]);
+        gq = fmaxf(gq, S.red[6][w]);
     }
     const double inv_sqm = 1.0 / sqrt((double)m);
     const double smax_c = cn_min < FLT_MAX ? inv_sqm / (double)cn_min * (1.0 + 1e-6) : 0.0;
     const double smax_q = qn_min < FLT_MAX ? inv_sqm / (double)qn_min * (1.0 + 1e-6) : 0.0;
-    // absolute FP32 covariance error bound for every cell of this tile
-    const double E = p.err_k * (double)kEps32 * (double)m * smax_c * smax_q * (double)(rows + 8) + e_seed;
+    // Absolute FP32 covariance error bound for every cell of this tile.  One
+    // walk step is two FFMA on FP32-rounded operands: rounding <= u(|a| + |b|)
+    // with |a|, |b| <= m smax_c smax_q (Cauchy-Schwarz) + the increment, and the
+    // operands' own rounding <= 2u per product, so one step errs by at most
+    // u (2 m smax_c smax_q + 3 P), P = max|df_c||dg_q| + max|df_q||dg_c| over the
+    // walked rows and q.  err_k = 4 doubles that first-order bound (margin for
+    // second-order terms and the FP64 statistics' rounding) over rows + 8 steps;
+    // e_seed bounds the seed (0 for FP64 / resident seeds).
+    const double P = (double)dc * (double)gq + (double)dq * (double)gc;
+    const double E =
+        p.err_k * (double)kEps32 * (double)(rows + 8) * ((double)m * smax_c * smax_q + 1.5 * P) + e_seed;
     const float Ef = (float)E;
     // Row thresholds.  crow.z = tc: a live row's cells with x = cov*qn > tc may be
     // within the error band of d^2 = r^2 (slow path); kNoEval marks rows whose
