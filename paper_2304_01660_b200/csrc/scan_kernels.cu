@@ -231,7 +231,7 @@ __device__ __noinline__ void slow_track(const F9 x, const F9 qn, float tz, float
     }
 }
 
-template <int MODE>
+template <int MODE, int STRIDE = 1>
 __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(const ScanParams p) {
     pdl_enter();
     // static shared memory (33 KB): CTA-relative LDS addressing, no shared
@@ -581,10 +581,22 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
                 // tc = kNoEval (never exceeded), and the kill stores wait for the
                 // end of the 9-step block.  The max is a depth-2 FMNMX3 tree.
                 float x[kDiag];
+                float mx;
+                if (STRIDE > 1) {
+                    // reduced-density evaluation: cell (step, j) only when
+                    // (j + step) % STRIDE == 0, so each row tests 1/STRIDE of its
+                    // band.  Kills stay certain; a row missed here is walked again
+                    // by the next pass.  The walk (2 FFMA per cell) is unchanged.
+                    mx = -FLT_MAX;
 #pragma unroll
-                for (int j = 0; j < kDiag; ++j) x[j] = cov[j] * rn[(j + uu) % kDiag];
-                const float mx = fmaxf(fmaxf(fmaxf(fmaxf(x[0], x[1]), x[2]), fmaxf(fmaxf(x[3], x[4]), x[5])),
-                                       fmaxf(fmaxf(x[6], x[7]), x[8]));
+                    for (int j = 0; j < kDiag; ++j)
+                        if ((j + uu) % STRIDE == 0) mx = fmaxf(mx, cov[j] * rn[(j + uu) % kDiag]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < kDiag; ++j) x[j] = cov[j] * rn[(j + uu) % kDiag];
+                    mx = fmaxf(fmaxf(fmaxf(fmaxf(x[0], x[1]), x[2]), fmaxf(fmaxf(x[3], x[4]), x[5])),
+                               fmaxf(fmaxf(x[6], x[7]), x[8]));
+                }
                 hit |= (mx > cr.z ? 1u : 0u) << uu;
             } else if (cr.z != kNoEval) {  // CTA-uniform branch: the row is undecided
                 float x[kDiag];
@@ -667,7 +679,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
     }
     if (tid == 0) {
         atomicAdd(&p.acc[0], (unsigned long long)rows * (unsigned long long)kW);
-        atomicAdd(&p.acc[1], (unsigned long long)evals * (unsigned long long)kW);
+        atomicAdd(&p.acc[1], (unsigned long long)evals * (unsigned long long)(kW / STRIDE));
         if (td.seed < 0) atomicAdd(&p.acc[2], (unsigned long long)kW);
     }
     }  // persistent tile loop
@@ -1615,7 +1627,11 @@ static int scan_grid() {
 
 void launch_scan(int mode, const ScanParams& p, cudaStream_t st) {
     switch (mode) {
-        case kPrune: launch_pdl(k_scan<kPrune>, scan_grid<kPrune>(), kThreads, st, p); break;
+        case kPrune:
+            if (p.half == 2) launch_pdl(k_scan<kPrune, 2>, scan_grid<kPrune>(), kThreads, st, p);
+            else if (p.half >= 3) launch_pdl(k_scan<kPrune, 3>, scan_grid<kPrune>(), kThreads, st, p);
+            else launch_pdl(k_scan<kPrune>, scan_grid<kPrune>(), kThreads, st, p);
+            break;
         case kPruneTrack: launch_pdl(k_scan<kPruneTrack>, scan_grid<kPruneTrack>(), kThreads, st, p); break;
         default: launch_pdl(k_scan<kCollect>, scan_grid<kCollect>(), kThreads, st, p); break;
     }
