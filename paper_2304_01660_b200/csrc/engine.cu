@@ -127,6 +127,7 @@ struct tsd_ctx {
     DBuf<int> blk, list;
     DBuf<double> nnout;
     DBuf<int2> groups, slots;  // groups of the current stage; per-span candidate groups
+    DBuf<double> bcost;        // per-CTA span costs of a compaction
     DBuf<TryCtl> ctl;  // device-resident control block of the current try
     DBuf<unsigned long long> lbstat;  // compaction look-back status words
     unsigned epoch = 0;
@@ -472,8 +473,9 @@ struct tsd_ctx {
             epoch = 1;
         }
         slots.ensure(group_slots(N));
+        bcost.ensure((size_t)compact_blocks(N) * 6);
         launch_compact_group(alive.p, N, list.p, lbstat.p, epoch, ctl.p, gate, groups.p, slots.p, (int)m,
-                             sparse_rows, band_keep, band_few, seed_w, st);
+                             sparse_rows, band_keep, band_few, seed_w, bcost.p, st);
         ck(cudaGetLastError(), "compact");
         ctr.kernel_launches += 1;
         // fused peers: no rank's next scan may store kills into this rank's
@@ -888,6 +890,7 @@ void tsd_ctx_destroy(tsd_ctx* c) {
     c->nnout.release();
     c->groups.release();
     c->slots.release();
+    c->bcost.release();
     c->hm.release();
     c->hm_cols.release();
     c->hm_cnt.release();

@@ -1122,7 +1122,7 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
                                                         int gate, int2* __restrict__ groups,
                                                         int2* __restrict__ slots, int m, int fixed_span,
                                                         float band_keep, int scan_slots, int band_few,
-                                                        float seed_w) {
+                                                        float seed_w, double* __restrict__ bcost) {
     pdl_enter();
     if (gated_off(ctl, gate)) return;
     __shared__ int s_bid, s_excl, s_last, s_k;
@@ -1202,10 +1202,10 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
             if (lane == 0) s_cost[w][k] = v;
         }
         __syncthreads();
-        if (threadIdx.x < kSpans) {
+        if (threadIdx.x < kSpans) {  // per-CTA partials: no atomic contention on 6 words
             double v = 0.0;
             for (int x = 0; x < 32; ++x) v += s_cost[x][threadIdx.x];
-            if (v != 0.0) atomicAdd(&ctl->cost[threadIdx.x], v);
+            bcost[bid * kSpans + threadIdx.x] = v;
         }
     }
     // ---- compaction (decoupled look-back)
@@ -1271,6 +1271,28 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
     if (!s_last) return;
     __threadfence();
     const int total = *(volatile int*)&ctl->ctotal;
+    {  // span costs: sum of the per-CTA partials
+        double c6[kSpans];
+#pragma unroll
+        for (int k = 0; k < kSpans; ++k) c6[k] = 0.0;
+        for (int b = threadIdx.x; b < nb; b += blockDim.x)
+#pragma unroll
+            for (int k = 0; k < kSpans; ++k) c6[k] += __ldcg(&bcost[b * kSpans + k]);
+#pragma unroll
+        for (int k = 0; k < kSpans; ++k) {
+            double v = c6[k];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) s_cost[w][k] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < kSpans) {
+            double v = 0.0;
+            for (int x = 0; x < 32; ++x) v += s_cost[x][threadIdx.x];
+            s_cost[0][threadIdx.x] = v;  // row 0 read by thread 0 below (after its own partial)
+        }
+        __syncthreads();
+    }
     if (threadIdx.x == 0) {
         ctl->cticket = 0;
         ctl->cdone = 0;
@@ -1297,14 +1319,13 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
                                  (long long)total * 64 < (long long)(__ldcg(&out[total - 1]) - __ldcg(&out[0]) + 1))) {
             double best = 1e300;
             for (int x = 0; x < kSpans; ++x) {
-                const double v = *(volatile double*)&ctl->cost[x];
+                const double v = s_cost[0][x];
                 if (v < best) {
                     best = v;
                     k = x;
                 }
             }
         }
-        for (int x = 0; x < kSpans; ++x) ctl->cost[x] = 0.0;
         s_k = k;
         ctl->span = 16 << k;
     }
@@ -1679,12 +1700,12 @@ void launch_track_init(TryCtl* ctl, int N, int m, bool bands_ran, cudaStream_t s
 
 void launch_compact_group(const uint8_t* a, int n, int* out, unsigned long long* status, unsigned epoch,
                           TryCtl* ctl, int gate, int2* groups, int2* slots, int m, int fixed_span, float band_keep,
-                          int band_few, float seed_w, cudaStream_t st) {
+                          int band_few, float seed_w, double* bcost, cudaStream_t st) {
     launch_pdl(k_compact_group, compact_blocks(n), kCompactBlock, st, a, n, out, status, epoch, ctl, gate, groups, slots,
                                                                m, fixed_span, band_keep,
                                                                gate == kGateTrack ? scan_grid<kPruneTrack>()
                                                                                   : scan_slots_prune(),
-                                                               band_few, seed_w);
+                                                               band_few, seed_w, bcost);
 }
 
 int group_slots(int n) { return compact_blocks(n) * 504; }
