@@ -149,6 +149,7 @@ struct tsd_ctx {
     // misses is walked again later).  Measured: C2 41.0 -> 39.5 ms, C4 1060 ->
     // 1013 ms with 1/3 in pass 0 and 1/2 in the later band passes.
     int half_pass0 = 3, half_bands = 2;
+    long long half_bands_m = 256;  // later passes use half_bands only from this length on
     int seed32_track = 1;    // FP32 seeds in the full-row launch (wider error band, half the seed cost; C4 -3.4%)
     int seed32_collect = 1;  // ... and in the collection launch
     float band_keep = 0.85f;  // band loop stops when a pass leaves more than this fraction alive
@@ -603,7 +604,7 @@ struct tsd_ctx {
                 } else {
                     q.space = kSpaceBand;  // groups and bands set by the previous compaction
                 }
-                q.half = (pass == 0 ? half_pass0 : half_bands);
+                q.half = pass == 0 ? half_pass0 : (m >= half_bands_m ? half_bands : 1);
                 scan(kPrune, q);
                 reduce_alive(N);
                 compact(N, pass, m);
@@ -1536,6 +1537,7 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "band_few") c->band_few = std::max(0, (int)v);
         else if (k == "half_pass0") c->half_pass0 = std::max(1, std::min(3, (int)v));
         else if (k == "half_bands") c->half_bands = std::max(1, std::min(3, (int)v));
+        else if (k == "half_bands_m") c->half_bands_m = (long long)v;
         else if (k == "seed_w") c->seed_w = (float)std::max(0.01, v);
         else if (k == "band_keep") c->band_keep = (float)std::max(0.0, std::min(1.0, v));
         else if (k == "band_passes") c->band_passes = std::max(1, std::min(64, (int)v));
