@@ -162,6 +162,23 @@ __device__ __forceinline__ void pdl_enter() {
     asm volatile("griddepcontrol.launch_dependents;" :::);
 }
 
+// GPU-scope memory-model helpers.  Cross-CTA hand-offs use a release/acquire
+// atomic by one thread after a CTA barrier (cumulative through bar.sync)
+// instead of a sequentially consistent fence in every thread.
+__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // Order-preserving float <-> uint32 map (for atomicMax on floats of any sign).
 __device__ __forceinline__ unsigned f2key(float f) {
     const unsigned b = __float_as_uint(f);

@@ -684,13 +684,9 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
     }
     }  // persistent tile loop
     // the last CTA out resets the slot counter for the next launch
-    if (tid == 0) {
-        __threadfence();
-        if (atomicAdd(&p.ctl->ctas_done, 1) == (int)gridDim.x - 1) {
-            p.ctl->next = 0;
-            p.ctl->ctas_done = 0;
-            __threadfence();
-        }
+    if (tid == 0 && atom_add_acq_rel(&p.ctl->ctas_done, 1) == (int)gridDim.x - 1) {
+        p.ctl->next = 0;
+        p.ctl->ctas_done = 0;
     }
 }
 
@@ -776,12 +772,10 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_ref_pairs(const double* __r
     if (MODE == 1 && ex != nullptr) {
         // single-rank exact pass: the last CTA out gathers the survivors' nn
         __shared__ int s_last;
-        __threadfence();
         __syncthreads();
-        if (threadIdx.x == 0) s_last = atomicAdd(&ctl->xdone, 1) == (int)gridDim.x - 1;
+        if (threadIdx.x == 0) s_last = atom_add_acq_rel(&ctl->xdone, 1) == (int)gridDim.x - 1;
         __syncthreads();
         if (!s_last) return;
-        __threadfence();
         const int ec = ctl->ec;
         for (int e = threadIdx.x; e < ec; e += blockDim.x)
             nnout[e] = __longlong_as_double((long long)__ldcg(&nnkey[ex[e]]));
@@ -1211,19 +1205,15 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
     // ---- compaction (decoupled look-back)
     int tot;
     const int ex = block_exscan(c, wsum, &tot);
-    volatile unsigned long long* vs = status;
+    // the words carry only counts: relaxed GPU-scope stores and loads suffice
     if (threadIdx.x < 32) {
         if (bid == 0) {
             if (lane == 0) {
-                __threadfence();
-                vs[0] = lb_word(epoch, 2u, (unsigned)tot);
+                st_relaxed_u64(&status[0], lb_word(epoch, 2u, (unsigned)tot));
                 s_excl = 0;
             }
         } else {
-            if (lane == 0) {
-                __threadfence();
-                vs[bid] = lb_word(epoch, 1u, (unsigned)tot);
-            }
+            if (lane == 0) st_relaxed_u64(&status[bid], lb_word(epoch, 1u, (unsigned)tot));
             int excl = 0;
             int j = bid - 1;
             for (;;) {
@@ -1231,7 +1221,7 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
                 unsigned long long wv;
                 bool ok;
                 do {
-                    wv = idx >= 0 ? vs[idx] : lb_word(epoch, 2u, 0u);
+                    wv = idx >= 0 ? ld_relaxed_u64(&status[idx]) : lb_word(epoch, 2u, 0u);
                     ok = (unsigned)(wv >> 34) == (epoch & 0x3fffffffu) && ((wv >> 32) & 3u) != 0u;
                 } while (!__all_sync(0xffffffffu, ok));
                 const unsigned incl_mask = __ballot_sync(0xffffffffu, ((wv >> 32) & 3u) == 2u);
@@ -1250,8 +1240,7 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
                 j -= 32;
             }
             if (lane == 0) {
-                __threadfence();
-                vs[bid] = lb_word(epoch, 2u, (unsigned)(excl + tot));
+                st_relaxed_u64(&status[bid], lb_word(epoch, 2u, (unsigned)(excl + tot)));
                 s_excl = excl;
             }
         }
@@ -1264,12 +1253,10 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
     }
     if (bid == nb - 1 && threadIdx.x == 0) ctl->ctotal = s_excl + tot;
     // ---- the last CTA to finish sees every scatter, slot and cost: it finalises
-    __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(&ctl->cdone, 1) == nb - 1;
+    if (threadIdx.x == 0) s_last = atom_add_acq_rel(&ctl->cdone, 1) == nb - 1;
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
     const int total = *(volatile int*)&ctl->ctotal;
     {  // span costs: sum of the per-CTA partials
         double c6[kSpans];
