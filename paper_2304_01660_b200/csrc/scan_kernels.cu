@@ -63,7 +63,7 @@ struct __align__(16) ScanSmem {
         } seed32;
     } u;
     float red[7][kThreads / 32];
-    int flag;
+    int flag[2];
 };
 
 __device__ __forceinline__ float warp_max(float v) {
@@ -72,49 +72,71 @@ __device__ __forceinline__ float warp_max(float v) {
     return v;
 }
 
-// Bands left for the catch-all tracked launch: the far rest [tK0, N) when the
-// far chunks are unfinished, and the near chunk [m, kend) unless it ran.
-__device__ __forceinline__ void track_rest(const TryCtl* ctl, int N, int m, long long& nf, long long& nn) {
-    const long long k_max = (long long)N - 1;
-    nf = nn = 0;
-    if (ctl->tphase >= 2) return;
-    if (ctl->tphase == 0) {
-        if ((long long)ctl->tK0 <= k_max) nf = (k_max - ctl->tK0 + kW) / kW;
-        if (ctl->kend > m) nn = ((long long)ctl->kend - m + kW - 1) / kW;
-    } else {
-        nn = ctl->tnb;  // the pending near chunk starts at m
-    }
-}
+// Launch-invariant tile-space values, read from the control block once per
+// CTA (the previous kernels of the try wrote them): the tile loop then decodes
+// a slot with one load (its group) instead of a chain of control-block loads.
+struct TileCtx {
+    long long slots;  // tile slots of the launch
+    long long G;      // groups (band / tracked / full spaces)
+    long long nf;     // catch-all: far bands [tK0, N) still to run
+    long long k0;     // band / tracked spaces: first diagonal of band 0
+};
 
-// Number of tile slots of a launch's tile space (device-side: the group count
-// of kSpaceBand / kSpaceFull is only known on the device).
-__device__ __forceinline__ long long tile_slots(const ScanParams& p) {
+__device__ __forceinline__ TileCtx load_ctx(const ScanParams& p) {
     const TryCtl* ctl = p.ctl;
+    TileCtx c{0, 0, 0, 0};
     switch (p.space) {
-        case kSpaceSeed: return (long long)p.nb * ((p.N + p.L - 1) / p.L);  // nb = sides (1 or 2)
-        case kSpaceBlocks: return 2ll * p.nb * ((p.N + p.L - 1) / p.L);
-        case kSpaceBand: return ctl->stop < p.pass ? 0 : 2ll * ctl->bnb * ctl->G;
-        case kSpaceTrack: return ctl->tphase >= 2 ? 0 : 2ll * ctl->tnb * ctl->G;
+        case kSpaceSeed: c.slots = (long long)p.nb * ((p.N + p.L - 1) / p.L); break;  // nb = sides (1 or 2)
+        case kSpaceBlocks:
+            c.G = (p.N + p.L - 1) / p.L;
+            c.slots = 2ll * p.nb * c.G;
+            c.k0 = p.K0;
+            break;
+        case kSpaceBand:
+            c.G = ctl->G;
+            c.k0 = ctl->bK0;
+            c.slots = ctl->stop < p.pass ? 0 : 2ll * ctl->bnb * c.G;
+            break;
+        case kSpaceTrack:
+            c.G = ctl->G;
+            c.k0 = ctl->tK0;
+            c.slots = ctl->tphase >= 2 ? 0 : 2ll * ctl->tnb * c.G;
+            break;
         case kSpaceTrackRest: {
-            long long nf, nn;
-            track_rest(ctl, p.N, p.m, nf, nn);
-            return 2ll * (nf + nn) * ctl->G;
+            // bands left for the catch-all: the far rest [tK0, N) when the far
+            // chunks are unfinished, and the near chunk [m, kend) unless it ran
+            const long long k_max = (long long)p.N - 1;
+            long long nf = 0, nn = 0;
+            const int ph = ctl->tphase;
+            if (ph == 0) {
+                if ((long long)ctl->tK0 <= k_max) nf = (k_max - ctl->tK0 + kW) / kW;
+                if (ctl->kend > p.m) nn = ((long long)ctl->kend - p.m + kW - 1) / kW;
+            } else if (ph == 1) {
+                nn = ctl->tnb;  // the pending near chunk starts at m
+            }
+            c.G = ctl->G;
+            c.nf = nf;
+            c.k0 = ctl->tK0;
+            c.slots = 2ll * (nf + nn) * c.G;
+            break;
         }
         default: {  // full rows: the farthest group needs ceil((N - m) / kW) tiles a side
+            c.G = ctl->G;
             const long long maxc = ((long long)p.N - p.m + kW - 1) / kW;
-            return maxc > 0 ? 2ll * maxc * ctl->G : 0;
+            c.slots = maxc > 0 ? 2ll * maxc * c.G : 0;
         }
     }
+    return c;
 }
 
 // Slot -> tile.  Band spaces are band-major (near bands first), full rows are
 // distance-major across groups (near tiles of every group first), so kills
 // from near diagonals land before the far tiles are fetched.
-__device__ __forceinline__ bool tile_decode(const ScanParams& p, long long t, TileDesc& td) {
+__device__ __forceinline__ bool tile_decode(const ScanParams& p, const TileCtx& c, long long t, TileDesc& td) {
     const int N = p.N;
     const int side = (int)(t & 1);
     int a, e;
-    long long G, k0;
+    long long k0;
     if (p.space == kSpaceSeed) {
         if (p.nb == 1) t <<= 1;  // one-sided band 0: positive side only
         const int j = (int)(t >> 1);
@@ -136,40 +158,31 @@ __device__ __forceinline__ bool tile_decode(const ScanParams& p, long long t, Ti
         return true;
     }
     td.seed = -1;
+    const long long G = c.G;
+    const long long b = t / (2 * G);
     if (p.space == kSpaceBlocks) {
-        G = (N + p.L - 1) / p.L;
-        const long long b = t / (2 * G);
         const int g = (int)((t >> 1) % G);
         a = g * p.L;
         e = min(N, a + p.L) - 1;
-        k0 = (long long)p.K0 + b * kW;
+        k0 = c.k0 + b * kW;
     } else if (p.space == kSpaceBand || p.space == kSpaceTrack || p.space == kSpaceTrackRest) {
-        G = p.ctl->G;
-        const long long b = t / (2 * G);
         const int2 gr = p.groups[(t >> 1) % G];
         a = gr.x;
         e = gr.y;
-        if (p.space == kSpaceTrackRest) {
-            long long nf, nn;
-            track_rest(p.ctl, N, p.m, nf, nn);
-            k0 = b < nf ? (long long)p.ctl->tK0 + b * kW : (long long)p.m + (b - nf) * kW;
-        } else {
-            k0 = (long long)(p.space == kSpaceBand ? p.ctl->bK0 : p.ctl->tK0) + b * kW;
-        }
+        if (p.space == kSpaceTrackRest) k0 = b < c.nf ? c.k0 + b * kW : (long long)p.m + (b - c.nf) * kW;
+        else k0 = c.k0 + b * kW;
     } else {
-        G = p.ctl->G;
-        const long long i = t / (2 * G);
         const int2 gr = p.groups[(t >> 1) % G];
         a = gr.x;
         e = gr.y;
         td.r0 = a;
         td.rows = e - a + 1;
         if (side == 0) {  // k in [m, N-1-a]
-            if ((long long)p.m + i * kW > (long long)N - 1 - a) return false;
-            td.k0 = p.m + (int)i * kW;
+            if ((long long)p.m + b * kW > (long long)N - 1 - a) return false;
+            td.k0 = p.m + (int)b * kW;
             td.dir = +1;
         } else {  // k in [-e, -m]
-            const long long khi = -(long long)p.m - i * kW;
+            const long long khi = -(long long)p.m - b * kW;
             if (e + khi < 0) return false;
             td.k0 = (int)(khi - kW + 1);
             td.dir = -1;
@@ -240,21 +253,28 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
     __shared__ uint8_t* s_peer_alive[kMaxPeers];  // slow path: peer pointers without a param copy
     if (threadIdx.x < kMaxPeers) s_peer_alive[threadIdx.x] = p.peers.alive[threadIdx.x];
     const int tid = threadIdx.x;
-    const long long slots = tile_slots(p);
+    const TileCtx cx = load_ctx(p);
+    const long long slots = cx.slots;
     // persistent CTAs: slots are fetched dynamically; rank r owns slots r, r+world, ...
     const long long mine = p.world > 1 ? (slots > p.rank ? (slots - p.rank + p.world - 1) / p.world : 0) : slots;
     // first round static (CTA b takes slot b: the hardware spreads consecutive
     // CTAs over the SMs, so a launch with fewer tiles than CTAs stays balanced),
-    // then dynamic
-    for (long long f = blockIdx.x;;) {
+    // then dynamic.  Per slot, the next slot's fetch, the decode and the
+    // all-decided test overlap and share one barrier, which also retires the
+    // previous tile's shared memory; the fetched slot lands in S.flag[par],
+    // which is not rewritten before the next iteration's barrier.
+    int par = 0;
+    for (long long f = blockIdx.x;; par ^= 1) {
     if (f >= mine) break;
+    if (tid == 0) S.flag[par] = atomicAdd(&p.ctl->next, 1);
     TileDesc td;
-    const bool valid = tile_decode(p, f * p.world + p.rank, td);
-    __syncthreads();  // smem of the previous tile is dead; S.flag is free
-    if (tid == 0) S.flag = atomicAdd(&p.ctl->next, 1);
-    __syncthreads();
-    f = (long long)S.flag + gridDim.x;
-    if (!valid) continue;
+    const bool valid = tile_decode(p, cx, f * p.world + p.rank, td);
+    int any = 0;
+    if (valid)  // tiles whose rows are all decided are skipped
+        for (int s = tid; s < td.rows; s += kThreads) any |= p.alive[td.r0 + s];
+    const bool work = __syncthreads_or(any);
+    f = (long long)S.flag[par] + gridDim.x;
+    if (!work) continue;
     const int rows = td.rows;
     const int dir = td.dir;
     const int N = p.N;
@@ -265,12 +285,6 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
     const int qbase = dir > 0 ? td.r0 + td.k0 : r_end + td.k0 + kW - 1;
     const int nq = rows - 1 + kW;
 
-    // ---- 0. skip tiles whose rows are all decided -------------------------
-    {
-        int any = 0;
-        for (int s = tid; s < rows; s += kThreads) any |= p.alive[td.r0 + s];
-        if (!__syncthreads_or(any)) continue;
-    }
 
     // ---- 1. seeds: cov(c_first, q) for this thread's kDiag diagonals --------
     float cov[kDiag];
