@@ -149,6 +149,7 @@ struct ScanParams {
     int seed32;          // FP32 direct seeds (with their error term in E) outside the band passes too
     Peers peers;         // fused cross-rank kills / maxima (n > 1), else local
     int half;            // band passes: evaluate 1 cell in `half` (1: all)
+    int pair;            // band 0 (kSpaceSeed, both sides): one paired walk per row block (k_band0_pair)
     const double* seedqt;  // resident raw dot products QT(i, i+k) of the band-0 tiles (kW per tile)
     unsigned long long* acc;  // accounting: [0] cells walked, [1] cells evaluated, [2] seed dots
 };

@@ -121,6 +121,7 @@ struct tsd_ctx {
     DBuf<double> seedqt;
     int64_t seed_m = -1;
     int seed_L = 0, seed_kA = 0, seed_nb = 0;
+    bool seed_pair = false;  // band 0 of this run walks both sides together (k_band0_pair)
     DBuf<int> cand;
     DBuf<float> ythr;
     DBuf<unsigned long long> nnkey, acc;  // acc: [0] cells, [1] seeds
@@ -149,7 +150,8 @@ struct tsd_ctx {
     // misses is walked again later).  Measured: C2 41.0 -> 39.5 ms, C4 1060 ->
     // 1013 ms with 1/3 in pass 0 and 1/2 in the later band passes.
     int half_pass0 = 3, half_bands = 2;
-    long long half_bands_m = 256;  // later passes use half_bands only from this length on
+    long long half_bands_m = 256;
+    int pair_band0 = 1;  // both sides of band 0 in one packed-FP32x2 walk  // later passes use half_bands only from this length on
     int seed32_track = 1;    // FP32 seeds in the full-row launch (wider error band, half the seed cost; C4 -3.4%)
     int seed32_collect = 1;  // ... and in the collection launch
     float band_keep = 0.85f;  // band loop stops when a pass leaves more than this fraction alive
@@ -349,18 +351,25 @@ struct tsd_ctx {
     // Rows per band-0 block: 512 when the blocks fill the persistent grid, else
     // smaller blocks (256/128) so that small series still occupy every SM
     // (measured at C2: 256 rows 55.5 ms, 128 rows 56.8 ms, 512 rows 57.8 ms).
-    int block_rows(int64_t N) const {
+    int block_rows(int64_t N, bool paired = false) const {
         if (dense_rows > 0) return dense_rows;
-        const int64_t want = (4 * (int64_t)scan_slots_prune()) / 5;  // ~one wave of the band-pass scan grid
+        // ~one wave of the band-pass scan grid: two tiles per block (one per
+        // side), or one when both sides walk together (k_band0_pair)
+        const int64_t want = (4 * (int64_t)(paired ? band0_pair_slots() : scan_slots_prune())) / 5;
+        const int per = paired ? 1 : 2;
         for (int L = kMaxRows; L > 128; L /= 2)
-            if (2 * ((N + L - 1) / L) >= want) return L;
+            if (per * ((N + L - 1) / L) >= want) return L;
         return 128;
     }
 
     // ---- resident seed rows ----------------------------------------------
     void seed_init(int64_t m, int64_t kA) {
         const int64_t N = n - m + 1;
-        seed_L = block_rows(N);
+        // the paired walk only when its largest blocks still fill a wave
+        // (measured: C4 / C5 gain 1-2%; at C2 the smaller blocks it would need
+        // cost more in staging than the walk saves)
+        seed_pair = pair_band0 != 0 && band0_sides == 2 && block_rows(N, true) == kMaxRows;
+        seed_L = block_rows(N, seed_pair);
         seed_kA = (int)kA;
         seed_nb = 2 * (int)((N + seed_L - 1) / seed_L);
         seedqt.ensure((size_t)seed_nb * kW);
@@ -596,6 +605,7 @@ struct tsd_ctx {
                     q.L = seed_L;
                     q.kA = seed_kA;
                     q.nb = band0_sides;
+                    q.pair = seed_pair;
                 } else if (pass == 0) {
                     q.space = kSpaceBlocks;
                     q.L = block_rows(N);
@@ -1538,6 +1548,7 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "half_pass0") c->half_pass0 = std::max(1, std::min(3, (int)v));
         else if (k == "half_bands") c->half_bands = std::max(1, std::min(3, (int)v));
         else if (k == "half_bands_m") c->half_bands_m = (long long)v;
+        else if (k == "pair_band0") c->pair_band0 = v != 0.0;
         else if (k == "seed_w") c->seed_w = (float)std::max(0.01, v);
         else if (k == "band_keep") c->band_keep = (float)std::max(0.0, std::min(1.0, v));
         else if (k == "band_passes") c->band_passes = std::max(1, std::min(64, (int)v));

@@ -24,6 +24,23 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, c
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
+// the same with dynamic shared memory
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl_smem(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                   Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 void launch_init_stats(const double* t, int n, int m, double* mu, double* sig, double* scratch_a,
                        double* scratch_b, cudaStream_t st);
 void launch_advance_stats(const double* t, int n, int m, double* mu, double* sig, cudaStream_t st);
@@ -63,7 +80,8 @@ void launch_compact_group(const uint8_t* a, int n, int* out, unsigned long long*
                           TryCtl* ctl, int gate, int2* groups, int2* slots, int m, int fixed_span, float band_keep,
                           int band_few, float seed_w, double* bcost, cudaStream_t st);
 int group_slots(int n);
-int scan_slots_prune();  // persistent grid of the band-pass scan (SMs x resident CTAs)
+int scan_slots_prune();
+int band0_pair_slots();  // persistent grid of the paired band-0 walk (k_band0_pair)  // persistent grid of the band-pass scan (SMs x resident CTAs)
 // tracked full-row chunks: schedule of the first chunk (after the band passes)
 void launch_track_init(TryCtl* ctl, int N, int m, bool bands_ran, cudaStream_t st);
 void launch_seed_init(const double* t, int n, int m, int L, int kA, int nb, double* qt, cudaStream_t st);

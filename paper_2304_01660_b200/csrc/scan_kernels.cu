@@ -244,6 +244,69 @@ __device__ __noinline__ void slow_track(const F9 x, const F9 qn, float tz, float
     }
 }
 
+// FP64 direct seeds: cov(c_first, q) for this thread's kDiag diagonals, q =
+// qbase + u (dir > 0) or qbase - u (dir < 0), u = tid*kDiag + j.
+// cov = sum_p (t[c+p]-mu_c) t[q+p] - mu_q * sum_p (t[c+p]-mu_c).  sa / swin:
+// shared scratch of kSeedChunk and kW + kSeedChunk doubles; every thread of
+// the CTA calls it (it synchronises).
+__device__ __forceinline__ void seed_fp64(const ScanParams& p, int c_first, int qbase, int dir, double* sa,
+                                          double* swin, float (&cov)[kDiag]) {
+    const int tid = threadIdx.x;
+    const int N = p.N, m = p.m;
+    const int qlo = dir > 0 ? qbase : qbase - (kW - 1);
+    const int o_t = dir > 0 ? tid * kDiag : kW - kDiag - tid * kDiag;  // lowest window offset
+    double acc[kDiag];
+#pragma unroll
+    for (int i = 0; i < kDiag; ++i) acc[i] = 0.0;
+    double delta = 0.0;
+    const double mu_c = p.mu[c_first];
+    for (int pc = 0; pc < m; pc += kSeedChunk) {
+        const int len = min(kSeedChunk, m - pc);
+        __syncthreads();
+#pragma unroll 4
+        for (int x = tid; x < len; x += kThreads) sa[x] = p.t[c_first + pc + x] - mu_c;
+#pragma unroll 4
+        for (int x = tid; x < kW + len - 1; x += kThreads) {
+            const int g = qlo + pc + x;
+            swin[x] = (g >= 0 && g < p.n) ? p.t[g] : 0.0;
+        }
+        __syncthreads();
+        double w[kDiag];
+#pragma unroll
+        for (int i = 0; i < kDiag - 1; ++i) w[i] = swin[o_t + i];
+        int pp = 0;
+        for (; pp + kDiag <= len; pp += kDiag) {
+#pragma unroll
+            for (int uu = 0; uu < kDiag; ++uu) {
+                // ring: window value for offset o_t + pp + uu + i lives in w[(uu + i) % kDiag]
+                w[(uu + kDiag - 1) % kDiag] = swin[o_t + pp + uu + kDiag - 1];
+                const double av = sa[pp + uu];
+                delta += av;
+#pragma unroll
+                for (int i = 0; i < kDiag; ++i) acc[i] = fma(av, w[(uu + i) % kDiag], acc[i]);
+            }
+        }
+        for (; pp < len; ++pp) {
+            const double av = sa[pp];
+            delta += av;
+#pragma unroll
+            for (int i = 0; i < kDiag; ++i) acc[i] = fma(av, swin[o_t + pp + i], acc[i]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < kDiag; ++i) {
+        const int q = qlo + o_t + i;
+        acc[i] = (q >= 0 && q < N) ? acc[i] - p.mu[q] * delta : 0.0;
+    }
+    if (dir > 0) {
+#pragma unroll
+        for (int j = 0; j < kDiag; ++j) cov[j] = (float)acc[j];
+    } else {
+#pragma unroll
+        for (int j = 0; j < kDiag; ++j) cov[j] = (float)acc[kDiag - 1 - j];
+    }
+}
+
 template <int MODE, int STRIDE = 1>
 __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(const ScanParams p) {
     pdl_enter();
@@ -369,59 +432,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
             for (int j = 0; j < kDiag; ++j) cov[j] = (float)seedv[kDiag - 1 - j];
         }
     } else {
-    // cov = sum_p (t[c+p]-mu_c) t[q+p] - mu_q * sum_p (t[c+p]-mu_c)
-    const int qlo = dir > 0 ? qbase : qbase - (kW - 1);
-    const int o_t = dir > 0 ? tid * kDiag : kW - kDiag - tid * kDiag;  // lowest window offset
-    double acc[kDiag];
-#pragma unroll
-    for (int i = 0; i < kDiag; ++i) acc[i] = 0.0;
-    double delta = 0.0;
-    const double mu_c = p.mu[c_first];
-    for (int pc = 0; pc < m; pc += kSeedChunk) {
-        const int len = min(kSeedChunk, m - pc);
-        __syncthreads();
-#pragma unroll 4
-        for (int x = tid; x < len; x += kThreads) S.u.seed.a[x] = p.t[c_first + pc + x] - mu_c;
-#pragma unroll 4
-        for (int x = tid; x < kW + len - 1; x += kThreads) {
-            const int g = qlo + pc + x;
-            S.u.seed.win[x] = (g >= 0 && g < p.n) ? p.t[g] : 0.0;
-        }
-        __syncthreads();
-        double w[kDiag];
-#pragma unroll
-        for (int i = 0; i < kDiag - 1; ++i) w[i] = S.u.seed.win[o_t + i];
-        int pp = 0;
-        for (; pp + kDiag <= len; pp += kDiag) {
-#pragma unroll
-            for (int uu = 0; uu < kDiag; ++uu) {
-                // ring: window value for offset o_t + pp + uu + i lives in w[(uu + i) % kDiag]
-                w[(uu + kDiag - 1) % kDiag] = S.u.seed.win[o_t + pp + uu + kDiag - 1];
-                const double av = S.u.seed.a[pp + uu];
-                delta += av;
-#pragma unroll
-                for (int i = 0; i < kDiag; ++i) acc[i] = fma(av, w[(uu + i) % kDiag], acc[i]);
-            }
-        }
-        for (; pp < len; ++pp) {
-            const double av = S.u.seed.a[pp];
-            delta += av;
-#pragma unroll
-            for (int i = 0; i < kDiag; ++i) acc[i] = fma(av, S.u.seed.win[o_t + pp + i], acc[i]);
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < kDiag; ++i) {
-        const int q = qlo + o_t + i;
-        acc[i] = (q >= 0 && q < N) ? acc[i] - p.mu[q] * delta : 0.0;
-    }
-    if (dir > 0) {
-#pragma unroll
-        for (int j = 0; j < kDiag; ++j) cov[j] = (float)acc[j];
-    } else {
-#pragma unroll
-        for (int j = 0; j < kDiag; ++j) cov[j] = (float)acc[kDiag - 1 - j];
-    }
+        seed_fp64(p, c_first, qbase, dir, S.u.seed.a, S.u.seed.win, cov);
     }
     __syncthreads();  // seed buffers are reused below
 
@@ -661,14 +672,14 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
             rd[uu % kDiag] = qdp[ss + kDiag];
             rn[uu % kDiag] = qnp[ss + kDiag];
         }
-        if (MODE == kPrune && hit) {
-            // certain kills of the row candidates (FP32 only)
-            do {
-                const int uu = __ffs(hit) - 1;
-                hit &= hit - 1;
-                const int ss = s0 + uu;
+        if (MODE == kPrune) {
+            // certain kills of the row candidates (FP32 only), warp-aggregated:
+            // lane b stores the row of step s0 + b if any lane killed it
+            const unsigned h = __reduce_or_sync(0xffffffffu, hit);
+            if (lane < kDiag && ((h >> lane) & 1u)) {
+                const int ss = s0 + lane;
                 peer_kill(p.peers, p.alive, dir > 0 ? td.r0 + ss : r_end - ss);
-            } while (hit);
+            }
         }
     }
 
@@ -698,6 +709,266 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
     }
     }  // persistent tile loop
     // the last CTA out resets the slot counter for the next launch
+    if (tid == 0 && atom_add_acq_rel(&p.ctl->ctas_done, 1) == (int)gridDim.x - 1) {
+        p.ctl->next = 0;
+        p.ctl->ctas_done = 0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Band 0 with both sides in one walk (packed FP32x2).
+//
+// A band-0 tile of k_scan walks one side of one row block.  Here one CTA walks
+// both sides of row block j together: lane .x of every register pair is the
+// positive side (rows a + s, q = c + kA + u, resident seed row 2j), lane .y the
+// negative side (rows e - s, q = c - kA - u, seed row 2j+1), so each step is
+// FFMA2 / FMUL2 on pairs.  Per side the arithmetic is exactly k_scan's: the
+// same operands, the same two roundings per cell in the same order, the same
+// kill rule, so the kills are identical and the error bound E (taken over
+// both sides' maxima) stays valid.  Half the issue slots of the walk.
+struct __align__(16) PairSmem {
+    float4 crow[kRowsPad];  // per row step: {cdf+, cdf-, cdg+, cdg-}
+    float2 ctc[kRowsPad];   // per row step: thresholds {tc+, tc-} (first: norms)
+    union {
+        struct {
+            float4 qd[kQPad];  // per q step: {qdf+, qdf-, qdg+, qdg-}
+            float2 qn[kQPad];  // per q step: norms (NaN: invalid q)
+        } walk;
+        struct {
+            double a[kSeedChunk];
+            double win[kW + kSeedChunk];
+        } seed;
+    } u;
+    float red[7][kThreads / 32];
+    int flag[2];
+};
+
+template <int STRIDE>
+__global__ void __launch_bounds__(kThreads, 4) k_band0_pair(const ScanParams p) {
+    pdl_enter();
+    extern __shared__ __align__(16) unsigned char pair_smem[];
+    PairSmem& S = *reinterpret_cast<PairSmem*>(pair_smem);
+    const int tid = threadIdx.x;
+    const int N = p.N, m = p.m, L = p.L, kA = p.kA;
+    const long long slots = (N + L - 1) / L;
+    const long long mine = p.world > 1 ? (slots > p.rank ? (slots - p.rank + p.world - 1) / p.world : 0) : slots;
+    int par = 0;
+    for (long long f = blockIdx.x;; par ^= 1) {
+    if (f >= mine) break;
+    if (tid == 0) S.flag[par] = atomicAdd(&p.ctl->next, 1);
+    const int jb = (int)(f * p.world + p.rank);
+    const int a = jb * L, e = min(N, a + L) - 1, rows = e - a + 1;
+    const bool v0 = (long long)a + kA < N, v1 = (long long)e - kA >= 0;
+    int any = 0;
+    if (v0 || v1)
+        for (int s = tid; s < rows; s += kThreads) any |= p.alive[a + s];
+    const bool work = __syncthreads_or(any);
+    f = (long long)S.flag[par] + gridDim.x;
+    if (!work) continue;
+    const int qb0 = a + kA, qb1 = e - kA;  // q of step 0, u = 0 on each side
+    const int nq = rows - 1 + kW;
+
+    // ---- seeds (resident rows; the partial last block's negative side direct)
+    float2 cov[kDiag];
+    bool direct1 = false;
+    {
+        float c0[kDiag], c1[kDiag];
+        const double* qt0 = p.seedqt + (size_t)(2 * jb) * kW + tid * kDiag;
+        const double mm0 = (double)m * p.mu[a];
+#pragma unroll
+        for (int j = 0; j < kDiag; ++j) {
+            const int q = qb0 + tid * kDiag + j;
+            c0[j] = (v0 && q < N) ? (float)(qt0[j] - mm0 * p.mu[q]) : 0.f;
+        }
+        if (rows == L) {
+            const double* qt1 = p.seedqt + (size_t)(2 * jb + 1) * kW + tid * kDiag;
+            const double mm1 = (double)m * p.mu[e];
+#pragma unroll
+            for (int j = 0; j < kDiag; ++j) {
+                const int q = qb1 - tid * kDiag - j;
+                c1[j] = (v1 && q >= 0) ? (float)(qt1[j] - mm1 * p.mu[q]) : 0.f;
+            }
+        } else if (v1) {
+            seed_fp64(p, e, qb1, -1, S.u.seed.a, S.u.seed.win, c1);
+            direct1 = true;
+            __syncthreads();  // seed scratch is reused below
+        } else {
+#pragma unroll
+            for (int j = 0; j < kDiag; ++j) c1[j] = 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < kDiag; ++j) cov[j] = make_float2(c0[j], c1[j]);
+    }
+
+    // ---- stage the walk operands of both sides (k_scan's staging, per side)
+    float cn_min = FLT_MAX, qn_min = FLT_MAX, qn_max = 0.f;
+    float dc = 0.f, gc = 0.f, dq = 0.f, gq = 0.f;
+#pragma unroll 4
+    for (int s = tid; s < rows; s += kThreads) {
+        const int c0 = a + s, c1 = e - s;
+        const int ci1 = min(c1 + 1, N - 1);  // s == 0 takes no increment
+        float4 v;
+        v.x = (s == 0 || !v0) ? 0.f : p.df[c0];
+        v.z = (s == 0 || !v0) ? 0.f : p.dg[c0];
+        v.y = (s == 0 || !v1) ? 0.f : -p.df[ci1];
+        v.w = (s == 0 || !v1) ? 0.f : -p.dg[ci1];
+        const float n0 = p.nrm[c0];
+        if (n0 != 0.f) cn_min = fminf(cn_min, n0);  // both sides walk the rows [a, e]
+        dc = fmaxf(dc, fmaxf(fabsf(v.x), fabsf(v.y)));
+        gc = fmaxf(gc, fmaxf(fabsf(v.z), fabsf(v.w)));
+        S.crow[s] = v;
+        S.ctc[s] = make_float2(n0, p.nrm[c1]);
+    }
+    const int rows_p = (rows + kDiag - 1) / kDiag * kDiag;
+    for (int s = rows + tid; s <= rows_p; s += kThreads) {
+        S.crow[s] = make_float4(0.f, 0.f, 0.f, 0.f);
+        S.ctc[s] = make_float2(FLT_MAX, FLT_MAX);
+    }
+    const float qnan = __int_as_float(0x7fffffff);
+#pragma unroll 4
+    for (int u = tid; u < rows_p + kW + kDiag; u += kThreads) {
+        const int q0 = qb0 + u, q1 = qb1 - u;
+        const bool ok0 = v0 && u < nq && q0 < N;
+        const bool ok1 = v1 && u < nq && q1 >= 0;
+        const int qc0 = ok0 ? q0 : 0, qc1 = ok1 ? q1 : 0;
+        const int qi1 = min(qc1 + 1, N - 1);
+        float a0 = p.df[qc0], b0 = p.dg[qc0], a1 = p.df[qi1], b1 = p.dg[qi1];
+        const float n0 = p.nrm[qc0], n1 = p.nrm[qc1];
+        if (!ok0) a0 = b0 = 0.f;
+        if (!ok1 || qc1 + 1 >= N) a1 = b1 = 0.f;
+        if (ok0 && n0 != 0.f) {
+            qn_min = fminf(qn_min, n0);
+            qn_max = fmaxf(qn_max, n0);
+        }
+        if (ok1 && n1 != 0.f) {
+            qn_min = fminf(qn_min, n1);
+            qn_max = fmaxf(qn_max, n1);
+        }
+        dq = fmaxf(dq, fmaxf(fabsf(a0), fabsf(a1)));
+        gq = fmaxf(gq, fmaxf(fabsf(b0), fabsf(b1)));
+        S.u.walk.qd[u] = make_float4(a0, a1, b0, b1);
+        S.u.walk.qn[u] = make_float2((ok0 && n0 != 0.f) ? n0 : qnan, (ok1 && n1 != 0.f) ? n1 : qnan);
+    }
+    cn_min = -warp_max(-cn_min);
+    qn_min = -warp_max(-qn_min);
+    qn_max = warp_max(qn_max);
+    dc = warp_max(dc);
+    gc = warp_max(gc);
+    dq = warp_max(dq);
+    gq = warp_max(gq);
+    if ((tid & 31) == 0) {
+        S.red[0][tid >> 5] = cn_min;
+        S.red[1][tid >> 5] = qn_min;
+        S.red[2][tid >> 5] = qn_max;
+        S.red[3][tid >> 5] = dc;
+        S.red[4][tid >> 5] = gc;
+        S.red[5][tid >> 5] = dq;
+        S.red[6][tid >> 5] = gq;
+    }
+    __syncthreads();
+    cn_min = FLT_MAX;
+    qn_min = FLT_MAX;
+    qn_max = 0.f;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+        cn_min = fminf(cn_min, S.red[0][w]);
+        qn_min = fminf(qn_min, S.red[1][w]);
+        qn_max = fmaxf(qn_max, S.red[2][w]);
+        dc = fmaxf(dc, S.red[3][w]);
+        gc = fmaxf(gc, S.red[4][w]);
+        dq = fmaxf(dq, S.red[5][w]);
+        gq = fmaxf(gq, S.red[6][w]);
+    }
+    const double inv_sqm = 1.0 / sqrt((double)m);
+    const double smax_c = cn_min < FLT_MAX ? inv_sqm / (double)cn_min * (1.0 + 1e-6) : 0.0;
+    const double smax_q = qn_min < FLT_MAX ? inv_sqm / (double)qn_min * (1.0 + 1e-6) : 0.0;
+    // k_scan's bound over the union of both sides' operands; the direct FP64
+    // seed and the resident seeds carry no seed error term
+    const double P = (double)dc * (double)gq + (double)dq * (double)gc;
+    const double E = p.err_k * (double)kEps32 * (double)(rows + 8) * ((double)m * smax_c * smax_q + 1.5 * P);
+    constexpr float kNoEval = FLT_MAX;
+    int evals = 0;
+    for (int s = tid; s < rows; s += kThreads) {
+        const float2 cn = S.ctc[s];
+        float2 tc;
+        const bool live0 = v0 && p.alive[a + s] != 0, live1 = v1 && p.alive[e - s] != 0;
+        if (!live0 || cn.x == 0.f) {
+            tc.x = kNoEval;
+        } else {
+            const double eps_row = E * (double)cn.x * (double)qn_max + kSlack + 8.0 * (double)kEps32;
+            tc.x = (float)((p.thr0 + eps_row) / (double)cn.x);
+            tc.x = tc.x + fabsf(tc.x) * 2.4e-7f;  // round toward +inf (conservative)
+        }
+        if (!live1 || cn.y == 0.f) {
+            tc.y = kNoEval;
+        } else {
+            const double eps_row = E * (double)cn.y * (double)qn_max + kSlack + 8.0 * (double)kEps32;
+            tc.y = (float)((p.thr0 + eps_row) / (double)cn.y);
+            tc.y = tc.y + fabsf(tc.y) * 2.4e-7f;
+        }
+        S.ctc[s] = tc;
+        evals += (tc.x != kNoEval) + (tc.y != kNoEval);
+    }
+    evals = __syncthreads_count(evals);
+
+    // ---- walk: k_scan's ring, on pairs
+    float4 rd[kDiag];
+    float2 rn[kDiag];
+    const int ub = tid * kDiag;
+    const float4* qdp = S.u.walk.qd + ub;
+    const float2* qnp = S.u.walk.qn + ub;
+#pragma unroll
+    for (int j = 0; j < kDiag; ++j) {
+        rd[j] = qdp[j];
+        rn[j] = qnp[j];
+    }
+    float4 cr_next = S.crow[0];
+    float2 tc_next = S.ctc[0];
+    for (int s0 = 0; s0 < rows_p; s0 += kDiag) {
+        unsigned hit0 = 0u, hit1 = 0u;
+#pragma unroll
+        for (int uu = 0; uu < kDiag; ++uu) {
+            const int ss = s0 + uu;
+            const float4 cr = cr_next;
+            const float2 tc = tc_next;
+            cr_next = S.crow[ss + 1];
+            tc_next = S.ctc[ss + 1];
+            const float2 cdf = make_float2(cr.x, cr.y), cdg = make_float2(cr.z, cr.w);
+#pragma unroll
+            for (int j = 0; j < kDiag; ++j) {
+                const int rj = (j + uu) % kDiag;
+                cov[j] = __ffma2_rn(cdf, make_float2(rd[rj].z, rd[rj].w), cov[j]);
+                cov[j] = __ffma2_rn(make_float2(rd[rj].x, rd[rj].y), cdg, cov[j]);
+            }
+            float mx0 = -FLT_MAX, mx1 = -FLT_MAX;
+#pragma unroll
+            for (int j = 0; j < kDiag; ++j)
+                if ((j + uu) % STRIDE == 0) {
+                    const float2 x = __fmul2_rn(cov[j], rn[(j + uu) % kDiag]);
+                    mx0 = fmaxf(mx0, x.x);
+                    mx1 = fmaxf(mx1, x.y);
+                }
+            hit0 |= (mx0 > tc.x ? 1u : 0u) << uu;
+            hit1 |= (mx1 > tc.y ? 1u : 0u) << uu;
+            rd[uu % kDiag] = qdp[ss + kDiag];
+            rn[uu % kDiag] = qnp[ss + kDiag];
+        }
+        // warp-aggregated kills: lanes 0..8 store the positive side's killed
+        // rows of this block, lanes 16..24 the negative side's (one store per
+        // row and warp instead of one per thread and hit)
+        {
+            const unsigned h0 = __reduce_or_sync(0xffffffffu, hit0), h1 = __reduce_or_sync(0xffffffffu, hit1);
+            const int lane = tid & 31, b = lane & 15;
+            if (b < kDiag && (((lane < 16 ? h0 : h1) >> b) & 1u))
+                peer_kill(p.peers, p.alive, lane < 16 ? a + s0 + b : e - (s0 + b));
+        }
+    }
+    if (tid == 0) {
+        atomicAdd(&p.acc[0], (unsigned long long)rows * (unsigned long long)kW * (unsigned long long)(v0 + v1));
+        atomicAdd(&p.acc[1], (unsigned long long)evals * (unsigned long long)(kW / STRIDE));
+        if (direct1) atomicAdd(&p.acc[2], (unsigned long long)kW);
+    }
+    }  // persistent tile loop
     if (tid == 0 && atom_add_acq_rel(&p.ctl->ctas_done, 1) == (int)gridDim.x - 1) {
         p.ctl->next = 0;
         p.ctl->ctas_done = 0;
@@ -1647,9 +1918,42 @@ static int scan_grid() {
     return g_scan_grid[MODE];
 }
 
+static int g_pair_grid = 0;
+
+int band0_pair_slots() {
+    if (g_pair_grid == 0) {
+        int dev = 0, sms = 148, per = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int bytes = (int)sizeof(PairSmem);
+        cudaFuncSetAttribute(k_band0_pair<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        cudaFuncSetAttribute(k_band0_pair<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        cudaFuncSetAttribute(k_band0_pair<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        cudaFuncSetAttribute(k_band0_pair<1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_band0_pair<2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_band0_pair<3>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_band0_pair<3>, kThreads, bytes);
+        if (const char* e = std::getenv("TSD_SCAN_CTAS")) per = std::min(per, std::max(1, std::atoi(e)));
+        g_pair_grid = sms * (per > 0 ? per : 1);
+    }
+    return g_pair_grid;
+}
+
+static void launch_band0_pair(const ScanParams& p, cudaStream_t st) {
+    const int grid = band0_pair_slots();
+    const size_t bytes = sizeof(PairSmem);
+    if (p.half == 2) launch_pdl_smem(k_band0_pair<2>, grid, kThreads, bytes, st, p);
+    else if (p.half >= 3) launch_pdl_smem(k_band0_pair<3>, grid, kThreads, bytes, st, p);
+    else launch_pdl_smem(k_band0_pair<1>, grid, kThreads, bytes, st, p);
+}
+
 void launch_scan(int mode, const ScanParams& p, cudaStream_t st) {
     switch (mode) {
         case kPrune:
+            if (p.space == kSpaceSeed && p.pair) {  // both sides of band 0 in one walk
+                launch_band0_pair(p, st);
+                break;
+            }
             if (p.half == 2) launch_pdl(k_scan<kPrune, 2>, scan_grid<kPrune>(), kThreads, st, p);
             else if (p.half >= 3) launch_pdl(k_scan<kPrune, 3>, scan_grid<kPrune>(), kThreads, st, p);
             else launch_pdl(k_scan<kPrune>, scan_grid<kPrune>(), kThreads, st, p);

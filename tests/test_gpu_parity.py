@@ -113,6 +113,22 @@ def test_merlin_golden_c2(engine):
     check_merlin(rep, fx)
 
 
+@pytest.mark.parametrize("pair", [0, 1])
+def test_merlin_golden_c2_band0_walks(engine, pair):
+    # band 0 walked per side (k_scan) and both sides together in packed FP32x2
+    # (k_band0_pair, which 512-row blocks enable at this size): same records
+    fx = load_golden("c2.json")
+    engine.set_series(series_of(fx["input"]))
+    engine.set_param("dense_rows", 512)
+    engine.set_param("pair_band0", pair)
+    try:
+        rep = engine.merlin_full(fx["min_len"], fx["max_len"], top_k=fx["top_k"], seglen=fx["seglen"])
+        check_merlin(rep, fx)
+    finally:
+        engine.set_param("dense_rows", 0)
+        engine.set_param("pair_band0", 1)
+
+
 @pytest.mark.slow
 def test_merlin_golden_c4(engine):
     # BASELINE config 4: n=1,000,000 random walk, lengths 512..1024 (513 lengths);
