@@ -159,20 +159,28 @@ __device__ __forceinline__ bool tile_decode(const ScanParams& p, const TileCtx& 
     }
     td.seed = -1;
     const long long G = c.G;
-    const long long b = t / (2 * G);
+    long long b, gi;  // band and group of the slot (32-bit division when it fits: no 64-bit emulation)
+    if (c.slots <= 0xffffffffll) {
+        const unsigned tt = (unsigned)t, g1 = (unsigned)G;
+        b = tt / (2u * g1);
+        gi = (tt >> 1) % g1;
+    } else {
+        b = t / (2 * G);
+        gi = (t >> 1) % G;
+    }
     if (p.space == kSpaceBlocks) {
-        const int g = (int)((t >> 1) % G);
+        const int g = (int)gi;
         a = g * p.L;
         e = min(N, a + p.L) - 1;
         k0 = c.k0 + b * kW;
     } else if (p.space == kSpaceBand || p.space == kSpaceTrack || p.space == kSpaceTrackRest) {
-        const int2 gr = p.groups[(t >> 1) % G];
+        const int2 gr = p.groups[gi];
         a = gr.x;
         e = gr.y;
         if (p.space == kSpaceTrackRest) k0 = b < c.nf ? c.k0 + b * kW : (long long)p.m + (b - c.nf) * kW;
         else k0 = c.k0 + b * kW;
     } else {
-        const int2 gr = p.groups[(t >> 1) % G];
+        const int2 gr = p.groups[gi];
         a = gr.x;
         e = gr.y;
         td.r0 = a;
