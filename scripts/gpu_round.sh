@@ -19,7 +19,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
    --log-file $out/launches_c4_$tag.csv python scripts/one_run.py c4 16 > /dev/null 2>&1; echo "ncu list c4 rc=$?"
 # full capture: pass 0 and the next band passes of a working C4 try (skip the
 # first, all-killing try: 3 launches), and 8 consecutive scans of C2
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_scan -s 8 -c 6 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_scan|k_band0" -s 8 -c 6 \
    -o $out/scan_c4_$tag -f python scripts/one_run.py c4 3 > $out/ncu_full_c4_$tag.log 2>&1; echo "ncu full c4 rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_scan -s 20 -c 8 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_scan|k_band0" -s 20 -c 8 \
    -o $out/scan_c2_$tag -f python scripts/one_run.py c2 12 > $out/ncu_full_c2_$tag.log 2>&1; echo "ncu full c2 rc=$?"

@@ -219,6 +219,24 @@ def test_group_sharded_merlin_equals_single(engine, ranks, fused):
     g.close()
 
 
+def test_group_sharded_paired_band0(engine):
+    # the paired band-0 walk (k_band0_pair, forced by 512-row blocks) with its
+    # row blocks dealt over 2 ranks and fused peer kills: golden C2 records
+    import paper_2304_01660_b200 as P
+    g = P.Group([0, 0])
+    g.set_param("fused_peers", 1)
+    g.set_param("dense_rows", 512)
+    g.set_param("pair_band0", 1)
+    fx = load_golden("c2.json")
+    g.set_series(series_of(fx["input"]))
+    rep = g.merlin_full(fx["min_len"], fx["min_len"] + 15, top_k=fx["top_k"], seglen=fx["seglen"])
+    want = dict(fx)
+    want["per_length"] = [e for e in fx["per_length"] if e["m"] <= fx["min_len"] + 15]
+    want["max_len"] = fx["min_len"] + 15
+    check_merlin(rep, want)
+    g.close()
+
+
 def test_group_sharded_range_sets(engine, oracle):
     import paper_2304_01660_b200 as P
     g = P.Group([0, 0])
