@@ -211,7 +211,22 @@ int tsd_reset_counters(tsd_ctx* ctx);
 /* Diagnostic: FP32 FFMA throughput of `device` (TFLOP/s, 2 flops per FFMA),
  * measured with a dependent-chain-free FFMA loop over all SMs. */
 int tsd_fp32_peak_probe(int device, double* tflops);
-/* Tuning knobs (testing only): key in {"dense_rows","sparse_rows","err_scale"}. */
+/* Tuning knobs (testing and tuning only).  Except err_scale, they change the
+ * schedule, never the results.  Returns TSD_EINVAL for an unknown key.  Keys:
+ *   dense_rows      rows per band-0 block (0: auto)
+ *   sparse_rows     fixed group span (0: cost model)
+ *   err_scale       err_k of the FP32 error bound (default 4; a smaller value
+ *                   voids the bound's proof)
+ *   band_passes     cap on band passes per try;  band_few / band_keep: break rule
+ *   half_pass0, half_bands, half_bands_m   reduced-density evaluation strides
+ *   pair_band0      paired both-sides band-0 walk for large series (1)
+ *   band0_sides     sides of band 0 (2)
+ *   seed_w          cost-model weight of a seed element vs a walked row
+ *   seed32_track, seed32_collect           FP32 seeds in those launches
+ *   track_chunks    tracked full-row chunks (1: one catch-all launch)
+ *   fused_peers     rank groups: peer stores inside the kernels (1)
+ *   scan_events     bracket scans with events (per-phase timing; slower)
+ *   result_prefix   records copied back with the try's single sync */
 int tsd_set_param(tsd_ctx* ctx, const char* key, double value);
 
 #ifdef __cplusplus
