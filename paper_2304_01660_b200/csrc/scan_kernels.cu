@@ -656,8 +656,10 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
                         // row max of the FP32 route value x = cov*qn over valid q (NaN for
                         // invalid q is ignored by fmaxf; a constant q contributes exactly
                         // 0); the tile's error term E*qn_max is folded in at the end
-                        const float y = warp_max(mx);
-                        if (lane == 0 && y > -FLT_MAX) atomicMax(&S.ykey[ss], f2key(y));
+                        // (keys are order-preserving and mx is never NaN: one REDUX
+                        // gives the key of the warp max)
+                        const unsigned yk = __reduce_max_sync(0xffffffffu, f2key(mx));
+                        if (lane == 0 && yk > f2key(-FLT_MAX)) atomicMax(&S.ykey[ss], yk);
                     }
                 }
                 if (MODE == kCollect) {
