@@ -64,6 +64,7 @@ struct __align__(16) ScanSmem {
     } u;
     float red[7][kThreads / 32];
     int flag[2];
+    int2 span[2][kThreads / 32];  // per warp: first / last undecided row of the tile (double-buffered)
 };
 
 __device__ __forceinline__ float warp_max(float v) {
@@ -340,10 +341,37 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
     if (tid == 0) S.flag[par] = atomicAdd(&p.ctl->next, 1);
     TileDesc td;
     const bool valid = tile_decode(p, cx, f * p.world + p.rank, td);
-    int any = 0;
-    if (valid)  // tiles whose rows are all decided are skipped
-        for (int s = tid; s < td.rows; s += kThreads) any |= p.alive[td.r0 + s];
-    const bool work = __syncthreads_or(any);
+    bool work;
+    if (MODE == kCollect || p.space == kSpaceSeed) {
+        int any = 0;
+        if (valid)  // tiles whose rows are all decided are skipped
+            for (int s = tid; s < td.rows; s += kThreads) any |= p.alive[td.r0 + s];
+        work = __syncthreads_or(any);
+    } else {
+        // directly seeded tiles shrink to their first..last undecided row:
+        // rows only die, and the seed is taken at the new first row
+        int lo = INT_MAX, hi = -1;
+        if (valid)
+            for (int s = tid; s < td.rows; s += kThreads)
+                if (p.alive[td.r0 + s]) {
+                    lo = min(lo, s);
+                    hi = s;
+                }
+        lo = __reduce_min_sync(0xffffffffu, lo);
+        hi = __reduce_max_sync(0xffffffffu, hi);
+        if ((tid & 31) == 0) S.span[par][tid >> 5] = make_int2(lo, hi);
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < kThreads / 32; ++w) {
+            lo = min(lo, S.span[par][w].x);
+            hi = max(hi, S.span[par][w].y);
+        }
+        work = hi >= 0;
+        if (work) {
+            td.r0 += lo;
+            td.rows = hi - lo + 1;
+        }
+    }
     f = (long long)S.flag[par] + gridDim.x;
     if (!work) continue;
     const int rows = td.rows;
