@@ -1445,6 +1445,7 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
     __shared__ int s_bid, s_excl, s_last, s_k;
     __shared__ int wsum[32];
     __shared__ int s_fa[32], s_la[32];
+    __shared__ int2 s_lb[32];
     __shared__ double s_cost[32][kSpans];
     const int nb = gridDim.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1525,47 +1526,50 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
             bcost[bid * kSpans + threadIdx.x] = v;
         }
     }
-    // ---- compaction (decoupled look-back)
+    // ---- compaction (decoupled look-back).  Every thread examines one
+    // predecessor (thread i: CTA bid-1-i), so one round of loads covers 1024
+    // predecessors; each warp sums its values up to its nearest inclusive
+    // prefix, and the warps combine in order.  The words carry only counts:
+    // relaxed GPU-scope stores and loads suffice.
     int tot;
     const int ex = block_exscan(c, wsum, &tot);
-    // the words carry only counts: relaxed GPU-scope stores and loads suffice
-    if (threadIdx.x < 32) {
-        if (bid == 0) {
-            if (lane == 0) {
-                st_relaxed_u64(&status[0], lb_word(epoch, 2u, (unsigned)tot));
-                s_excl = 0;
-            }
-        } else {
-            if (lane == 0) st_relaxed_u64(&status[bid], lb_word(epoch, 1u, (unsigned)tot));
-            int excl = 0;
-            int j = bid - 1;
-            for (;;) {
-                const int idx = j - lane;
+    if (threadIdx.x == 0) {
+        st_relaxed_u64(&status[bid], lb_word(epoch, bid == 0 ? 2u : 1u, (unsigned)tot));
+        if (bid == 0) s_excl = 0;
+    }
+    if (bid > 0) {
+        int excl = 0;
+        for (int j0 = bid - 1;; j0 -= (int)blockDim.x) {
+            const int idx = j0 - (int)threadIdx.x;
+            unsigned state = 2u, val = 0u;  // before CTA 0: an inclusive zero
+            if (idx >= 0) {
                 unsigned long long wv;
-                bool ok;
                 do {
-                    wv = idx >= 0 ? ld_relaxed_u64(&status[idx]) : lb_word(epoch, 2u, 0u);
-                    ok = (unsigned)(wv >> 34) == (epoch & 0x3fffffffu) && ((wv >> 32) & 3u) != 0u;
-                } while (!__all_sync(0xffffffffu, ok));
-                const unsigned incl_mask = __ballot_sync(0xffffffffu, ((wv >> 32) & 3u) == 2u);
-                int v = (int)(unsigned)wv;
-                if (incl_mask) {
-                    const int L = __ffs(incl_mask) - 1;  // nearest inclusive predecessor
-                    if (lane > L) v = 0;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                    excl += v;
+                    wv = ld_relaxed_u64(&status[idx]);
+                } while ((unsigned)(wv >> 34) != (epoch & 0x3fffffffu) || ((wv >> 32) & 3u) == 0u);
+                state = (unsigned)(wv >> 32) & 3u;
+                val = (unsigned)wv;
+            }
+            const unsigned incl = __ballot_sync(0xffffffffu, state == 2u);
+            const int L = incl ? __ffs(incl) - 1 : 31;
+            const unsigned part = __reduce_add_sync(0xffffffffu, lane <= L ? val : 0u);
+            if (lane == 0) s_lb[w] = make_int2(incl != 0u, (int)part);
+            __syncthreads();
+            bool found = false;
+            for (int x = 0; x < (int)(blockDim.x >> 5); ++x) {
+                const int2 v = s_lb[x];
+                excl += v.y;
+                if (v.x) {
+                    found = true;
                     break;
                 }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                excl += v;
-                j -= 32;
             }
-            if (lane == 0) {
-                st_relaxed_u64(&status[bid], lb_word(epoch, 2u, (unsigned)(excl + tot)));
-                s_excl = excl;
-            }
+            if (found) break;
+            __syncthreads();  // s_lb is rewritten by the next window
+        }
+        if (threadIdx.x == 0) {
+            st_relaxed_u64(&status[bid], lb_word(epoch, 2u, (unsigned)(excl + tot)));
+            s_excl = excl;
         }
     }
     __syncthreads();
