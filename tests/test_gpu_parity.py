@@ -193,6 +193,31 @@ def test_merlin_vs_oracle_top3(engine, oracle):
             assert recs_list(rep.per_length[m]) == recs_list(exp["recs"][0][: exp["counts"][0]])
 
 
+@pytest.mark.parametrize("seed", range(1, 9))
+def test_merlin_random_shapes_vs_oracle(engine, oracle, seed):
+    # ragged shapes: n from 600 to 6000 (N below, near and above one tile of
+    # 1152 diagonals and 128..512-row blocks), short and long windows, top-1..3;
+    # every length's records, final r and retry count equal the C restatement
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(600, 6001))
+    lo = int(rng.integers(4, 97))
+    hi = lo + int(rng.integers(0, 13))
+    top_k = int(rng.integers(1, 4))
+    x = oracle.gen_randomwalk(n, 100 + seed)
+    if seed % 2 == 0:  # a periodic series with noise: many near-equal neighbours
+        t = np.arange(n)
+        x = np.sin(2 * np.pi * t / (37 + seed)) + 0.05 * x / (np.abs(x).max() + 1.0)
+    engine.set_series(x)
+    rep = engine.merlin_full(lo, hi, top_k=top_k)
+    exp = oracle.merlin(x, lo, hi, top_k=top_k)
+    for k, m in enumerate(range(lo, hi + 1)):
+        assert (m in rep.failed_lengths) == bool(exp["failed"][k]), m
+        assert float(rep.final_r[k]) == float(exp["final_r"][k]), m
+        assert int(rep.retries[k]) == int(exp["retries"][k]), m
+        if not exp["failed"][k]:
+            assert recs_list(rep.per_length[m]) == recs_list(exp["recs"][k][: exp["counts"][k]]), m
+
+
 def test_merlin_constant_series_fails_lengths(engine):
     engine.set_series(np.full(400, 2.5))
     rep = engine.merlin_full(8, 12)
