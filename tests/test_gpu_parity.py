@@ -193,8 +193,8 @@ def test_merlin_vs_oracle_top3(engine, oracle):
             assert recs_list(rep.per_length[m]) == recs_list(exp["recs"][0][: exp["counts"][0]])
 
 
-@pytest.mark.parametrize("seed", range(1, 9))
-def test_merlin_random_shapes_vs_oracle(engine, oracle, seed):
+@pytest.mark.parametrize("seed,paired", [(s, 0) for s in range(1, 9)] + [(s, 1) for s in range(1, 5)])
+def test_merlin_random_shapes_vs_oracle(engine, oracle, seed, paired):
     # ragged shapes: n from 600 to 6000 (N below, near and above one tile of
     # 1152 diagonals and 128..512-row blocks), short and long windows, top-1..3;
     # every length's records, final r and retry count equal the C restatement
@@ -208,7 +208,12 @@ def test_merlin_random_shapes_vs_oracle(engine, oracle, seed):
         t = np.arange(n)
         x = np.sin(2 * np.pi * t / (37 + seed)) + 0.05 * x / (np.abs(x).max() + 1.0)
     engine.set_series(x)
-    rep = engine.merlin_full(lo, hi, top_k=top_k)
+    if paired:  # the paired band-0 walk on a series of one or a few (partial) blocks
+        engine.set_param("dense_rows", 512)
+    try:
+        rep = engine.merlin_full(lo, hi, top_k=top_k)
+    finally:
+        engine.set_param("dense_rows", 0)
     exp = oracle.merlin(x, lo, hi, top_k=top_k)
     for k, m in enumerate(range(lo, hi + 1)):
         assert (m in rep.failed_lengths) == bool(exp["failed"][k]), m
