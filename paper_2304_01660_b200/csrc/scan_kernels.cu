@@ -1018,18 +1018,34 @@ __global__ void __launch_bounds__(kThreads, 4) k_band0_pair(const ScanParams p) 
 __device__ double ref_dist_warp(const double* __restrict__ t, int m, int i, int j, double* buf) {
     const int lane = threadIdx.x & 31;
     double mean = 0.0, sg = 0.0;
-    if (lane < 2) {
-        const double* x = t + (lane == 0 ? i : j);
+    {
+        // window statistics: the warp stages 128-element chunks of both
+        // windows in shared memory (coalesced, all loads in flight); lane 0
+        // (window i) and lane 1 (window j) keep the reference's sequential sums
         double s = 0.0, q = 0.0;
-        for (int k = 0; k < m; ++k) {
-            const double v = x[k];
-            s = __dadd_rn(s, v);
-            q = __dadd_rn(q, __dmul_rn(v, v));
+        for (int base = 0; base < m; base += 128) {
+            const int len = min(128, m - base);
+            for (int k = lane; k < len; k += 32) {
+                buf[k] = t[i + base + k];
+                buf[128 + k] = t[j + base + k];
+            }
+            __syncwarp();
+            if (lane < 2) {
+                const double* x = buf + 128 * lane;
+                for (int k = 0; k < len; ++k) {
+                    const double v = x[k];
+                    s = __dadd_rn(s, v);
+                    q = __dadd_rn(q, __dmul_rn(v, v));
+                }
+            }
+            __syncwarp();
         }
-        const double md = (double)m;
-        mean = __ddiv_rn(s, md);
-        const double var = __dsub_rn(__ddiv_rn(q, md), __dmul_rn(mean, mean));
-        sg = __dsqrt_rn(var > 0.0 ? var : 0.0);
+        if (lane < 2) {
+            const double md = (double)m;
+            mean = __ddiv_rn(s, md);
+            const double var = __dsub_rn(__ddiv_rn(q, md), __dmul_rn(mean, mean));
+            sg = __dsqrt_rn(var > 0.0 ? var : 0.0);
+        }
     }
     const double mx = __shfl_sync(0xffffffffu, mean, 0), sx = __shfl_sync(0xffffffffu, sg, 0);
     const double my = __shfl_sync(0xffffffffu, mean, 1), sy = __shfl_sync(0xffffffffu, sg, 1);
