@@ -200,14 +200,18 @@ __global__ void k_next_length(const double* __restrict__ t, int n, int m, const 
         }
     }
     if (qt != nullptr) {
-        const long long total = (long long)nb * kW;
-        for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-             e += (long long)gridDim.x * blockDim.x) {
-            const int b = (int)(e / kW), u = (int)(e % kW);
+        // one seed row per block iteration: no 64-bit index division, the row
+        // value t[i+m] is a broadcast, qt and t[q+m] are coalesced
+        for (int b = blockIdx.x; b < nb; b += gridDim.x) {
             const int j = b >> 1;
             const int i = (b & 1) ? j * L + L - 1 : j * L;
-            const int q = (b & 1) ? i - kA - u : i + kA + u;
-            if (i < cnt && q >= 0 && q < cnt) qt[e] = fma(t[i + m], t[q + m], qt[e]);
+            if (i >= cnt) continue;
+            const double ti = t[i + m];
+            double* row = qt + (size_t)b * kW;
+            for (int u = threadIdx.x; u < kW; u += blockDim.x) {
+                const int q = (b & 1) ? i - kA - u : i + kA + u;
+                if (q >= 0 && q < cnt) row[u] = fma(ti, t[q + m], row[u]);
+            }
         }
     }
 }
