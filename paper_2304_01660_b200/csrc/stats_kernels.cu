@@ -177,9 +177,15 @@ __global__ void k_next_length(const double* __restrict__ t, int n, int m, const 
         cr_next[2] = 0;
     }
     const double sqm = sqrt((double)m1);
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
-        double u, s;
-        advance1(t, m, i, mu_in, sig_in, u, s);
+    const int lane = threadIdx.x & 31;
+    // the loop bound is warp-uniform (the shuffle below needs every lane)
+    const int cnt_w = (cnt + 31) & ~31;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt_w; i += gridDim.x * blockDim.x) {
+        double u = 0.0, s = 0.0;
+        if (i < cnt) advance1(t, m, i, mu_in, sig_in, u, s);
+        // mu_{i-1} of length m+1 from the neighbouring lane (lane 0 recomputes it)
+        double up = __shfl_up_sync(0xffffffffu, u, 1);
+        if (i >= cnt) continue;
         mu_out[i] = u;
         sig_out[i] = s;
         nrm[i] = s < kSigmaEps ? 0.f : (float)(1.0 / (sqm * s));
@@ -192,8 +198,10 @@ __global__ void k_next_length(const double* __restrict__ t, int n, int m, const 
             df[0] = 0.f;
             dg[0] = 0.f;
         } else {
-            double up, sp;
-            advance1(t, m, i - 1, mu_in, sig_in, up, sp);  // mu_{i-1} of length m+1 (same rounding)
+            if (lane == 0) {
+                double sp;
+                advance1(t, m, i - 1, mu_in, sig_in, up, sp);  // same rounding as the neighbour's
+            }
             const double a = t[i + m1 - 1], b = t[i - 1];
             df[i] = (float)((a - b) * 0.5);
             dg[i] = (float)((a - u) + (b - up));
