@@ -150,7 +150,7 @@ struct tsd_ctx {
     // misses is walked again later).  Measured: C2 41.0 -> 39.5 ms, C4 1060 ->
     // 1013 ms with 1/3 in pass 0 and 1/2 in the later band passes.
     int half_pass0 = 3, half_bands = 3;
-    long long half_bands_m = 256;
+    long long half_bands_m = 128;
     int pair_band0 = 1;  // both sides of band 0 in one packed-FP32x2 walk  // later passes use half_bands only from this length on
     int seed32_track = 1;    // FP32 seeds in the full-row launch (wider error band, half the seed cost; C4 -3.4%)
     int seed32_collect = 1;  // ... and in the collection launch
