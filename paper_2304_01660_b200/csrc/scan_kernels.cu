@@ -1,27 +1,30 @@
 // PD3 scan kernels for sm_100a (north_star (b), (c)).
 //
-// k_scan<MODE> is the hot path: one CTA per parallelogram tile of the distance
-// matrix (TileDesc).  It replaces the reference's per-segment scan_chunk loop
-// (src/pardrag.cpp:157-282) with a B200 layout:
-//   * seeds: the tile's first row of covariances is computed directly in FP64
-//     from the series staged in shared memory (the reference seeds row+column
-//     per chunk, pardrag.cpp:162-182; a parallelogram needs only the row);
+// k_scan<MODE> is the hot path: persistent CTAs that fetch parallelogram tiles
+// of the distance matrix (TileDesc) and replace the reference's per-segment
+// scan_chunk loop (src/pardrag.cpp:157-282) with a B200 layout:
+//   * seeds: the covariances of the tile's first row, from resident FP64 seed
+//     rows carried across lengths (band 0), or as FP32 dot products over the
+//     series staged in shared memory with their rounding in the error bound
+//     (the reference seeds row+column per chunk, pardrag.cpp:162-182; a
+//     parallelogram needs only the row);
 //   * walk: every thread advances kDiag adjacent diagonals with the FP32
 //     centered-covariance recurrence cov(i,j) = cov(i-1,j-1) + df_i dg_j + df_j dg_i
 //     (2 FFMA per cell; the q-side operands slide through registers, the
 //     c-side operand is a shared-memory broadcast);
-//   * decision: corr = cov * nrm_c * nrm_q is compared with 1 - r^2/(2m) in a
-//     branch-free fast path (one FMUL + FMNMX per cell); a cell that may be
-//     within the proven FP32 error band of the threshold falls into the slow
-//     path, which kills certain pairs (both ends, like cand/neighbor clearing,
-//     pardrag.cpp:256-259) and queues knife-edge pairs for the exact FP64
-//     recheck (the analogue of pardrag.cpp:255).
+//   * decision: x = cov * nrm_q is compared with the row's threshold
+//     (corr > 1 - r^2/(2m) widened by the proven FP32 error bound).  Band
+//     passes only make certain kills (aggregated per warp); the full rows also
+//     queue knife-edge pairs for the exact FP64 recheck (the analogue of
+//     pardrag.cpp:255) and track each row's maximum for its nn bounds.
+// k_band0_pair walks both sides of a band-0 row block in one CTA on packed
+// FP32x2 registers (FFMA2), with k_scan's per-side arithmetic.
 // Kills are monotone byte stores, so the final state is schedule-independent.
 //
 // k_ref_pairs evaluates reference_sq_dist (pardrag.cpp:57-69 -> znormalize +
 // sq_ed, distance.cpp:8-33) bit-exactly, one warp per pair: the reference's
-// sequential sums stay sequential (lane 0), only the element-wise z-normalised
-// terms are computed in parallel.
+// sequential sums stay sequential (lanes 0/1), only the element-wise loads and
+// z-normalised terms are computed in parallel.
 #include <float.h>
 #include <limits.h>
 #include <stdlib.h>
@@ -42,7 +45,8 @@ constexpr int kRowsPad = kMaxRows + kDiag + 1;
 constexpr int kQPad = kMaxRows + kDiag + kW + kDiag;
 
 // Per-mode shared memory: the band passes need neither the collection
-// thresholds nor the row-max keys, which frees 4 KB per CTA (7 CTAs per SM).
+// thresholds nor the row-max keys, which frees 4 KB per CTA (6 band-pass CTAs per
+// SM fit at 80 registers; 7 were measured slower).
 template <int MODE>
 struct __align__(16) ScanSmem {
     float4 crow[kRowsPad];                           // per row: {cdf, cdg, tc, cn}
