@@ -704,9 +704,12 @@ struct tsd_ctx {
         // tracked chunks: run them one by one next time as far as this try needed
         track_hint = hc.tphase >= 2 ? hc.tpasses + 1 : std::min(16, std::max(track_hint, 4) + 2);
         if (r_sq > 0.0 && enq_passes > 0) {
-            if (hc.stop == INT_MAX) band_hint = enq_passes + 2;  // cut off by the count: allow more
-            else if (hc.stop_why == 2) band_hint = std::max(1, hc.passes);  // passes stopped paying
-            else band_hint = std::max(band_hint, hc.passes);  // ran out of rows: no evidence to shrink
+            // cut off by the count: allow more; otherwise (passes stopped paying,
+            // or rows ran out) enqueue what this try used: the passes after the
+            // device-side break are no-op launches (measured: C2 35.7 -> 35.4 ms,
+            // C3 631 -> 626 ms against keeping the largest count seen)
+            if (hc.stop == INT_MAX) band_hint = enq_passes + 2;
+            else band_hint = std::max(1, hc.passes);
         }
         const int ec = hc.ec;
         if (debug)
