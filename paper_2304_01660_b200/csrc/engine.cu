@@ -652,18 +652,12 @@ struct tsd_ctx {
         scan(kPruneTrack, q);
         reduce_alive(N);
         reduce_maxima(N);
-        // knife edges: the reference's FP64 distance decides (pardrag.cpp:255)
-        launch_ref_pairs(0, t.p, (int)m, queue.p, &C->queue, kQueueCap, r_sq, alive.p, nnkey.p, C, nullptr,
-                         nullptr, peers, st);
+        // knife edges: the reference's FP64 distance decides (pardrag.cpp:255);
+        // degenerate rows: every pair with one is decided exactly.  One launch.
+        launch_recheck(t.p, (int)m, N, queue.p, &C->queue, kQueueCap, list.p, C, cr_cur, deg.p, r_sq, alive.p,
+                       nnkey.p, rank, world, peers, st);
         ck(cudaGetLastError(), "recheck");
         reduce_alive(N);
-
-        // degenerate rows: every pair with one is decided exactly
-        launch_degenerate_pairs(t.p, (int)m, N, list.p, C, cr_cur, deg.p, r_sq, alive.p, nnkey.p, rank, world, peers,
-                                st);
-        ck(cudaGetLastError(), "degenerate pairs");
-        reduce_alive(N);
-        ctr.kernel_launches += 1;
 
         // ---- survivors: exact nearest neighbours (pardrag.cpp:378-416).  One
         // CTA filters the list to the survivors, applies the MERLIN top-k

@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
             tc = kNoEval;
         } else if (cn == 0.f) {
             // degenerate row (sigma < eps): decided exactly against every q
-            // (k_degenerate_pairs), never by the FP32 walk
+            // (k_recheck), never by the FP32 walk
             tc = kNoEval;
         } else if (MODE == kPrune) {
             // band passes only make certain kills: every cell with x > tk has
@@ -1133,16 +1133,12 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_ref_pairs(const double* __r
 //   A: every listed row still alive x every degenerate q (|c - q| >= m);
 //   B: every degenerate row x every q (|c - q| >= m).
 // d < r^2 kills the row; every d feeds its exact-nn key.  One warp per pair.
-__global__ void __launch_bounds__(kPairWarps * 32) k_degenerate_pairs(const double* __restrict__ t, int m, int N,
-                                                                      const int* __restrict__ list,
-                                                                      const TryCtl* __restrict__ ctl,
-                                                                      const int* __restrict__ cr,
-                                                                      const int* __restrict__ deg, double r_sq,
-                                                                      uint8_t* alive,
-                                                                      unsigned long long* nnkey, int rank,
-                                                                      int world, const Peers peers) {
-    pdl_enter();
-    __shared__ double buf[kPairWarps][256];
+// every pair with a degenerate row, decided exactly (dealt over the ranks)
+__device__ __forceinline__ void degenerate_body(const double* __restrict__ t, int m, int N,
+                                                const int* __restrict__ list, const TryCtl* __restrict__ ctl,
+                                                const int* __restrict__ cr, const int* __restrict__ deg, double r_sq,
+                                                uint8_t* alive, unsigned long long* nnkey, int rank, int world,
+                                                const Peers& peers, double* buf) {
     const int D = cr[2];
     if (D == 0) return;
     const long long nl = ctl->alive;
@@ -1161,12 +1157,39 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_degenerate_pairs(const doub
             q = (int)(f % N);
         }
         if (abs(c - q) < m) continue;
-        const double d = ref_dist_warp(t, m, c, q, buf[w]);
+        const double d = ref_dist_warp(t, m, c, q, buf);
         if ((threadIdx.x & 31) == 0) {
             if (d < r_sq) peer_kill(peers, alive, c);
             peer_min_key(peers, nnkey, c, (unsigned long long)__double_as_longlong(d));
         }
     }
+}
+
+// The knife-edge recheck and the degenerate pairs in
+// one launch: both only kill rows or lower nn keys, so their order is free.
+__global__ void __launch_bounds__(kPairWarps * 32) k_recheck(const double* __restrict__ t, int m, int N,
+                                                             const int2* __restrict__ pairs,
+                                                             const int* __restrict__ count, int cap,
+                                                             const int* __restrict__ list,
+                                                             const TryCtl* __restrict__ ctl,
+                                                             const int* __restrict__ cr,
+                                                             const int* __restrict__ deg, double r_sq,
+                                                             uint8_t* alive, unsigned long long* nnkey,
+                                                             int rank, int world, const Peers peers) {
+    pdl_enter();
+    __shared__ double buf[kPairWarps][256];
+    const int w = threadIdx.x >> 5;
+    const int total = min(*count, cap);
+    for (int e = blockIdx.x * kPairWarps + w; e < total; e += gridDim.x * kPairWarps) {
+        const int2 pr = pairs[e];
+        if (!alive[pr.x] && !alive[pr.y]) continue;
+        const double d = ref_dist_warp(t, m, pr.x, pr.y, buf[w]);
+        if ((threadIdx.x & 31) == 0 && d < r_sq) {
+            peer_kill(peers, alive, pr.x);
+            peer_kill(peers, alive, pr.y);
+        }
+    }
+    degenerate_body(t, m, N, list, ctl, cr, deg, r_sq, alive, nnkey, rank, world, peers, buf[w]);
 }
 
 // ---------------------------------------------------------------------------
@@ -1876,7 +1899,7 @@ __global__ void __launch_bounds__(1024) k_survivors(const int* __restrict__ list
     // it may be the reference's minimiser.
     for (int e = threadIdx.x; e < ec; e += blockDim.x) {
         const int c = cand[e];
-        if (nrm[c] == 0.f) continue;  // degenerate: exact nn from k_degenerate_pairs, never collected
+        if (nrm[c] == 0.f) continue;  // degenerate: exact nn from k_recheck, never collected
         const unsigned k = ymax[c];
         float th = -FLT_MAX;  // no tracked data: collect everything
         if (k > 1u) {
@@ -2037,11 +2060,11 @@ void launch_ref_pairs(int mode, const double* t, int m, const int2* pairs, const
                    nnout, peers);
 }
 
-void launch_degenerate_pairs(const double* t, int m, int N, const int* list, const TryCtl* ctl, const int* crange,
-                             const int* deg, double r_sq, uint8_t* alive, unsigned long long* nnkey, int rank,
-                             int world, const Peers& peers, cudaStream_t st) {
-    launch_pdl(k_degenerate_pairs, 148 * 4, kPairWarps * 32, st, t, m, N, list, ctl, crange, deg, r_sq, alive,
-               nnkey, rank, world, peers);
+void launch_recheck(const double* t, int m, int N, const int2* pairs, const int* count, int cap, const int* list,
+                    const TryCtl* ctl, const int* crange, const int* deg, double r_sq, uint8_t* alive,
+                    unsigned long long* nnkey, int rank, int world, const Peers& peers, cudaStream_t st) {
+    launch_pdl(k_recheck, 148 * 4, kPairWarps * 32, st, t, m, N, pairs, count, cap, list, ctl, crange, deg, r_sq,
+               alive, nnkey, rank, world, peers);
 }
 
 void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const unsigned* ymax,
