@@ -141,6 +141,16 @@ struct tsd_ctx {
     bool debug = std::getenv("TSD_DEBUG") != nullptr;
     int dense_rows = 0;  // rows per band-0 block; 0: auto (block_rows)
     int sparse_rows = 0;   // 0: choose by cost model (on the device)
+    // Bands of a later band pass: at least enough to fill band_fill waves of
+    // the scan grid (the compaction sizes the pass from its group count).
+    // Measured: more bands per pass kill more rows before the full rows; the
+    // best factor grows with the series (C2: 6 -> 33.3 ms vs 35.4 ms at 1;
+    // C4: 24 -> 768 ms vs 878 ms; C3 / C5 flat from 16 on).  0: automatic.
+    double band_fill = 0.0;
+    int band_slots(int64_t N) const {
+        const double f = band_fill > 0.0 ? band_fill : (N < (1 << 18) ? 6.0 : 24.0);
+        return (int)std::max(1.0, f * (double)scan_slots_prune());
+    }
     int band_passes = 6;  // cap on band passes (incl. pass 0) per try; full rows cover the rest (measured: C4 914 -> 896 ms vs 40)
     int band_hint = 0;     // adaptive count: passes the previous try needed (0: none yet)
     int track_hint = 0;    // ... and tracked chunks (plus the catch-all launch)
@@ -485,7 +495,7 @@ struct tsd_ctx {
         slots.ensure(group_slots(N));
         bcost.ensure((size_t)compact_blocks(N) * 6);
         launch_compact_group(alive.p, N, list.p, lbstat.p, epoch, ctl.p, gate, groups.p, slots.p, (int)m,
-                             sparse_rows, band_keep, band_few, seed_w, bcost.p, st);
+                             sparse_rows, band_keep, band_few, seed_w, bcost.p, band_slots(N), st);
         ck(cudaGetLastError(), "compact");
         ctr.kernel_launches += 1;
         // fused peers: no rank's next scan may store kills into this rank's
@@ -1548,6 +1558,7 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "pair_band0") c->pair_band0 = v != 0.0;
         else if (k == "seed_w") c->seed_w = (float)std::max(0.01, v);
         else if (k == "band_keep") c->band_keep = (float)std::max(0.0, std::min(1.0, v));
+        else if (k == "band_fill") c->band_fill = std::max(0.0, v);
         else if (k == "band_passes") c->band_passes = std::max(1, std::min(64, (int)v));
         else if (k == "result_prefix") c->result_prefix = std::max(16, std::min(1 << 20, (int)v));
         else fail(TSD_EINVAL, "unknown parameter " + k);

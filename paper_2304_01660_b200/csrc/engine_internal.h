@@ -79,7 +79,7 @@ int compact_blocks(int n);
 // words; slots: group_slots(n) entries)
 void launch_compact_group(const uint8_t* a, int n, int* out, unsigned long long* status, unsigned epoch,
                           TryCtl* ctl, int gate, int2* groups, int2* slots, int m, int fixed_span, float band_keep,
-                          int band_few, float seed_w, double* bcost, cudaStream_t st);
+                          int band_few, float seed_w, double* bcost, int band_slots, cudaStream_t st);
 int group_slots(int n);
 int scan_slots_prune();
 int band0_pair_slots();  // persistent grid of the paired band-0 walk (k_band0_pair)  // persistent grid of the band-pass scan (SMs x resident CTAs)

@@ -2090,11 +2090,11 @@ void launch_track_init(TryCtl* ctl, int N, int m, bool bands_ran, cudaStream_t s
 
 void launch_compact_group(const uint8_t* a, int n, int* out, unsigned long long* status, unsigned epoch,
                           TryCtl* ctl, int gate, int2* groups, int2* slots, int m, int fixed_span, float band_keep,
-                          int band_few, float seed_w, double* bcost, cudaStream_t st) {
+                          int band_few, float seed_w, double* bcost, int band_slots, cudaStream_t st) {
     launch_pdl(k_compact_group, compact_blocks(n), kCompactBlock, st, a, n, out, status, epoch, ctl, gate, groups, slots,
                                                                m, fixed_span, band_keep,
                                                                gate == kGateTrack ? scan_grid<kPruneTrack>()
-                                                                                  : scan_slots_prune(),
+                                                                                  : band_slots,
                                                                band_few, seed_w, bcost);
 }
 
