@@ -122,6 +122,32 @@ int tsd_next_threshold(const double* history, int64_t history_len, int phase, in
 int tsd_pardrag(tsd_ctx* ctx, int64_t m, double r_sq, int64_t seglen, const double* mu,
                 const double* sigma, tsd_record* out, int64_t cap, int64_t* count);
 
+/* ---- the two PD3 phases (pardrag.hpp:68-84; src/pardrag.cpp:339-419) -------
+ * On the device a try is one stream-ordered sequence (band passes, full rows,
+ * knife-edge recheck, exact nn), so the selection phase already decides every
+ * row exactly.  par_select: cand[i] (N = n-m+1 entries) is 1 for every
+ * subsequence with nn^2 >= r_sq (a candidate set with no false positives) and
+ * nn[i] its exact nn^2 (+inf for pruned rows: the device keeps no partial
+ * route minima).  par_refine: the records of the candidates still set in
+ * `cand` (callers may clear entries between the phases, as
+ * tests/pardrag_test.cpp:178-189 does), exact nn, sorted like sort_discords;
+ * a candidate-free state returns no records without a device pass. */
+int tsd_par_select(tsd_ctx* ctx, int64_t m, double r_sq, int64_t seglen, const double* mu,
+                   const double* sigma, uint8_t* cand, double* nn);
+int tsd_par_refine(tsd_ctx* ctx, int64_t m, double r_sq, int64_t seglen, const double* mu,
+                   const double* sigma, const uint8_t* cand, tsd_record* out, int64_t cap,
+                   int64_t* count);
+
+/* ---- MERLIN's length step, exposed for checking ----------------------------
+ * stats_walk: init_stats(m0) on the device, then m1-m0 length steps exactly as
+ * tsd_merlin runs them (fused != 0: the one-launch k_next_length step with the
+ * resident seed rows at kA = m1 when they fit; 0: the plain Eq. 7-8 advance).
+ * mu/sigma receive the n-m1+1 values of length m1 (src/stats.cpp:38-58 bit for
+ * bit).  seed_rows: the resident rows (info = {m, L, kA, nb}; out, if cap >=
+ * nb*1152, the raw dot products QT_m(i, i +- (kA+u)) row-major). */
+int tsd_stats_walk(tsd_ctx* ctx, int64_t m0, int64_t m1, int fused, double* mu, double* sigma);
+int tsd_seed_rows(tsd_ctx* ctx, double* out, int64_t cap, int64_t info[4]);
+
 /* ---- MERLIN (merlin.hpp:50-54; src/merlin.cpp:57-137) ---------------------
  * Arrays have L = max_len-min_len+1 entries (recs: L*top_k, row-major).
  * counts[k]  records kept for length min_len+k (0 for failed lengths)

@@ -48,10 +48,10 @@ class _Common:
 
     def _check(self, rc):
         if rc != 0:
-            raise CheckerError(rc, self.lib[self.prefix + "last_error"]().decode())
+            raise CheckerError(rc, getattr(self.lib, self.prefix + "last_error")().decode())
 
     def _bind_common(self):
-        self.lib[self.prefix + "last_error"].restype = C.c_char_p
+        getattr(self.lib, self.prefix + "last_error").restype = C.c_char_p
         self._gen = self._fn("gen_randomwalk", C.c_int, [_i64, C.c_uint64, _dp])
         self._init = self._fn("init_stats", C.c_int, [_dp, _i64, _i64, _dp, _dp])
         self._adv = self._fn("advance_stats", C.c_int, [_dp, _i64, _i64, _i64, _dp, _dp])

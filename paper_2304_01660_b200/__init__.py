@@ -34,7 +34,8 @@ EXPORTS = (
     "tsd_heatmap_build", "tsd_heatmap_set", "tsd_heatmap_rank",
     "tsd_group_create", "tsd_group_destroy", "tsd_group_last_error", "tsd_group_size", "tsd_group_ctx",
     "tsd_group_series_set", "tsd_group_merlin", "tsd_group_pardrag", "tsd_matrix_profile_fp64",
-    "tsd_ipc_export", "tsd_ipc_join",
+    "tsd_ipc_export", "tsd_ipc_join", "tsd_par_select", "tsd_par_refine", "tsd_stats_walk",
+    "tsd_seed_rows",
 )
 
 
@@ -100,6 +101,10 @@ def load_library(path: str = LIB_PATH):
     f("tsd_next_threshold", C.c_int, [_dp, _i64, C.c_int, _i64, C.c_double, C.c_int,
                                       C.POINTER(C.c_double)])
     f("tsd_pardrag", C.c_int, [vp, _i64, C.c_double, _i64, vp, vp, vp, _i64, C.POINTER(_i64)])
+    f("tsd_par_select", C.c_int, [vp, _i64, C.c_double, _i64, vp, vp, _u8, _dp])
+    f("tsd_par_refine", C.c_int, [vp, _i64, C.c_double, _i64, vp, vp, _u8, vp, _i64, C.POINTER(_i64)])
+    f("tsd_stats_walk", C.c_int, [vp, _i64, _i64, C.c_int, _dp, _dp])
+    f("tsd_seed_rows", C.c_int, [vp, vp, _i64, _ip])
     f("tsd_merlin", C.c_int, [vp, _i64, _i64, C.POINTER(_Opts), _ip, vp, _dp, _ip, _u8])
     f("tsd_brute_force_nn", C.c_int, [vp, _i64, _dp])
     f("tsd_matrix_profile_fp64", C.c_int, [vp, _i64, _dp])
@@ -276,6 +281,39 @@ class Engine:
             sg.ctypes.data if sg is not None else None,
             out.ctypes.data, N, C.byref(cnt)))
         return out[: cnt.value].copy()
+
+    def par_select(self, m: int, r_sq: float, seglen: int):
+        """(cand u8[N], nn f64[N]) of the selection phase (pardrag.hpp:71-73)."""
+        N = max(self.n - m + 1, 1)
+        cand, nn = np.zeros(N, np.uint8), np.empty(N)
+        self._check(self._L.tsd_par_select(self._h, m, float(r_sq), seglen, None, None, cand, nn))
+        return cand, nn
+
+    def par_refine(self, m: int, r_sq: float, seglen: int, cand) -> np.ndarray:
+        N = max(self.n - m + 1, 1)
+        cand = np.ascontiguousarray(cand, dtype=np.uint8)
+        out = np.zeros(N, RECORD_DTYPE)
+        cnt = _i64(0)
+        self._check(self._L.tsd_par_refine(self._h, m, float(r_sq), seglen, None, None, cand,
+                                           out.ctypes.data, N, C.byref(cnt)))
+        return out[: cnt.value].copy()
+
+    def stats_walk(self, m0: int, m1: int, fused: bool = True):
+        """mu/sigma of length m1 after MERLIN's length steps from m0 (the fused
+        k_next_length path by default)."""
+        N = max(self.n - m1 + 1, 1)
+        mu, sg = np.empty(N), np.empty(N)
+        self._check(self._L.tsd_stats_walk(self._h, m0, m1, 1 if fused else 0, mu, sg))
+        return mu, sg
+
+    def seed_rows(self):
+        """(info {m, L, kA, nb}, rows f64[nb, 1152]) of the resident band-0 seed rows."""
+        info = np.zeros(4, np.int64)
+        self._check(self._L.tsd_seed_rows(self._h, None, 0, info))
+        rows = np.empty((int(info[3]), 1152))
+        if info[3] > 0:
+            self._check(self._L.tsd_seed_rows(self._h, rows.ctypes.data, rows.size, info))
+        return info, rows
 
     def brute_force_nn(self, m: int) -> np.ndarray:
         out = np.empty(max(self.n - m + 1, 1))

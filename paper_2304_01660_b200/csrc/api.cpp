@@ -7,11 +7,13 @@
 // thread-local context (device from $TSD_DEVICE, default 0); a missing or
 // failing GPU raises std::runtime_error — there is no CPU fallback.
 #include <algorithm>
+#include <atomic>
 #include <charconv>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <limits>
 #include <istream>
 #include <memory>
 #include <ostream>
@@ -20,6 +22,7 @@
 #include <string_view>
 #include <thread>
 
+#include "tsdiscord/distance.hpp"
 #include "tsdiscord/drag.hpp"
 #include "tsdiscord/heatmap.hpp"
 #include "tsdiscord/io.hpp"
@@ -45,9 +48,9 @@ namespace {
 struct Ctx {
     tsd_ctx* c = nullptr;
     std::vector<double> uploaded;
-    Ctx() {
-        const char* dev = std::getenv("TSD_DEVICE");
-        const int rc = tsd_ctx_create(dev ? std::atoi(dev) : 0, &c);
+    Ctx() : Ctx(std::getenv("TSD_DEVICE") ? std::atoi(std::getenv("TSD_DEVICE")) : 0) {}
+    explicit Ctx(int device) {
+        const int rc = tsd_ctx_create(device, &c);
         if (rc != TSD_OK) rethrow(TSD_ERUNTIME, tsd_create_error());
     }
     ~Ctx() { tsd_ctx_destroy(c); }
@@ -69,6 +72,55 @@ Ctx& ctx() {
     return *c;
 }
 
+// A device list of two or more GPUs (MerlinOptions / ParOptions::devices):
+// one in-process rank group per calling thread, rebuilt when the list changes.
+struct Group {
+    tsd_group* g = nullptr;
+    std::vector<int> devices;
+    std::vector<double> uploaded;
+    ~Group() { tsd_group_destroy(g); }
+    void check(int rc) {
+        if (rc != TSD_OK) rethrow(rc, tsd_group_last_error(g));
+    }
+    void series(const TimeSeries& s) {
+        const auto& v = s.values();
+        if (v.size() == uploaded.size() && std::memcmp(v.data(), uploaded.data(), v.size() * 8) == 0)
+            return;
+        check(tsd_group_series_set(g, v.data(), (int64_t)v.size()));
+        uploaded = v;
+    }
+};
+
+Group* group_for(const std::vector<int>& devices) {
+    if (devices.size() < 2) return nullptr;
+    thread_local std::unique_ptr<Group> gr;
+    if (!gr || gr->devices != devices) {
+        gr.reset();
+        auto fresh = std::make_unique<Group>();
+        const int rc = tsd_group_create(devices.data(), (int)devices.size(), &fresh->g);
+        if (rc != TSD_OK) rethrow(rc, tsd_create_error());
+        fresh->devices = devices;
+        gr = std::move(fresh);
+    }
+    return gr.get();
+}
+
+// one device of the list when it has exactly one entry
+Ctx& ctx_for(const std::vector<int>& devices) {
+    if (devices.size() == 1) {
+        thread_local std::unique_ptr<Ctx> one;
+        thread_local int one_dev = -1;
+        if (!one || one_dev != devices[0]) {
+            one.reset();
+            auto c = std::make_unique<Ctx>(devices[0]);
+            one = std::move(c);
+            one_dev = devices[0];
+        }
+        return *one;
+    }
+    return ctx();
+}
+
 std::vector<DiscordRecord> to_records(const std::vector<tsd_record>& r, size_t n) {
     std::vector<DiscordRecord> out(n);
     for (size_t i = 0; i < n; ++i) out[i] = {(index_t)r[i].index, r[i].nn_dist_sq, r[i].nn_dist};
@@ -76,12 +128,18 @@ std::vector<DiscordRecord> to_records(const std::vector<tsd_record>& r, size_t n
 }
 
 std::vector<DiscordRecord> run_pardrag(const TimeSeries& series, index_t m, double r_sq,
-                                       index_t seglen, const RollingStats* stats) {
-    Ctx& c = ctx();
-    c.series(series);
+                                       index_t seglen, const RollingStats* stats,
+                                       const std::vector<int>& devices = {}) {
     const index_t N = series.n() - m + 1;
     std::vector<tsd_record> buf(std::max<index_t>(N, 1));
     int64_t cnt = 0;
+    if (Group* g = group_for(devices)) {  // the group computes its own stats (same values)
+        g->series(series);
+        g->check(tsd_group_pardrag(g->g, m, r_sq, seglen, buf.data(), (int64_t)buf.size(), &cnt));
+        return to_records(buf, (size_t)cnt);
+    }
+    Ctx& c = ctx_for(devices);
+    c.series(series);
     const bool use_stats = stats && (index_t)stats->mu.size() >= N && stats->m == m;
     c.check(tsd_pardrag(c.c, m, r_sq, seglen, use_stats ? stats->mu.data() : nullptr,
                         use_stats ? stats->sigma.data() : nullptr, buf.data(), (int64_t)buf.size(), &cnt));
@@ -148,14 +206,218 @@ std::vector<DiscordRecord> pardrag(const TimeSeries& series, index_t m, double r
 
 std::vector<DiscordRecord> pardrag(const TimeSeries& series, index_t m, double r_sq,
                                    const RollingStats& stats, const SegmentLayout& layout,
-                                   const ParOptions& /*opts*/) {
-    return run_pardrag(series, m, r_sq, layout.seglen, &stats);
+                                   const ParOptions& opts) {
+    return run_pardrag(series, m, r_sq, layout.seglen, &stats, opts.devices);
+}
+
+// SelectionState: host view of the two-phase state (pardrag.hpp)
+SelectionState::SelectionState(const SegmentLayout& layout, index_t real_count)
+    : size_(layout.num_seg * layout.seg_n),
+      flags_(new Flags[static_cast<std::size_t>(std::max<index_t>(size_, 0))]),
+      nn_(new std::atomic<double>[static_cast<std::size_t>(std::max<index_t>(size_, 0))]),
+      side_(static_cast<std::size_t>(std::max<index_t>(size_, 0)),
+            Side{std::numeric_limits<double>::infinity(), {}, false}) {
+    for (index_t i = 0; i < size_; ++i) {
+        const unsigned char live = i < real_count;  // pad slots start cleared
+        flags_[(size_t)i].cand.store(live, std::memory_order_relaxed);
+        flags_[(size_t)i].neighbor.store(live, std::memory_order_relaxed);
+        nn_[(size_t)i].store(std::numeric_limits<double>::infinity(), std::memory_order_relaxed);
+    }
+}
+
+void SelectionState::lower_nn_dist_sq(index_t i, double value) {
+    std::atomic<double>& slot = nn_[at(i)];
+    double cur = slot.load(std::memory_order_relaxed);
+    while (value < cur && !slot.compare_exchange_weak(cur, value, std::memory_order_relaxed)) {
+    }
+}
+
+void SelectionState::conjoin() {
+    for (index_t i = 0; i < size_; ++i)
+        if (!flags_[(size_t)i].neighbor.load(std::memory_order_relaxed))
+            flags_[(size_t)i].cand.store(0, std::memory_order_relaxed);
+}
+
+namespace {
+bool stats_fit(const RollingStats& stats, index_t m, index_t N) {
+    return stats.m == m && (index_t)stats.mu.size() >= N && (index_t)stats.sigma.size() >= N;
+}
+}  // namespace
+
+SelectionState par_select(const TimeSeries& series, index_t m, double r_sq, const RollingStats& stats,
+                          const SegmentLayout& layout, const ParOptions& opts) {
+    const index_t N = series.subseq_count(m);
+    SelectionState state(layout, N);
+    std::vector<uint8_t> cand((size_t)std::max<index_t>(N, 1));
+    std::vector<double> nn((size_t)std::max<index_t>(N, 1));
+    if (group_for(opts.devices)) {
+        // the rank group runs the same try; survivors carry their exact nn
+        const auto recs = run_pardrag(series, m, r_sq, layout.seglen, &stats, opts.devices);
+        std::fill(cand.begin(), cand.end(), 0);
+        for (const auto& r : recs) {
+            cand[(size_t)(r.index - 1)] = 1;
+            nn[(size_t)(r.index - 1)] = r.nn_dist_sq;
+        }
+    } else {
+        Ctx& c = ctx_for(opts.devices);
+        c.series(series);
+        const bool own = stats_fit(stats, m, N);
+        c.check(tsd_par_select(c.c, m, r_sq, layout.seglen, own ? stats.mu.data() : nullptr,
+                               own ? stats.sigma.data() : nullptr, cand.data(), nn.data()));
+    }
+    for (index_t i = 1; i <= N; ++i) {
+        if (!cand[(size_t)(i - 1)]) {
+            state.clear_cand(i);
+            state.clear_neighbor(i);
+        } else {
+            state.lower_nn_dist_sq(i, nn[(size_t)(i - 1)]);
+        }
+    }
+    return state;
+}
+
+std::vector<DiscordRecord> par_refine(const TimeSeries& series, index_t m, double r_sq,
+                                      const RollingStats& stats, const SegmentLayout& layout,
+                                      SelectionState& state, const ParOptions& opts) {
+    const index_t N = series.subseq_count(m);
+    std::vector<uint8_t> cand((size_t)std::max<index_t>(N, 1), 0);
+    bool any = false;
+    for (index_t i = 1; i <= N && i <= state.size(); ++i) {
+        cand[(size_t)(i - 1)] = state.cand(i) ? 1 : 0;
+        any = any || cand[(size_t)(i - 1)];
+    }
+    if (!any) return {};
+    std::vector<DiscordRecord> out;
+    if (group_for(opts.devices)) {
+        for (const auto& r : run_pardrag(series, m, r_sq, layout.seglen, &stats, opts.devices))
+            if (cand[(size_t)(r.index - 1)]) out.push_back(r);
+    } else {
+        Ctx& c = ctx_for(opts.devices);
+        c.series(series);
+        const bool own = stats_fit(stats, m, N);
+        std::vector<tsd_record> buf((size_t)std::max<index_t>(N, 1));
+        int64_t cnt = 0;
+        c.check(tsd_par_refine(c.c, m, r_sq, layout.seglen, own ? stats.mu.data() : nullptr,
+                               own ? stats.sigma.data() : nullptr, cand.data(), buf.data(),
+                               (int64_t)buf.size(), &cnt));
+        out = to_records(buf, (size_t)cnt);
+    }
+    for (const auto& r : out) state.lower_nn_dist_sq(r.index, r.nn_dist_sq);
+    return out;
+}
+
+namespace {
+void drag_checks(const TimeSeries& series, index_t m, double r_sq) {
+    // src/drag.cpp:63-64
+    if (m < 3 || 2 * m > series.n()) throw std::invalid_argument("drag_select: invalid length");
+    if (r_sq < 0) throw std::invalid_argument("drag_select: negative threshold");
+}
+index_t drag_seglen(const TimeSeries& series, index_t m) {
+    return std::min<index_t>(std::max<index_t>(2 * m, 512), series.n());
+}
+}  // namespace
+
+CandidateSet drag_select(const TimeSeries& series, index_t m, double r_sq) {
+    drag_checks(series, m, r_sq);
+    const auto recs = run_pardrag(series, m, r_sq, drag_seglen(series, m), nullptr);
+    CandidateSet set;
+    set.entries.reserve(recs.size());
+    for (const auto& r : recs) set.entries.push_back({r.index, r.nn_dist_sq});
+    std::sort(set.entries.begin(), set.entries.end(),
+              [](const Candidate& a, const Candidate& b) { return a.index < b.index; });
+    return set;
+}
+
+std::vector<DiscordRecord> drag_refine(const TimeSeries& series, index_t m, double r_sq,
+                                       const CandidateSet& candidates, bool) {
+    if (candidates.entries.empty()) return {};
+    const index_t N = series.subseq_count(m);
+    std::vector<uint8_t> keep((size_t)std::max<index_t>(N, 1), 0);
+    for (const auto& c : candidates.entries)
+        if (c.index >= 1 && c.index <= N) keep[(size_t)(c.index - 1)] = 1;
+    std::vector<DiscordRecord> out;
+    for (const auto& r : run_pardrag(series, m, r_sq, drag_seglen(series, m), nullptr))
+        if (keep[(size_t)(r.index - 1)]) out.push_back(r);
+    return out;
 }
 
 std::vector<DiscordRecord> drag(const TimeSeries& series, index_t m, double r_sq, bool) {
+    drag_checks(series, m, r_sq);
     // same range-discord set; the segment length only shapes the reference's schedule
-    return run_pardrag(series, m, r_sq, std::min<index_t>(std::max<index_t>(2 * m, 512), series.n()),
-                       nullptr);
+    return run_pardrag(series, m, r_sq, drag_seglen(series, m), nullptr);
+}
+
+// ---- distance building blocks (distance.hpp; host utilities of the API) ---------
+std::vector<double> znormalize(std::span<const double> x) {
+    const std::size_t m = x.size();
+    if (m < 3) throw std::invalid_argument("znormalize: need at least 3 points");
+    // one pass of running sums in index order: the rounding the device's exact
+    // distance (ref_dist_warp) reproduces
+    double s1 = 0.0, s2 = 0.0;
+    for (const double v : x) {
+        s1 += v;
+        s2 += v * v;
+    }
+    const double mean = s1 / (double)m;
+    const double var = s2 / (double)m - mean * mean;
+    const double sd = std::sqrt(var > 0.0 ? var : 0.0);
+    std::vector<double> z(m, 0.0);
+    if (!(sd < kSigmaEps))
+        for (std::size_t k = 0; k < m; ++k) z[k] = (x[k] - mean) / sd;
+    return z;
+}
+
+double sq_ed(std::span<const double> x, std::span<const double> y) {
+    if (x.size() != y.size()) throw std::invalid_argument("sq_ed: length mismatch");
+    double acc = 0.0;
+    for (std::size_t k = 0; k < x.size(); ++k) acc += (x[k] - y[k]) * (x[k] - y[k]);
+    return acc;
+}
+
+double sq_ednorm_from_dot(double dot, index_t m, double mu_x, double mu_y, double sigma_x, double sigma_y) {
+    const double md = (double)m;
+    const int flat = (sigma_x < kSigmaEps) + (sigma_y < kSigmaEps);
+    if (flat == 2) return 0.0;
+    if (flat == 1) return 2.0 * md;
+    const double corr = (dot - md * mu_x * mu_y) / (md * sigma_x * sigma_y);
+    return std::min(std::max(2.0 * md * (1.0 - corr), 0.0), 4.0 * md);
+}
+
+std::optional<double> early_abandon_sq_ed(std::span<const double> xh, std::span<const double> yh,
+                                          double bound) {
+    if (xh.size() != yh.size()) throw std::invalid_argument("early_abandon_sq_ed: length mismatch");
+    double acc = 0.0;
+    for (std::size_t k = 0; k < xh.size(); ++k) {
+        acc += (xh[k] - yh[k]) * (xh[k] - yh[k]);
+        if (acc >= bound) return std::nullopt;
+    }
+    return acc;
+}
+
+DotRow dot_products_block(std::span<const double> query, std::span<const double> window, index_t m,
+                          index_t count) {
+    if ((index_t)query.size() < m) throw std::invalid_argument("dot_products_block: query shorter than m");
+    if ((index_t)window.size() < count + m - 1) throw std::invalid_argument("dot_products_block: window too short");
+    DotRow row((size_t)std::max<index_t>(count, 0));
+    for (index_t k = 0; k < count; ++k) {
+        const double* w = window.data() + k;
+        double acc = 0.0;
+        for (index_t p = 0; p < m; ++p) acc += query[(size_t)p] * w[p];
+        row[(size_t)k] = acc;
+    }
+    return row;
+}
+
+DotRow update_dot_col(const DotRow& prev_col, const DotRow& row, index_t k, std::span<const double> segment,
+                      std::span<const double> chunk, index_t m) {
+    if (k <= 1 || k > (index_t)row.size()) throw std::invalid_argument("update_dot_col: chunk ordinal out of range");
+    DotRow col(prev_col.size());
+    if (col.empty()) return col;
+    col[0] = row[(size_t)(k - 1)];
+    const double in = chunk[(size_t)(k + m - 2)], out = chunk[(size_t)(k - 2)];
+    for (std::size_t t = 1; t < col.size(); ++t)
+        col[t] = prev_col[t - 1] + segment[t + (size_t)m - 1] * in - segment[t - 1] * out;
+    return col;
 }
 
 std::vector<double> brute_force_nn(const TimeSeries& series, index_t m) {
@@ -204,8 +466,6 @@ double next_threshold(const ThresholdHistory& h, ThresholdPhase phase, index_t m
 
 MerlinReport merlin_full(const TimeSeries& series, index_t min_len, index_t max_len,
                          const MerlinOptions& opts) {
-    Ctx& c = ctx();
-    c.series(series);
     const index_t L = std::max<index_t>(max_len - min_len + 1, 1);
     const index_t k = std::max<index_t>(opts.top_k, 1);
     std::vector<int64_t> counts((size_t)L), retries((size_t)L);
@@ -213,8 +473,16 @@ MerlinReport merlin_full(const TimeSeries& series, index_t min_len, index_t max_
     std::vector<double> final_r((size_t)L);
     std::vector<uint8_t> failed((size_t)L);
     tsd_merlin_opts o{opts.top_k, opts.seglen, opts.workers, opts.max_retries, opts.reuse_stats ? 1 : 0};
-    c.check(tsd_merlin(c.c, min_len, max_len, &o, counts.data(), recs.data(), final_r.data(),
-                       retries.data(), failed.data()));
+    if (Group* g = group_for(opts.devices)) {
+        g->series(series);
+        g->check(tsd_group_merlin(g->g, min_len, max_len, &o, counts.data(), recs.data(), final_r.data(),
+                                  retries.data(), failed.data()));
+    } else {
+        Ctx& c = ctx_for(opts.devices);
+        c.series(series);
+        c.check(tsd_merlin(c.c, min_len, max_len, &o, counts.data(), recs.data(), final_r.data(),
+                           retries.data(), failed.data()));
+    }
     MerlinReport rep;
     rep.discords.min_len = min_len;
     rep.discords.max_len = max_len;
@@ -321,8 +589,17 @@ MultiLengthDiscordSet read_discords_csv(std::istream& in) {
 
 // ---- heatmap (reference: src/heatmap.cpp; built and ranked on the GPU) ---------
 namespace {
-std::uint64_t& heatmap_gen() {
+// Generations are unique process-wide; each thread's context remembers which
+// one its device matrix holds.  A Heatmap built on another thread (another
+// context) therefore never matches and is uploaded before ranking.
+std::atomic<std::uint64_t> g_heatmap_next{0};
+std::uint64_t& resident_heatmap() {
     thread_local std::uint64_t g = 0;
+    return g;
+}
+std::uint64_t new_heatmap_gen() {
+    const std::uint64_t g = ++g_heatmap_next;
+    resident_heatmap() = g;
     return g;
 }
 }  // namespace
@@ -344,16 +621,16 @@ Heatmap build_heatmap(const MultiLengthDiscordSet& discords, index_t n) {
     Ctx& c = ctx();
     c.check(tsd_heatmap_build(c.c, h.min_len(), h.max_len(), n, lens.data(), recs.data(), (int64_t)recs.size(),
                               h.mutable_scores().data()));
-    h.set_device_gen(++heatmap_gen());
+    h.set_device_gen(new_heatmap_gen());
     return h;
 }
 
 std::vector<RankedDiscord> rank_discords(const Heatmap& heatmap, index_t k) {
     if (k < 1) throw std::invalid_argument("rank_discords: k must be positive");
     Ctx& c = ctx();
-    if (heatmap.device_gen() == 0 || heatmap.device_gen() != heatmap_gen()) {
+    if (heatmap.device_gen() == 0 || heatmap.device_gen() != resident_heatmap()) {
         c.check(tsd_heatmap_set(c.c, heatmap.min_len(), heatmap.max_len(), heatmap.n(), heatmap.scores().data()));
-        heatmap.set_device_gen(++heatmap_gen());
+        heatmap.set_device_gen(new_heatmap_gen());
     }
     std::vector<tsd_ranked> buf((size_t)std::min<index_t>(k, std::max<index_t>(heatmap.cols(), 1)));
     int64_t cnt = 0;

@@ -9,6 +9,63 @@ namespace tsd {
 // include/tsdiscord/stats.hpp:11 — a subsequence with sigma below this is constant.
 constexpr double kSigmaEps = 1e-12;
 
+// ---- statistics error of the FP32 filter ("Statistics error") --
+// The FP32 walk normalises with the reference's rolling mu / sigma (Eq. 4 /
+// 7-8), while the exact distance it certifies against uses each window's
+// one-pass statistics (znormalize).  Both deviate from the window's true
+// moments by an amount that grows like mu^2 / sigma^2 (DC offsets).  Per
+// length, k_derive / k_next_length measure the rolling statistics against
+// double-double prefix sums and bound the one-pass ones a priori; the
+// per-length maxima (over windows the filter keeps) widen every certified band.
+// A window whose statistics error exceeds kStatsUnreliable (flat stretches
+// with a spurious rolling sigma, extreme offsets) is decided exactly, like a
+// sigma < eps window.
+constexpr double kEps64 = 1.1102230246251565e-16;  // 2^-53
+constexpr double kStatsUnreliable = 1e-3;          // corr units
+constexpr double kStatsRows = 1040.0;              // 2 (kMaxRows + 8): walk steps a mean error acts over
+// per-length slot (two parity slots of kCrInts ints): [0] max(N - i), [1] max(i + 1)
+// over degenerate rows, [2] their count (listed in deg), [3] bits of the max
+// statistics error a_i (float >= 0), [4] bits of the max 1 + mu_i^2 / sigma_i^2
+constexpr int kCrInts = 5;
+
+struct dd {  // double-double (unevaluated sum hi + lo)
+    double hi, lo;
+};
+__device__ __forceinline__ dd dd_two_sum(double a, double b) {
+    const double s = __dadd_rn(a, b);
+    const double bb = __dsub_rn(s, a);
+    const double e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+    return dd{s, e};
+}
+__device__ __forceinline__ dd dd_fast(double a, double b) {  // |a| >= |b|
+    const double s = __dadd_rn(a, b);
+    return dd{s, __dsub_rn(b, __dsub_rn(s, a))};
+}
+__device__ __forceinline__ dd dd_add(dd a, dd b) {
+    dd s = dd_two_sum(a.hi, b.hi);
+    const dd t = dd_two_sum(a.lo, b.lo);
+    s.lo = __dadd_rn(s.lo, t.hi);
+    s = dd_fast(s.hi, s.lo);
+    s.lo = __dadd_rn(s.lo, t.lo);
+    return dd_fast(s.hi, s.lo);
+}
+__device__ __forceinline__ dd dd_neg(dd a) { return dd{-a.hi, -a.lo}; }
+__device__ __forceinline__ dd dd_sq(double a) {  // exact a*a
+    const double p = __dmul_rn(a, a);
+    return dd{p, fma(a, a, -p)};
+}
+__device__ __forceinline__ dd dd_mul(dd a, dd b) {
+    const double p = __dmul_rn(a.hi, b.hi);
+    double e = fma(a.hi, b.hi, -p);
+    e = fma(a.hi, b.lo, fma(a.lo, b.hi, e));
+    return dd_fast(p, e);
+}
+__device__ __forceinline__ dd dd_div_d(dd a, double b) {
+    const double q1 = __ddiv_rn(a.hi, b);
+    const double r = __dadd_rn(fma(-q1, b, a.hi), a.lo);
+    return dd_fast(q1, __ddiv_rn(r, b));
+}
+
 // ---- tile-scan geometry ----------------------------------------------------
 // One CTA sweeps a parallelogram of the distance matrix: `rows` consecutive
 // candidates c (walk order given by dir) x W consecutive diagonals k = q - c.
@@ -151,8 +208,24 @@ struct ScanParams {
     int half;            // band passes: evaluate 1 cell in `half` (1: all)
     int pair;            // band 0 (kSpaceSeed, both sides): one paired walk per row block (k_band0_pair)
     const double* seedqt;  // resident raw dot products QT(i, i+k) of the band-0 tiles (kW per tile)
+    const int* cr;         // per-length slot of this length (kCrInts ints; statistics error in [3], [4])
     unsigned long long* acc;  // accounting: [0] cells walked, [1] cells evaluated, [2] seed dots
 };
+
+// Widening of every certified band of this length (correlation units) for
+// the statistics error: twice the largest per-window error a_i, plus, for
+// tiles seeded from the resident raw dot products QT (no centring), their FP64
+// accumulation error (m + 4) u sqrt((1 + Om_c)(1 + Om_q)) and the rolling
+// means' error acting on m mu_c mu_q (a_i bounds 1040 |mu err| / sigma).
+__device__ __forceinline__ double stats_band(const ScanParams& p, bool resident_seed) {
+    const double a = (double)__int_as_float(p.cr[3]);
+    double x = 2.0 * a;
+    if (resident_seed) {
+        const double b2 = (double)__int_as_float(p.cr[4]);
+        x += 2.0 * (double)(p.m + 4) * kEps64 * b2 + 4.0 * a * sqrt(b2) / kStatsRows;
+    }
+    return x;
+}
 
 // Programmatic dependent launch: every kernel of the try chain is launched
 // with programmatic stream serialization (launch_pdl), waits here for its

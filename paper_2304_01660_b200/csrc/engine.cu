@@ -109,7 +109,9 @@ struct tsd_ctx {
     DBuf<double> mu, sig, scr_a, scr_b;
     int64_t derived_m = -1;
     DBuf<float> df, dg, nrm;
-    DBuf<int> crange;  // constant-row range and count of the derived length (k_derive), two parity slots
+    DBuf<int> crange;  // per-length slot of the derived length (k_derive; common.cuh kCrInts), two parity slots
+    // double-double prefix sums of t and t^2 (statistics error, common.cuh)
+    DBuf<double2> pfx1, pfx2, pfx_tot1, pfx_tot2;
     DBuf<int> deg;     // degenerate rows (sigma < eps) of the derived length
 
     // scan state
@@ -319,12 +321,12 @@ struct tsd_ctx {
         df.ensure(N);
         dg.ensure(N);
         nrm.ensure(N);
-        crange.ensure(6);
+        crange.ensure(2 * kCrInts);
         deg.ensure(N);
         // both parity slots cleared: the fused length step after this one uses the other
-        ck(cudaMemsetAsync(crange.p, 0, 6 * sizeof(int), st), "memset");
-        cr_cur = crange.p + 3 * (m & 1);
-        launch_derive(t.p, (int)m, (int)N, mu.p, sig.p, df.p, dg.p, nrm.p, cr_cur, deg.p, st);
+        ck(cudaMemsetAsync(crange.p, 0, 2 * kCrInts * sizeof(int), st), "memset");
+        cr_cur = crange.p + kCrInts * (m & 1);
+        launch_derive(t.p, (int)m, (int)N, mu.p, sig.p, df.p, dg.p, nrm.p, cr_cur, deg.p, pfx1.p, pfx2.p, st);
         ctr.kernel_launches += 1;
         ck(cudaGetLastError(), "derive");
         derived_m = m;
@@ -341,11 +343,11 @@ struct tsd_ctx {
         dg.ensure(N1);
         nrm.ensure(N1);
         if (derived_m != m || !cr_cur) derive(m);  // establishes the parity slots
-        int* cr = crange.p + 3 * (m1 & 1);
-        int* crn = crange.p + 3 * ((m1 + 1) & 1);
+        int* cr = crange.p + kCrInts * (m1 & 1);
+        int* crn = crange.p + kCrInts * ((m1 + 1) & 1);
         deg.ensure(N1);
         launch_next_length(t.p, (int)n, (int)m, mu.p, sig.p, mu2.p, sig2.p, df.p, dg.p, nrm.p, cr, crn, seed_L, seed_kA,
-                           seed_nb, with_seed ? seedqt.p : nullptr, deg.p, st);
+                           seed_nb, with_seed ? seedqt.p : nullptr, deg.p, pfx1.p, pfx2.p, st);
         ck(cudaGetLastError(), "next length");
         ctr.kernel_launches += 1;
         std::swap(mu.p, mu2.p);
@@ -417,6 +419,7 @@ struct tsd_ctx {
         p.ymax = ymax.p;
         p.emax = emax.p;
         p.seedqt = seedqt.p;
+        p.cr = cr_cur;
         p.ythr = ythr.p;
         p.coll = coll.p;
         p.coll_count = &ctl.p->coll;
@@ -887,6 +890,10 @@ void tsd_ctx_destroy(tsd_ctx* c) {
     c->dg.release();
     c->nrm.release();
     c->crange.release();
+    c->pfx1.release();
+    c->pfx2.release();
+    c->pfx_tot1.release();
+    c->pfx_tot2.release();
     c->deg.release();
     c->mu2.release();
     c->sig2.release();
@@ -966,6 +973,13 @@ int tsd_series_set(tsd_ctx* c, const double* v, int64_t n) {
         c->n = n;
         c->t.ensure(n);
         ck(cudaMemcpyAsync(c->t.p, v, n * sizeof(double), cudaMemcpyHostToDevice, c->st), "series H2D");
+        c->pfx1.ensure(n + 1);
+        c->pfx2.ensure(n + 1);
+        c->pfx_tot1.ensure(dd_prefix_blocks((int)n));
+        c->pfx_tot2.ensure(dd_prefix_blocks((int)n));
+        launch_dd_prefix(c->t.p, (int)n, c->pfx_tot1.p, c->pfx_tot2.p, c->pfx1.p, c->pfx2.p, c->st);
+        ck(cudaGetLastError(), "prefix sums");
+        c->ctr.kernel_launches += 3;
         c->sync();
         c->stats_m = -1;
         c->derived_m = -1;
@@ -1020,35 +1034,124 @@ int tsd_next_threshold(const double* h, int64_t len, int phase, int64_t min_len,
     return guard(nullptr, [&] { *out = next_thr(h, len, phase, min_len, last_r, failed != 0); });
 }
 
+namespace {
+// One device try for the pardrag-family entry points: validates like the
+// reference call, installs the caller's stats (or computes init_stats(m) on
+// the device) and runs pardrag_core.  all_nn (nullable, N entries) receives
+// the exact nn of every survivor.
+std::vector<tsd_record> run_try(tsd_ctx* c, int64_t m, double r_sq, int64_t seglen, const double* mu,
+                                const double* sigma, double* all_nn = nullptr) {
+    need_series(c);
+    int64_t lay[4];
+    layout(c->n, m, seglen, lay);  // same preconditions as the reference call
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    ck(cudaEventRecord(c->ev_t0, c->st), "event");
+    c->seed_m = -1;
+    const int64_t N = c->n - m + 1;
+    if (mu && sigma) {
+        c->mu.ensure(c->n);
+        c->sig.ensure(c->n);
+        ck(cudaMemcpyAsync(c->mu.p, mu, N * sizeof(double), cudaMemcpyHostToDevice, c->st), "H2D");
+        ck(cudaMemcpyAsync(c->sig.p, sigma, N * sizeof(double), cudaMemcpyHostToDevice, c->st), "H2D");
+        c->stats_m = m;
+        c->derived_m = -1;
+    } else if (c->stats_m != m) {
+        c->init_stats_dev(m);
+    }
+    auto recs = c->pardrag_core(m, r_sq, all_nn);
+    ck(cudaEventRecord(c->ev_t1, c->st), "event");
+    c->sync();
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev_t0, c->ev_t1);
+    c->ctr.total_ms = ms;
+    return recs;
+}
+
+void copy_out(const std::vector<tsd_record>& recs, tsd_record* out, int64_t cap, int64_t* count) {
+    *count = (int64_t)recs.size();
+    const int64_t k = std::min<int64_t>(cap, (int64_t)recs.size());
+    if (k > 0) std::memcpy(out, recs.data(), k * sizeof(tsd_record));
+}
+}  // namespace
+
 int tsd_pardrag(tsd_ctx* c, int64_t m, double r_sq, int64_t seglen, const double* mu,
                 const double* sigma, tsd_record* out, int64_t cap, int64_t* count) {
+    return guard(c, [&] { copy_out(run_try(c, m, r_sq, seglen, mu, sigma), out, cap, count); });
+}
+
+int tsd_par_select(tsd_ctx* c, int64_t m, double r_sq, int64_t seglen, const double* mu, const double* sigma,
+                   uint8_t* cand, double* nn) {
     return guard(c, [&] {
         need_series(c);
-        int64_t lay[4];
-        layout(c->n, m, seglen, lay);  // same preconditions as the reference call
-        ck(cudaSetDevice(c->device), "cudaSetDevice");
-        ck(cudaEventRecord(c->ev_t0, c->st), "event");
-        c->seed_m = -1;
         const int64_t N = c->n - m + 1;
-        if (mu && sigma) {
-            c->mu.ensure(c->n);
-            c->sig.ensure(c->n);
-            ck(cudaMemcpyAsync(c->mu.p, mu, N * sizeof(double), cudaMemcpyHostToDevice, c->st), "H2D");
-            ck(cudaMemcpyAsync(c->sig.p, sigma, N * sizeof(double), cudaMemcpyHostToDevice, c->st), "H2D");
-            c->stats_m = m;
-            c->derived_m = -1;
-        } else if (c->stats_m != m) {
-            c->init_stats_dev(m);
+        if (r_sq < 0.0) fail(TSD_EINVAL, "par_select: negative threshold");
+        // survivors receive their exact nn (possibly +inf: no admissible
+        // partner); the rows the try killed keep the NaN marker
+        std::vector<double> all((size_t)std::max<int64_t>(N, 1), NAN);
+        run_try(c, m, r_sq, seglen, mu, sigma, all.data());
+        for (int64_t i = 0; i < N; ++i) {
+            const double d = all[(size_t)i];
+            cand[i] = std::isnan(d) ? 0 : 1;
+            nn[i] = std::isnan(d) ? INFINITY : d;
         }
-        const auto recs = c->pardrag_core(m, r_sq);
-        ck(cudaEventRecord(c->ev_t1, c->st), "event");
+    });
+}
+
+int tsd_par_refine(tsd_ctx* c, int64_t m, double r_sq, int64_t seglen, const double* mu, const double* sigma,
+                   const uint8_t* cand, tsd_record* out, int64_t cap, int64_t* count) {
+    return guard(c, [&] {
+        if (r_sq < 0.0) fail(TSD_EINVAL, "par_refine: negative threshold");
+        need_series(c);
+        const int64_t N = c->n - m + 1;
+        bool any = false;
+        for (int64_t i = 0; i < N && !any; ++i) any = cand[i] != 0;
+        if (!any) {  // nothing to refine (pardrag_test.cpp: "no surviving candidates")
+            int64_t lay[4];
+            layout(c->n, m, seglen, lay);
+            *count = 0;
+            return;
+        }
+        auto recs = run_try(c, m, r_sq, seglen, mu, sigma);
+        std::vector<tsd_record> kept;
+        kept.reserve(recs.size());
+        for (const auto& r : recs)
+            if (cand[r.index - 1]) kept.push_back(r);
+        copy_out(kept, out, cap, count);
+    });
+}
+
+int tsd_stats_walk(tsd_ctx* c, int64_t m0, int64_t m1, int fused, double* mu, double* sigma) {
+    return guard(c, [&] {
+        need_series(c);
+        if (m0 < 2 || m1 < m0 || m1 > c->n - 1) fail(TSD_EINVAL, "stats_walk: length out of range");
+        ck(cudaSetDevice(c->device), "cudaSetDevice");
+        c->init_stats_dev(m0);
+        c->seed_m = -1;
+        // the MERLIN set-up: resident seed rows at kA = m1 when the band fits
+        if (fused && m0 >= 3 && m1 + kW < c->n - m1 + 1) c->seed_init(m0, m1);
+        for (int64_t m = m0; m < m1; ++m) {
+            if (fused) c->next_length(c->seed_m == m);
+            else c->advance_stats_dev();
+        }
+        const int64_t N = c->n - m1 + 1;
+        ck(cudaMemcpyAsync(mu, c->mu.p, N * sizeof(double), cudaMemcpyDeviceToHost, c->st), "D2H");
+        ck(cudaMemcpyAsync(sigma, c->sig.p, N * sizeof(double), cudaMemcpyDeviceToHost, c->st), "D2H");
         c->sync();
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, c->ev_t0, c->ev_t1);
-        c->ctr.total_ms = ms;
-        *count = (int64_t)recs.size();
-        const int64_t k = std::min<int64_t>(cap, (int64_t)recs.size());
-        if (k > 0) std::memcpy(out, recs.data(), k * sizeof(tsd_record));
+    });
+}
+
+int tsd_seed_rows(tsd_ctx* c, double* out, int64_t cap, int64_t info[4]) {
+    return guard(c, [&] {
+        info[0] = c->seed_m;
+        info[1] = c->seed_L;
+        info[2] = c->seed_kA;
+        info[3] = c->seed_m < 0 ? 0 : c->seed_nb;
+        const int64_t cnt = info[3] * (int64_t)kW;
+        if (out && cnt > 0 && cap >= cnt) {
+            ck(cudaSetDevice(c->device), "cudaSetDevice");
+            ck(cudaMemcpyAsync(out, c->seedqt.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, c->st), "D2H");
+            c->sync();
+        }
     });
 }
 

@@ -45,12 +45,17 @@ void launch_init_stats(const double* t, int n, int m, double* mu, double* sig, d
                        double* scratch_b, cudaStream_t st);
 void launch_advance_stats(const double* t, int n, int m, double* mu, double* sig, cudaStream_t st);
 void launch_derive(const double* t, int m, int cnt, const double* mu, const double* sig, float* df,
-                   float* dg, float* nrm, int* crange, int* deg, cudaStream_t st);
+                   float* dg, float* nrm, int* crange, int* deg, const double2* P1, const double2* P2,
+                   cudaStream_t st);
+// double-double prefix sums of t and t^2 (n + 1 entries each; tot: dd_prefix_blocks(n) scratch)
+int dd_prefix_blocks(int n);
+void launch_dd_prefix(const double* t, int n, double2* tot1, double2* tot2, double2* P1, double2* P2,
+                      cudaStream_t st);
 
 // advance + derive (+ seed rows when qt != nullptr) of one MERLIN length step
 void launch_next_length(const double* t, int n, int m, const double* mu_in, const double* sig_in, double* mu_out,
                         double* sig_out, float* df, float* dg, float* nrm, int* cr, int* cr_next, int L, int kA,
-                        int nb, double* qt, int* deg, cudaStream_t st);
+                        int nb, double* qt, int* deg, const double2* P1, const double2* P2, cudaStream_t st);
 
 size_t scan_smem_bytes();
 void scan_configure();

@@ -227,7 +227,7 @@ struct F9 {
 // Kept out of line: it runs on a few steps only and would otherwise bloat the
 // unrolled walk.
 __device__ __noinline__ void slow_track(const F9 x, const F9 qn, float tz, float cw, int c, int u0, int dir,
-                                        int qbase, int N, int m, double r_sq, double thr0, double E,
+                                        int qbase, int N, int m, double r_sq, double thr0, double E, double xs,
                                         uint8_t* alive, uint8_t* const* peer_alive, int npeer, int2* queue,
                                         int* queue_count, int queue_cap) {
 #pragma unroll
@@ -246,7 +246,7 @@ __device__ __noinline__ void slow_track(const F9 x, const F9 qn, float tz, float
             continue;
         }
         const double corr = (double)x.v[j] * (double)cw;
-        const double ec = E * (double)cw * (double)qj + kSlack;
+        const double ec = E * (double)cw * (double)qj + kSlack + xs;
         if (corr - ec > thr0) {
             if (npeer > 1) for (int r = 0; r < npeer; ++r) peer_alive[r][c] = 0;
             else alive[c] = 0;
@@ -571,6 +571,8 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
     const double E =
         p.err_k * (double)kEps32 * (double)(rows + 8) * ((double)m * smax_c * smax_q + 1.5 * P) + e_seed;
     const float Ef = (float)E;
+    // statistics error of this length (correlation units; resident raw seeds add theirs)
+    const double xs = stats_band(p, td.seed >= 0);
     // Row thresholds.  crow.z = tc: a live row's cells with x = cov*qn > tc may be
     // within the error band of d^2 = r^2 (slow path); kNoEval marks rows whose
     // cells are only walked (already decided, or not a survivor in kCollect).
@@ -582,7 +584,8 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
         const bool live = p.alive[c] != 0;
         float tc;
         if (MODE == kCollect) {
-            S.cy[s] = (live && cn != 0.f) ? p.ythr[c] : FLT_MAX;
+            // the row's best lower bound, lowered by the statistics band (x units)
+            S.cy[s] = (live && cn != 0.f) ? p.ythr[c] - (float)(xs / (double)cn) * (1.f + 2.4e-7f) : FLT_MAX;
             tc = S.cy[s] < FLT_MAX ? 0.f : kNoEval;
         } else if (!live) {
             tc = kNoEval;
@@ -594,12 +597,12 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
             // band passes only make certain kills: every cell with x > tk has
             // corr - eps_cell > thr0 (eps_cell <= eps_row); knife edges are left
             // to the full-row pass
-            const double eps_row = E * (double)cn * (double)qn_max + kSlack + 8.0 * (double)kEps32;
+            const double eps_row = E * (double)cn * (double)qn_max + kSlack + 8.0 * (double)kEps32 + xs;
             const double tk = (p.thr0 + eps_row) / (double)cn;
             tc = (float)tk;
             tc = tc + fabsf(tc) * 2.4e-7f;  // round toward +inf (conservative)
         } else {
-            const double eps_row = E * (double)cn * (double)qn_max + kSlack + 8.0 * (double)kEps32;
+            const double eps_row = E * (double)cn * (double)qn_max + kSlack + 8.0 * (double)kEps32 + xs;
             tc = (float)((p.thr0 - eps_row) / (double)cn);
             tc = tc - fabsf(tc) * 2.4e-7f;  // round toward -inf (conservative)
         }
@@ -681,7 +684,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
                             qv.v[j] = rn[(j + uu) % kDiag];
                         }
                         slow_track(xv, qv, cr.z, cr.w, dir > 0 ? td.r0 + ss : r_end - ss, ss + ub, dir, qbase, N,
-                                   m, p.r_sq, p.thr0, E, p.alive, s_peer_alive, p.peers.n, p.queue,
+                                   m, p.r_sq, p.thr0, E, xs, p.alive, s_peer_alive, p.peers.n, p.queue,
                                    p.queue_count, p.queue_cap);
                     }
                     if (S.ykey[ss] != 0u) {
@@ -727,11 +730,13 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
 
     if (MODE == kPruneTrack) {
         __syncthreads();
-        const unsigned ekey = __float_as_uint(Ef * qn_max * (1.f + 4.8e-7f));  // >= 0: bit order
         for (int s = tid; s < rows; s += kThreads) {
             const unsigned k = S.ykey[s];
             if (k > 1u) {
                 const int c = dir > 0 ? td.r0 + s : r_end - s;
+                // the tile's error term in x units of this row: E*qn_max + xs/cn (>= 0: bit order)
+                const unsigned ekey =
+                    __float_as_uint((float)(E * (double)qn_max + xs / (double)S.crow[s].w) * (1.f + 4.8e-7f));
                 if (p.peers.n > 1) {
                     for (int r = 0; r < p.peers.n; ++r) {
                         atomicMax(&p.peers.ymax[r][c], k);
@@ -928,6 +933,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_band0_pair(const ScanParams p) 
     // seed and the resident seeds carry no seed error term
     const double P = (double)dc * (double)gq + (double)dq * (double)gc;
     const double E = p.err_k * (double)kEps32 * (double)(rows + 8) * ((double)m * smax_c * smax_q + 1.5 * P);
+    const double xs = stats_band(p, true);  // statistics error, resident raw seeds included
     constexpr float kNoEval = FLT_MAX;
     int evals = 0;
     for (int s = tid; s < rows; s += kThreads) {
@@ -937,14 +943,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_band0_pair(const ScanParams p) 
         if (!live0 || cn.x == 0.f) {
             tc.x = kNoEval;
         } else {
-            const double eps_row = E * (double)cn.x * (double)qn_max + kSlack + 8.0 * (double)kEps32;
+            const double eps_row = E * (double)cn.x * (double)qn_max + kSlack + 8.0 * (double)kEps32 + xs;
             tc.x = (float)((p.thr0 + eps_row) / (double)cn.x);
             tc.x = tc.x + fabsf(tc.x) * 2.4e-7f;  // round toward +inf (conservative)
         }
         if (!live1 || cn.y == 0.f) {
             tc.y = kNoEval;
         } else {
-            const double eps_row = E * (double)cn.y * (double)qn_max + kSlack + 8.0 * (double)kEps32;
+            const double eps_row = E * (double)cn.y * (double)qn_max + kSlack + 8.0 * (double)kEps32 + xs;
             tc.y = (float)((p.thr0 + eps_row) / (double)cn.y);
             tc.y = tc.y + fabsf(tc.y) * 2.4e-7f;
         }

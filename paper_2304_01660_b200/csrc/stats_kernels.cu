@@ -9,6 +9,8 @@
 //              bit-identical to advance_stats.
 // K2b derive:  the FP32 arrays the tile scan walks (df, dg, 1/(sqrt(m) sigma)),
 //              computed in FP64 and rounded once (HBM-bound, fused per length).
+#include <algorithm>
+
 #include "common.cuh"
 #include "engine_internal.h"
 
@@ -93,6 +95,153 @@ __global__ void k_init_finish(const double* __restrict__ sum, const double* __re
     }
 }
 
+// ---- statistics error (common.cuh) --------------------------
+// Double-double prefix sums of the series and of its squares (P[k] = sum of
+// the first k values), built once per series (tsd_series_set): three
+// launches, chunk totals -> exclusive scan of the totals -> chunk scans.
+constexpr int kPfxThreads = 512;
+
+__device__ __forceinline__ dd warp_incl_scan_dd(dd v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double h = __shfl_up_sync(0xffffffffu, v.hi, o);
+        const double l = __shfl_up_sync(0xffffffffu, v.lo, o);
+        if (lane >= o) v = dd_add(dd{h, l}, v);
+    }
+    return v;
+}
+
+__global__ void __launch_bounds__(kPfxThreads) k_dd_chunk_sums(const double* __restrict__ t, int n, int chunk,
+                                                                 double2* __restrict__ tot1,
+                                                                 double2* __restrict__ tot2) {
+    __shared__ dd r1[kPfxThreads / 32], r2[kPfxThreads / 32];
+    const int b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
+    dd s1{0.0, 0.0}, s2{0.0, 0.0};
+    for (int i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+        const double v = t[i];
+        s1 = dd_add(s1, dd{v, 0.0});
+        s2 = dd_add(s2, dd_sq(v));
+    }
+    s1 = warp_incl_scan_dd(s1);  // lane 31 holds the warp total
+    s2 = warp_incl_scan_dd(s2);
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 31) {
+        r1[w] = s1;
+        r2[w] = s2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        dd a{0.0, 0.0}, q{0.0, 0.0};
+        for (int k = 0; k < kPfxThreads / 32; ++k) {
+            a = dd_add(a, r1[k]);
+            q = dd_add(q, r2[k]);
+        }
+        tot1[blockIdx.x] = make_double2(a.hi, a.lo);
+        tot2[blockIdx.x] = make_double2(q.hi, q.lo);
+    }
+}
+
+__global__ void k_dd_scan_totals(double2* __restrict__ tot1, double2* __restrict__ tot2, int nb) {
+    dd a{0.0, 0.0}, q{0.0, 0.0};  // exclusive, in place (one thread: nb <= a few thousand)
+    for (int b = 0; b < nb; ++b) {
+        const double2 x = tot1[b], y = tot2[b];
+        tot1[b] = make_double2(a.hi, a.lo);
+        tot2[b] = make_double2(q.hi, q.lo);
+        a = dd_add(a, dd{x.x, x.y});
+        q = dd_add(q, dd{y.x, y.y});
+    }
+}
+
+__global__ void __launch_bounds__(kPfxThreads) k_dd_chunk_scan(const double* __restrict__ t, int n, int chunk,
+                                                                 const double2* __restrict__ tot1,
+                                                                 const double2* __restrict__ tot2,
+                                                                 double2* __restrict__ P1, double2* __restrict__ P2) {
+    __shared__ dd w1[kPfxThreads / 32], w2[kPfxThreads / 32];
+    const int b0 = blockIdx.x * chunk, b1 = min(n, b0 + chunk);
+    dd c1{tot1[blockIdx.x].x, tot1[blockIdx.x].y}, c2{tot2[blockIdx.x].x, tot2[blockIdx.x].y};
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        P1[0] = make_double2(0.0, 0.0);
+        P2[0] = make_double2(0.0, 0.0);
+    }
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int base = b0; base < b1; base += blockDim.x) {
+        const int i = base + threadIdx.x;
+        const double v = i < b1 ? t[i] : 0.0;
+        dd s1 = warp_incl_scan_dd(dd{v, 0.0});
+        dd s2 = warp_incl_scan_dd(i < b1 ? dd_sq(v) : dd{0.0, 0.0});
+        if (lane == 31) {
+            w1[w] = s1;
+            w2[w] = s2;
+        }
+        __syncthreads();
+        dd o1 = c1, o2 = c2;  // carry + totals of the earlier warps of this tile
+        for (int k = 0; k < w; ++k) {
+            o1 = dd_add(o1, w1[k]);
+            o2 = dd_add(o2, w2[k]);
+        }
+        if (i < b1) {
+            const dd p1 = dd_add(o1, s1), p2 = dd_add(o2, s2);
+            P1[i + 1] = make_double2(p1.hi, p1.lo);
+            P2[i + 1] = make_double2(p2.hi, p2.lo);
+        }
+        for (int k = 0; k < kPfxThreads / 32; ++k) {  // the tile total joins the carry
+            c1 = dd_add(c1, w1[k]);
+            c2 = dd_add(c2, w2[k]);
+        }
+        __syncthreads();
+    }
+}
+
+// Statistics error a_i of window i (correlation units) and 1 + mu^2 / sigma^2:
+//   eps = |sigma_r - sigma| / sigma  (rolling sigma against the window's moments
+//         from the double-double prefix sums),
+//   gam = |mu_r - mu| / sigma,
+//   eta = 3 (m + 1) u (1 + Om + sqrt(Om)), Om = mu^2 / sigma^2: the one-pass
+//         variance error of the exact distance's znormalize (sequential sums of
+//         m terms), relative;
+//   a   = 2 eps + 2 eta + kStatsRows gam  (+inf if the window has no variance).
+__device__ __forceinline__ float stats_err(const double2* __restrict__ P1, const double2* __restrict__ P2, int i,
+                                           int m, double mu_r, double sg_r, float& b2) {
+    const double2 x0 = P1[i], x1 = P1[i + m], y0 = P2[i], y1 = P2[i + m];
+    const dd S1 = dd_add(dd{x1.x, x1.y}, dd_neg(dd{x0.x, x0.y}));
+    const dd S2 = dd_add(dd{y1.x, y1.y}, dd_neg(dd{y0.x, y0.y}));
+    const double md = (double)m;
+    const dd mu = dd_div_d(S1, md);
+    const dd v = dd_add(S2, dd_neg(dd_mul(mu, S1)));  // m var
+    const double var = (v.hi + v.lo) / md;
+    b2 = 0.f;
+    if (!(var > 0.0)) return __int_as_float(0x7f800000);
+    const double sa = sqrt(var), mua = mu.hi + mu.lo;
+    const double om = mua * mua / var;
+    const double eps_s = fabs(sg_r - sa) / sa;
+    const double gam = fabs(mu_r - mua) / sa;
+    const double eta = 3.0 * (md + 1.0) * kEps64 * (1.0 + om + sqrt(om));
+    b2 = (float)((1.0 + om) * (1.0 + 1e-6));
+    return (float)((2.0 * eps_s + 2.0 * eta + kStatsRows * gam) * (1.0 + 1e-6) + 1e-300);
+}
+
+// block max of two non-negative floats (as int bits) into cr[3], cr[4]
+__device__ __forceinline__ void stats_max_commit(float a, float b2, int* cr) {
+    __shared__ int sa[32], sb[32];
+    int ia = __reduce_max_sync(0xffffffffu, __float_as_int(a));
+    int ib = __reduce_max_sync(0xffffffffu, __float_as_int(b2));
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        sa[w] = ia;
+        sb[w] = ib;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+            ia = max(ia, sa[k]);
+            ib = max(ib, sb[k]);
+        }
+        if (ia > 0) atomicMax(&cr[3], ia);
+        if (ib > 0) atomicMax(&cr[4], ib);
+    }
+}
+
 // stats (length m, n-m+1 valid) -> length m+1 (n-m valid), in place.
 __global__ void k_advance(const double* __restrict__ t, int n, int m, double* __restrict__ mu,
                           double* __restrict__ sig) {
@@ -122,26 +271,36 @@ __global__ void k_advance(const double* __restrict__ t, int n, int m, double* __
 __global__ void k_derive(const double* __restrict__ t, int m, int cnt, const double* __restrict__ mu,
                          const double* __restrict__ sig, float* __restrict__ df,
                          float* __restrict__ dg, float* __restrict__ nrm, int* __restrict__ cr,
-                         int* __restrict__ deg) {
+                         int* __restrict__ deg, const double2* __restrict__ P1, const double2* __restrict__ P2) {
     pdl_enter();
     const double sqm = sqrt((double)m);
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    float amax = 0.f, bmax = 0.f;
+    const int cnt_w = (cnt + 31) & ~31;  // warp-uniform bound (the commit reduces over warps)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt_w; i += gridDim.x * blockDim.x) {
+        if (i >= cnt) continue;
         const double s = sig[i];
-        nrm[i] = s < kSigmaEps ? 0.f : (float)(1.0 / (sqm * s));
-        if (s < kSigmaEps) {
+        float b2 = 0.f;
+        const float a = stats_err(P1, P2, i, m, mu[i], s, b2);
+        const bool dgn = s < kSigmaEps || !(a <= (float)kStatsUnreliable);
+        nrm[i] = dgn ? 0.f : (float)(1.0 / (sqm * s));
+        if (dgn) {
             atomicMax(&cr[0], cnt - i);
             atomicMax(&cr[1], i + 1);
             deg[atomicAdd(&cr[2], 1)] = i;  // decided exactly, against every q
+        } else {
+            amax = fmaxf(amax, a);
+            bmax = fmaxf(bmax, b2);
         }
         if (i == 0) {
             df[0] = 0.f;
             dg[0] = 0.f;
         } else {
-            const double a = t[i + m - 1], b = t[i - 1];
-            df[i] = (float)((a - b) * 0.5);
-            dg[i] = (float)((a - mu[i]) + (b - mu[i - 1]));
+            const double a2 = t[i + m - 1], b = t[i - 1];
+            df[i] = (float)((a2 - b) * 0.5);
+            dg[i] = (float)((a2 - mu[i]) + (b - mu[i - 1]));
         }
     }
+    stats_max_commit(amax, bmax, cr);
 }
 
 // One MERLIN length step in one launch (north_star (a)): Eq. 7-8 advance of
@@ -168,14 +327,12 @@ __global__ void k_next_length(const double* __restrict__ t, int n, int m, const 
                               const double* __restrict__ sig_in, double* __restrict__ mu_out,
                               double* __restrict__ sig_out, float* __restrict__ df, float* __restrict__ dg,
                               float* __restrict__ nrm, int* __restrict__ cr, int* __restrict__ cr_next, int L, int kA,
-                              int nb, double* __restrict__ qt, int* __restrict__ deg) {
+                              int nb, double* __restrict__ qt, int* __restrict__ deg,
+                              const double2* __restrict__ P1, const double2* __restrict__ P2) {
     pdl_enter();
     const int m1 = m + 1, cnt = n - m;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        cr_next[0] = 0;
-        cr_next[1] = 0;
-        cr_next[2] = 0;
-    }
+    if (blockIdx.x == 0 && threadIdx.x < kCrInts) cr_next[threadIdx.x] = 0;
+    float amax = 0.f, bmax = 0.f;
     const double sqm = sqrt((double)m1);
     const int lane = threadIdx.x & 31;
     // the loop bound is warp-uniform (the shuffle below needs every lane)
@@ -188,11 +345,17 @@ __global__ void k_next_length(const double* __restrict__ t, int n, int m, const 
         if (i >= cnt) continue;
         mu_out[i] = u;
         sig_out[i] = s;
-        nrm[i] = s < kSigmaEps ? 0.f : (float)(1.0 / (sqm * s));
-        if (s < kSigmaEps) {
+        float b2 = 0.f;
+        const float ae = stats_err(P1, P2, i, m1, u, s, b2);
+        const bool dgn = s < kSigmaEps || !(ae <= (float)kStatsUnreliable);
+        nrm[i] = dgn ? 0.f : (float)(1.0 / (sqm * s));
+        if (dgn) {
             atomicMax(&cr[0], cnt - i);
             atomicMax(&cr[1], i + 1);
             deg[atomicAdd(&cr[2], 1)] = i;  // decided exactly, against every q
+        } else {
+            amax = fmaxf(amax, ae);
+            bmax = fmaxf(bmax, b2);
         }
         if (i == 0) {
             df[0] = 0.f;
@@ -207,6 +370,7 @@ __global__ void k_next_length(const double* __restrict__ t, int n, int m, const 
             dg[i] = (float)((a - u) + (b - up));
         }
     }
+    stats_max_commit(amax, bmax, cr);
     if (qt != nullptr) {
         // one seed row per block iteration: no 64-bit index division, the row
         // value t[i+m] is a broadcast, qt and t[q+m] are coalesced
@@ -243,15 +407,27 @@ void launch_advance_stats(const double* t, int n, int m, double* mu, double* sig
 }
 
 void launch_derive(const double* t, int m, int cnt, const double* mu, const double* sig, float* df,
-                   float* dg, float* nrm, int* crange, int* deg, cudaStream_t st) {
-    launch_pdl(k_derive, grid_for(cnt, 256), 256, st, t, m, cnt, mu, sig, df, dg, nrm, crange, deg);
+                   float* dg, float* nrm, int* crange, int* deg, const double2* P1, const double2* P2,
+                   cudaStream_t st) {
+    launch_pdl(k_derive, grid_for(cnt, 256), 256, st, t, m, cnt, mu, sig, df, dg, nrm, crange, deg, P1, P2);
+}
+
+int dd_prefix_blocks(int n) { return std::max(1, std::min(148 * 4, (n + 4095) / 4096)); }
+
+void launch_dd_prefix(const double* t, int n, double2* tot1, double2* tot2, double2* P1, double2* P2,
+                      cudaStream_t st) {
+    const int nb = dd_prefix_blocks(n);
+    const int chunk = (n + nb - 1) / nb;
+    k_dd_chunk_sums<<<nb, kPfxThreads, 0, st>>>(t, n, chunk, tot1, tot2);
+    k_dd_scan_totals<<<1, 1, 0, st>>>(tot1, tot2, nb);
+    k_dd_chunk_scan<<<nb, kPfxThreads, 0, st>>>(t, n, chunk, tot1, tot2, P1, P2);
 }
 
 void launch_next_length(const double* t, int n, int m, const double* mu_in, const double* sig_in, double* mu_out,
                         double* sig_out, float* df, float* dg, float* nrm, int* cr, int* cr_next, int L, int kA,
-                        int nb, double* qt, int* deg, cudaStream_t st) {
+                        int nb, double* qt, int* deg, const double2* P1, const double2* P2, cudaStream_t st) {
     launch_pdl(k_next_length, grid_for(n - m, 256), 256, st, t, n, m, mu_in, sig_in, mu_out, sig_out, df, dg, nrm, cr,
-               cr_next, L, kA, nb, qt, deg);
+               cr_next, L, kA, nb, qt, deg, P1, P2);
 }
 
 }  // namespace tsd

@@ -74,7 +74,8 @@ def make_series(spec: dict) -> np.ndarray:
     if spec["gen"] == "randomwalk":
         from . import gen_randomwalk
 
-        return gen_randomwalk(spec["n"], spec["seed"])
+        x = gen_randomwalk(spec["n"], spec["seed"])
+        return x + spec["offset"] if spec.get("offset") else x
     if spec["gen"] == "ecg":
         return gen_ecg_like(spec["n"], spec["seed"])
     raise ValueError(f"unknown generator {spec['gen']}")

@@ -5,6 +5,8 @@ UNMODIFIED reference library (oracle/_ref/libtsdref.so, built from
     python tests/golden/make_golden.py small          # seconds
     python tests/golden/make_golden.py c1 c2          # C1 ~2 s, C2 ~1 min (8 threads)
     python tests/golden/make_golden.py c4 --workers 8 # ~40 min: full-size parity
+    python tests/golden/make_golden.py semantics      # retry budget, reuse_stats, logic_error, offsets
+    python tests/golden/make_golden.py c10            # acceptance criterion 10 shape, top-6
 
 Every fixture stores the inputs (generator + seed, or the literal series), the
 call, and the reference's outputs, so tests can check both the C restatement
@@ -23,7 +25,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
-from oracle.refbind import Ref  # noqa: E402
+from oracle.refbind import CheckerError, Ref  # noqa: E402
 
 CONFIGS = {
     # c3: BASELINE config 3 (ECG-like n=500,000, lengths 64-512); "c3s" is its first
@@ -38,6 +40,8 @@ CONFIGS = {
     # "c5s": the first 32 lengths of C5 (top-3), the parity fixture that fits the
     # build container's CPU budget
     "c5s": (2_000_000, 1, 128, 159, 3, 512),
+    # acceptance criterion 10's case study (tests/acceptance_test.cpp:410-446): top-6
+    "c10": (35_040, 1048, 48, 672, 6, 512),
 }
 
 
@@ -45,10 +49,16 @@ def recs_to_list(recs):
     return [[int(r["index"]), float(r["nn_dist_sq"]).hex(), float(r["nn_dist"]).hex()] for r in recs]
 
 
-def merlin_fixture(R, x, gen, minL, maxL, top_k, seglen, workers, max_retries=100):
+def merlin_fixture(R, x, gen, minL, maxL, top_k, seglen, workers, max_retries=100,
+                   reuse_stats=True):
     t = time.time()
-    out = R.merlin(x, minL, maxL, top_k=top_k, seglen=seglen, workers=workers,
-                   max_retries=max_retries)
+    try:
+        out = R.merlin(x, minL, maxL, top_k=top_k, seglen=seglen, workers=workers,
+                       max_retries=max_retries, reuse_stats=reuse_stats)
+    except CheckerError as e:  # the reference threw (e.g. logic_error from src/merlin.cpp:19)
+        return dict(kind="merlin", input=gen, n=len(x), min_len=minL, max_len=maxL, top_k=top_k,
+                    seglen=seglen, max_retries=max_retries, reuse_stats=reuse_stats,
+                    error=dict(code=e.code, message=str(e).split("] ", 1)[1]))
     dt = time.time() - t
     per = []
     for k in range(maxL - minL + 1):
@@ -56,8 +66,8 @@ def merlin_fixture(R, x, gen, minL, maxL, top_k, seglen, workers, max_retries=10
                         retries=int(out["retries"][k]),
                         records=recs_to_list(out["recs"][k][: out["counts"][k]])))
     return dict(kind="merlin", input=gen, n=len(x), min_len=minL, max_len=maxL, top_k=top_k,
-                seglen=seglen, max_retries=max_retries, ref_seconds=dt, ref_workers=workers,
-                per_length=per)
+                seglen=seglen, max_retries=max_retries, reuse_stats=reuse_stats, ref_seconds=dt,
+                ref_workers=workers, per_length=per)
 
 
 def small(R):
@@ -118,6 +128,46 @@ def small(R):
     print("wrote small.json")
 
 
+def semantics(R):
+    """Reference-semantics cases the long goldens never reach:
+    the retry budget (src/merlin.cpp:104-107), reuse_stats=false (tests/merlin_test.cpp:80-99),
+    a warm-up failure that makes the steady phase throw logic_error (src/merlin.cpp:19,77-82),
+    and series with a DC offset (the rolling statistics and the FP32 filter see |mean| >> sigma)."""
+    fx = []
+
+    def walk(n, seed, offset=0.0):
+        x = R.gen_randomwalk(n, seed) + offset
+        g = dict(gen="randomwalk", n=n, seed=seed)
+        if offset:
+            g["offset"] = offset
+        return x, g
+
+    # retry budget: exhaustion accepts a non-empty list, an empty one fails the length
+    for mr in (0, 1, 2):
+        x, g = walk(2000, 5)
+        fx.append(dict(name=f"max_retries_{mr}", **merlin_fixture(R, x, g, 8, 20, 3, 64, 4, max_retries=mr)))
+        x, g = walk(77, 17)
+        fx.append(dict(name=f"max_retries_{mr}_short", **merlin_fixture(R, x, g, 4, 8, 1, 16, 1, max_retries=mr)))
+    # warm-up failure: a failed warm-up length leaves < 5 history entries at the first
+    # steady length -> ThresholdHistory::window_mean throws std::logic_error
+    for n, seed, minL in ((77, 17, 4), (69, 9, 6)):
+        x, g = walk(n, seed)
+        fx.append(dict(name=f"logic_error_{n}_{seed}", **merlin_fixture(R, x, g, minL, minL + 9, 1, 16, 1, max_retries=2)))
+    # reuse_stats = false (tests/merlin_test.cpp:80-99 shape) and true for comparison
+    for reuse in (False, True):
+        x, g = walk(1200, 55)
+        fx.append(dict(name=f"reuse_stats_{int(reuse)}", **merlin_fixture(R, x, g, 8, 24, 2, 48, 4, reuse_stats=reuse)))
+    # DC offsets: the reference stays self-consistent (== brute force) up to ~3e5 here
+    for off in (1e4, 1e5):
+        x, g = walk(3000, 2024, off)
+        fx.append(dict(name=f"offset_{off:g}_3000", **merlin_fixture(R, x, g, 8, 24, 2, 128, 4)))
+    x, g = walk(10000, 1, 1e5)
+    fx.append(dict(name="offset_1e+05_c1", **merlin_fixture(R, x, g, 64, 128, 1, 512, 8)))
+    with open(os.path.join(HERE, "semantics.json"), "w") as f:
+        json.dump(fx, f, indent=0)
+    print("wrote semantics.json")
+
+
 def big(R, name, workers):
     n, seed, minL, maxL, top_k, seglen = CONFIGS[name]
     if name.startswith("c3"):
@@ -143,5 +193,7 @@ if __name__ == "__main__":
     for w in a.what:
         if w == "small":
             small(R)
+        elif w == "semantics":
+            semantics(R)
         else:
             big(R, w, a.workers)

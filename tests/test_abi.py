@@ -95,3 +95,31 @@ def test_context_creation_fails_loudly_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError):
         P.Engine(0)
+
+
+def test_cpp_dropin_exports_reference_declarations():
+    # every function the reference headers declare (proj/include/tsdiscord/*.hpp)
+    # is defined by libtsdiscord_b200.so, so a reference caller relinks unchanged
+    P.load_library()
+    out = subprocess.run(["nm", "-DC", "--defined-only", P.LIB_PATH], capture_output=True, text=True).stdout
+    for sym in ["tsdiscord::znormalize(", "tsdiscord::sq_ed(", "tsdiscord::sq_ednorm_from_dot(",
+                "tsdiscord::early_abandon_sq_ed(", "tsdiscord::dot_products_block(",
+                "tsdiscord::update_dot_col(", "tsdiscord::drag_select(", "tsdiscord::drag_refine(",
+                "tsdiscord::drag(", "tsdiscord::brute_force_nn(", "tsdiscord::brute_force_topk(",
+                "tsdiscord::par_select(", "tsdiscord::par_refine(", "tsdiscord::pardrag(",
+                "tsdiscord::SelectionState::SelectionState(", "tsdiscord::SelectionState::conjoin(",
+                "tsdiscord::SelectionState::lower_nn_dist_sq(", "tsdiscord::merlin(",
+                "tsdiscord::merlin_full(", "tsdiscord::next_threshold(", "tsdiscord::init_stats(",
+                "tsdiscord::advance_stats(", "tsdiscord::compute_layout(", "tsdiscord::build_heatmap(",
+                "tsdiscord::rank_discords(", "tsdiscord::load_series(", "tsdiscord::gen_randomwalk(",
+                "tsdiscord::write_discords_csv(", "tsdiscord::read_discords_csv("]:
+        assert sym in out, sym
+
+
+def test_reference_acceptance_gate_links():
+    # built by build() from the unchanged reference test (tests/cpp/Makefile)
+    gate = os.path.join(ROOT, "tests", "cpp", "_ref", "acceptance")
+    if not os.path.exists(gate):
+        pytest.skip("acceptance gate not built (needs /root/reference)")
+    out = subprocess.run(["ldd", gate], capture_output=True, text=True).stdout
+    assert "libtsdiscord_b200.so" in out and "not found" not in out
