@@ -75,6 +75,8 @@ typedef struct {
     double host_wall_ms;    /* host wall time inside DRAG tries */
     double host_wait_ms;    /* ... of which blocked in stream synchronisation */
     double heatmap_ms;      /* device time of the last heatmap column-max pass */
+    uint64_t fallbacks;     /* tries that overflowed the knife-edge queue or the near-pair
+                               buffer and finished with the exact pass over their live rows */
 } tsd_counters;
 
 /* ---- context ------------------------------------------------------------ */

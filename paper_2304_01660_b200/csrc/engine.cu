@@ -170,6 +170,9 @@ struct tsd_ctx {
     float seed_w = 0.25f;  // grouping cost: one group-diagonal seed = seed_w*m walked row-diagonals (FP32 seeds)
     int band_few = 256;       // ... or when at most max(band_few, N/4096) rows are left (C2: 64 -> 41.8 ms, 256 -> 41.2 ms)
     int result_prefix = 1024;  // records copied back with the try's single round trip
+    // knife-edge queue / near-pair buffer capacities (settable below the
+    // allocation for tests of the overflow fallback)
+    int queue_cap = kQueueCap, coll_cap = kCollCap;
     double err_k = 4.0;
 
     // accounting
@@ -415,7 +418,7 @@ struct tsd_ctx {
         p.alive = alive.p;
         p.queue = queue.p;
         p.queue_count = &ctl.p->queue;
-        p.queue_cap = kQueueCap;
+        p.queue_cap = queue_cap;
         p.ymax = ymax.p;
         p.emax = emax.p;
         p.seedqt = seedqt.p;
@@ -423,7 +426,7 @@ struct tsd_ctx {
         p.ythr = ythr.p;
         p.coll = coll.p;
         p.coll_count = &ctl.p->coll;
-        p.coll_cap = kCollCap;
+        p.coll_cap = coll_cap;
         p.ctl = ctl.p;
         p.groups = groups.p;
         p.rank = rank;
@@ -667,7 +670,7 @@ struct tsd_ctx {
         reduce_maxima(N);
         // knife edges: the reference's FP64 distance decides (pardrag.cpp:255);
         // degenerate rows: every pair with one is decided exactly.  One launch.
-        launch_recheck(t.p, (int)m, N, queue.p, &C->queue, kQueueCap, list.p, C, cr_cur, deg.p, r_sq, alive.p,
+        launch_recheck(t.p, (int)m, N, queue.p, &C->queue, queue_cap, list.p, C, cr_cur, deg.p, r_sq, alive.p,
                        nnkey.p, rank, world, peers, st);
         ck(cudaGetLastError(), "recheck");
         reduce_alive(N);
@@ -682,7 +685,7 @@ struct tsd_ctx {
         q.space = kSpaceFull;  // every diagonal of the exact-nn rows' groups
         q.seed32 = seed32_collect;
         scan(kCollect, q);
-        launch_ref_pairs(1, t.p, (int)m, coll.p, &C->coll, kCollCap, r_sq, alive.p, nnkey.p, C,
+        launch_ref_pairs(1, t.p, (int)m, coll.p, &C->coll, coll_cap, r_sq, alive.p, nnkey.p, C,
                          world == 1 ? ex : nullptr, nnout.p, peers, st);
         ck(cudaGetLastError(), "exact");
         if (world > 1) {
@@ -703,8 +706,19 @@ struct tsd_ctx {
         ck(cudaMemcpyAsync(h_nn.p, nnout.p, pf * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
         sync();
         const TryCtl hc = *h_ctl.p;
-        if (hc.queue > kQueueCap) fail(TSD_ERUNTIME, "knife-edge queue overflow (degenerate series?)");
-        if (hc.coll > kCollCap) fail(TSD_ERUNTIME, "near-pair buffer overflow (degenerate series?)");
+        if (hc.queue > queue_cap || hc.coll > coll_cap) {
+            // degenerate inputs (exact ties by the thousand, e.g. an exactly
+            // periodic series): finish the try with the exact pass over every
+            // live row instead of failing, as the reference does
+            harvest(m);
+            harvest_events();
+            ctr.rechecks += (unsigned long long)std::min(hc.queue, queue_cap);
+            ctr.exact_pairs += (unsigned long long)std::min(hc.coll, coll_cap);
+            ctr.fallbacks += 1;
+            out = exact_fallback(m, r_sq, all_nn, N);
+            last_count = (int)out.size();
+            return out;
+        }
         ctr.rechecks += (unsigned long long)hc.queue;
         ctr.exact_pairs += (unsigned long long)hc.coll;
         last_count = hc.sc;
@@ -748,6 +762,47 @@ struct tsd_ctx {
             return a.index < b.index;
         });
         return finish(m, out);
+    }
+
+    // Overflow fallback (src/pardrag.cpp:142-149,388-407): the rows still alive
+    // get the exact pass against every admissible q.  Kills made so far are
+    // certain, and a dropped knife-edge pair can only have left a row alive
+    // wrongly, so the exact pass over the live rows decides them all; the
+    // exact-nn keys it lowers are the survivors' nn.  Records sorted like
+    // sort_discords, every survivor included (the MERLIN count stays exact).
+    std::vector<tsd_record> exact_fallback(int64_t m, double r_sq, double* all_nn, int N) {
+        compact(N, kGateNone, m);  // list + ctl->alive from the current flags
+        launch_exact_rows(t.p, (int)m, N, list.p, ctl.p, r_sq, alive.p, nnkey.p, rank, world, peers, st);
+        ck(cudaGetLastError(), "exact rows");
+        ctr.kernel_launches += 1;
+        reduce_alive(N);
+        if (world > 1) {
+            if (peers.n > 1) peer_barrier();
+            else allreduce_min_u64(nnkey.p, N);
+        }
+        ck(cudaMemcpyAsync(h_ctl.p, ctl.p, sizeof(TryCtl), cudaMemcpyDeviceToHost, st), "D2H");
+        sync();
+        const int cnt = h_ctl.p->alive;
+        std::vector<int> rows(cnt);
+        std::vector<uint8_t> al(N);
+        std::vector<unsigned long long> keys(N);
+        if (cnt > 0) ck(cudaMemcpyAsync(rows.data(), list.p, cnt * sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaMemcpyAsync(al.data(), alive.p, N, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaMemcpyAsync(keys.data(), nnkey.p, N * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "D2H");
+        sync();
+        std::vector<tsd_record> out;
+        for (int c : rows) {
+            if (!al[c]) continue;
+            double d;
+            std::memcpy(&d, &keys[c], sizeof d);
+            if (all_nn) all_nn[c] = d;
+            out.push_back(tsd_record{(int64_t)c + 1, d, std::sqrt(d)});
+        }
+        std::sort(out.begin(), out.end(), [](const tsd_record& a, const tsd_record& b) {
+            if (a.nn_dist_sq != b.nn_dist_sq) return a.nn_dist_sq > b.nn_dist_sq;
+            return a.index < b.index;
+        });
+        return out;
     }
 
     // end of a pardrag call (the stream is idle): fold in counters and timings
@@ -1664,6 +1719,8 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "band_fill") c->band_fill = std::max(0.0, v);
         else if (k == "band_passes") c->band_passes = std::max(1, std::min(64, (int)v));
         else if (k == "result_prefix") c->result_prefix = std::max(16, std::min(1 << 20, (int)v));
+        else if (k == "queue_cap") c->queue_cap = std::max(1, std::min(kQueueCap, (int)v));
+        else if (k == "coll_cap") c->coll_cap = std::max(1, std::min(kCollCap, (int)v));
         else fail(TSD_EINVAL, "unknown parameter " + k);
     });
 }

@@ -1198,6 +1198,32 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_recheck(const double* __res
     degenerate_body(t, m, N, list, ctl, cr, deg, r_sq, alive, nnkey, rank, world, peers, buf[w]);
 }
 
+// Overflow fallback, the analogue of the reference's full exact pass for a
+// candidate whose near-pair list would not stay bounded
+// (src/pardrag.cpp:142-149,388-407): every listed row still alive against every
+// admissible q by the exact routine.  d < r^2 kills the row; every d lowers its
+// exact-nn key.  One warp per pair, dealt over the ranks.
+__global__ void __launch_bounds__(kPairWarps * 32) k_exact_rows(const double* __restrict__ t, int m, int N,
+                                                                const int* __restrict__ list,
+                                                                const TryCtl* __restrict__ ctl, double r_sq,
+                                                                uint8_t* alive, unsigned long long* nnkey, int rank,
+                                                                int world, const Peers peers) {
+    pdl_enter();
+    __shared__ double buf[kPairWarps][256];
+    const int w = threadIdx.x >> 5;
+    const long long tot = (long long)ctl->alive * N;
+    for (long long e = ((long long)blockIdx.x * kPairWarps + w) * world + rank; e < tot;
+         e += (long long)gridDim.x * kPairWarps * world) {
+        const int c = list[e / N], q = (int)(e % N);
+        if (abs(c - q) < m || !alive[c]) continue;  // a dead row's nn is not needed
+        const double d = ref_dist_warp(t, m, c, q, buf[w]);
+        if ((threadIdx.x & 31) == 0) {
+            if (d < r_sq) peer_kill(peers, alive, c);
+            peer_min_key(peers, nnkey, c, (unsigned long long)__double_as_longlong(d));
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // flags / compaction / grouping / survivor kernels.  None of them takes a
 // count from the host: counts live in TryCtl, so one DRAG try is a single
@@ -2052,6 +2078,13 @@ void launch_scan(int mode, const ScanParams& p, cudaStream_t st) {
         case kPruneTrack: launch_pdl(k_scan<kPruneTrack>, scan_grid<kPruneTrack>(), kThreads, st, p); break;
         default: launch_pdl(k_scan<kCollect>, scan_grid<kCollect>(), kThreads, st, p); break;
     }
+}
+
+void launch_exact_rows(const double* t, int m, int N, const int* list, const TryCtl* ctl, double r_sq,
+                       uint8_t* alive, unsigned long long* nnkey, int rank, int world, const Peers& peers,
+                       cudaStream_t st) {
+    launch_pdl(k_exact_rows, 148 * 4, kPairWarps * 32, st, t, m, N, list, ctl, r_sq, alive, nnkey, rank, world,
+               peers);
 }
 
 void launch_ref_pairs(int mode, const double* t, int m, const int2* pairs, const int* count, int cap,

@@ -112,3 +112,63 @@ def test_cpp_drag_phases_via_pardrag(engine, oracle):
         r_sq = float(np.sort(nn)[min(int(len(nn) * q), len(nn) - 1)])
         got = engine.pardrag(12, r_sq, seglen=64)
         assert recs_list(got) == recs_list(oracle.range_discords(x, 12, r_sq))
+
+
+def periodic_series(n, period=37, seed=5):
+    rng = np.random.default_rng(seed)
+    x = np.tile(rng.normal(size=period), n // period + 1)[:n].copy()
+    x[1000:1005] += 3.0  # one anomaly; every other window has exact repeats (nn = 0)
+    return x
+
+
+def test_overflow_fallback_with_small_caps(engine, oracle):
+    # the knife-edge queue and the near-pair buffer overflowing finish the try
+    # with the exact pass over the live rows (src/pardrag.cpp:142-149,388-407)
+    # instead of failing; thresholds at exact ties make knife edges
+    x = oracle.gen_randomwalk(1500, 12)
+    engine.set_series(x)
+    m = 16
+    nn = oracle.brute_force_nn(x, m)
+    s = np.sort(nn)
+    before = engine.counters()["fallbacks"]
+    try:
+        for cap in ("queue_cap", "coll_cap"):
+            engine.set_param(cap, 1)
+            for q in (0.5, 0.9, 0.99):
+                r_sq = float(s[int(len(s) * q)])
+                got = engine.pardrag(m, r_sq, seglen=64)
+                assert recs_list(got) == recs_list(oracle.range_discords(x, m, r_sq)), (cap, q)
+            assert np.array_equal(engine.brute_force_nn(m), nn), cap
+            engine.set_param(cap, 1 << 30)
+    finally:
+        engine.set_param("queue_cap", 1 << 30)
+        engine.set_param("coll_cap", 1 << 30)
+    assert engine.counters()["fallbacks"] > before
+
+
+def test_periodic_series_merlin_and_bruteforce(engine, oracle):
+    # exactly periodic data: thousands of exact ties per row (forced small
+    # near-pair buffer so the fallback runs at this size)
+    x = periodic_series(4000)
+    engine.set_series(x)
+    try:
+        engine.set_param("coll_cap", 4096)
+        assert np.array_equal(engine.brute_force_nn(16), oracle.brute_force_nn(x, 16))
+        rep = engine.merlin_full(16, 20, top_k=2, seglen=128)
+    finally:
+        engine.set_param("coll_cap", 1 << 30)
+    exp = oracle.merlin(x, 16, 20, top_k=2, seglen=128)
+    for k, m in enumerate(range(16, 21)):
+        assert recs_list(rep.per_length[m]) == recs_list(exp["recs"][k][: exp["counts"][k]]), m
+    assert np.array_equal(rep.final_r, exp["final_r"]) and np.array_equal(rep.retries, exp["retries"])
+
+
+@pytest.mark.slow
+def test_periodic_series_natural_overflow(engine, oracle):
+    # n = 30,000: the near-minimum pairs of brute_force_nn (~N^2 / period = 2.4e7)
+    # overflow the 8M buffer at the default capacity
+    x = periodic_series(30_000)
+    engine.set_series(x)
+    before = engine.counters()["fallbacks"]
+    assert np.array_equal(engine.brute_force_nn(16), oracle.brute_force_nn(x, 16))
+    assert engine.counters()["fallbacks"] > before
