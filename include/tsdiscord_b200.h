@@ -140,6 +140,18 @@ int tsd_par_refine(tsd_ctx* ctx, int64_t m, double r_sq, int64_t seglen, const d
                    const double* sigma, const uint8_t* cand, tsd_record* out, int64_t cap,
                    int64_t* count);
 
+/* ---- the tile deal of the multi-rank scan (host side, no device needed) ----
+ * Decodes the tile slots rank `rank` of `world` fetches in one scan launch,
+ * with the kernels' own decoder (tile_space.cuh): space 0 = band 0 at offset
+ * kA over L-row blocks (nb sides, resident seeds), 1 = band [K0, K0+nb*1152)
+ * over L-row blocks, 2 = the same band over `groups` (G pairs first,last row),
+ * 3 = every diagonal |k| >= m of the groups (full rows).  out receives 5 ints
+ * per tile {r0, rows, k0, dir, seed}; *count the tiles (at most cap written).
+ * tests/test_multirank.py deals tiles to gloo ranks with it. */
+int tsd_tile_plan(int space, int64_t N, int64_t m, int64_t L, int64_t kA, int64_t nb, int64_t K0,
+                  const int32_t* groups, int64_t G, int rank, int world, int32_t* out, int64_t cap,
+                  int64_t* count);
+
 /* ---- MERLIN's length step, exposed for checking ----------------------------
  * stats_walk: init_stats(m0) on the device, then m1-m0 length steps exactly as
  * tsd_merlin runs them (fused != 0: the one-launch k_next_length step with the

@@ -35,7 +35,7 @@ EXPORTS = (
     "tsd_group_create", "tsd_group_destroy", "tsd_group_last_error", "tsd_group_size", "tsd_group_ctx",
     "tsd_group_series_set", "tsd_group_merlin", "tsd_group_pardrag", "tsd_matrix_profile_fp64",
     "tsd_ipc_export", "tsd_ipc_join", "tsd_par_select", "tsd_par_refine", "tsd_stats_walk",
-    "tsd_seed_rows",
+    "tsd_seed_rows", "tsd_tile_plan",
 )
 
 
@@ -104,6 +104,8 @@ def load_library(path: str = LIB_PATH):
     f("tsd_par_select", C.c_int, [vp, _i64, C.c_double, _i64, vp, vp, _u8, _dp])
     f("tsd_par_refine", C.c_int, [vp, _i64, C.c_double, _i64, vp, vp, _u8, vp, _i64, C.POINTER(_i64)])
     f("tsd_stats_walk", C.c_int, [vp, _i64, _i64, C.c_int, _dp, _dp])
+    f("tsd_tile_plan", C.c_int, [C.c_int, _i64, _i64, _i64, _i64, _i64, _i64, vp, _i64, C.c_int, C.c_int,
+                                 vp, _i64, C.POINTER(_i64)])
     f("tsd_seed_rows", C.c_int, [vp, vp, _i64, _ip])
     f("tsd_merlin", C.c_int, [vp, _i64, _i64, C.POINTER(_Opts), _ip, vp, _dp, _ip, _u8])
     f("tsd_brute_force_nn", C.c_int, [vp, _i64, _dp])
@@ -161,6 +163,30 @@ def next_threshold(history, phase: int, min_len: int, last_r: float, failed: boo
     _host_check(load_library().tsd_next_threshold(h, len(history), phase, min_len, last_r,
                                                    1 if failed else 0, C.byref(r)))
     return r.value
+
+
+TILE_SPACES = {"seed": 0, "blocks": 1, "band": 2, "full": 3}
+
+
+def tile_plan(space: str, N: int, m: int, rank: int = 0, world: int = 1, L: int = 512, kA: int = 0,
+              nb: int = 1, K0: int = 0, groups=None) -> np.ndarray:
+    """Tiles {r0, rows, k0, dir, seed} rank `rank` of `world` scans in one launch
+    of the given tile space (the kernels' own decoder; host only, no GPU)."""
+    L_ = load_library()
+    g = None
+    G = 0
+    if groups is not None:
+        g = np.ascontiguousarray(np.asarray(groups, dtype=np.int32).reshape(-1, 2))
+        G = len(g)
+    cnt = _i64(0)
+    _host_check(L_.tsd_tile_plan(TILE_SPACES[space], N, m, L, kA, nb, K0,
+                                 g.ctypes.data if g is not None else None, G, rank, world, None, 0,
+                                 C.byref(cnt)))
+    out = np.zeros((max(cnt.value, 1), 5), np.int32)
+    _host_check(L_.tsd_tile_plan(TILE_SPACES[space], N, m, L, kA, nb, K0,
+                                 g.ctypes.data if g is not None else None, G, rank, world,
+                                 out.ctypes.data, cnt.value, C.byref(cnt)))
+    return out[: cnt.value]
 
 
 def fp32_peak_tflops(device: int = 0) -> float:

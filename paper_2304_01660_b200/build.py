@@ -28,7 +28,7 @@ CXX_FLAGS = ["-O3", "-std=gnu++20", "-fPIC", "-I" + os.path.join(ROOT, "include"
              "-I/usr/local/cuda/include"]
 
 SOURCES = ["stats_kernels.cu", "scan_kernels.cu", "heatmap_kernels.cu", "mp_fp64.cu", "probe.cu", "engine.cu", "api.cpp"]
-HEADERS = ["common.cuh", "engine_internal.h", "nccl_shim.h", "peer_group.cuh"]
+HEADERS = ["common.cuh", "engine_internal.h", "nccl_shim.h", "peer_group.cuh", "tile_space.cuh"]
 
 
 def _newer(src: str, dst: str, deps) -> bool:

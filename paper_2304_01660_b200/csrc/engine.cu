@@ -33,6 +33,7 @@
 #include "engine_internal.h"
 #include "nccl_shim.h"
 #include "peer_group.cuh"
+#include "tile_space.cuh"
 
 using namespace tsd;
 
@@ -1695,6 +1696,72 @@ int tsd_reset_counters(tsd_ctx* c) {
     if (!c) return TSD_EINVAL;
     c->ctr = tsd_counters{};
     return TSD_OK;
+}
+
+int tsd_tile_plan(int space, int64_t N, int64_t m, int64_t L, int64_t kA, int64_t nb, int64_t K0,
+                  const int32_t* groups, int64_t G, int rank, int world, int32_t* out, int64_t cap,
+                  int64_t* count) {
+    return guard(nullptr, [&] {
+        if (world < 1 || rank < 0 || rank >= world) fail(TSD_EINVAL, "bad rank/world");
+        if (N < 1 || m < 1) fail(TSD_EINVAL, "bad N/m");
+        ScanParams p{};
+        p.N = (int)N;
+        p.m = (int)m;
+        p.L = (int)L;
+        p.kA = (int)kA;
+        p.nb = (int)nb;
+        p.K0 = (int)K0;
+        p.rank = rank;
+        p.world = world;
+        p.groups = reinterpret_cast<const int2*>(groups);
+        TileCtx c{0, 0, 0, 0};
+        switch (space) {
+            case 0:  // band 0 at kA over L-row blocks (resident seeds), nb sides
+                p.space = kSpaceSeed;
+                c.slots = nb * ((N + L - 1) / L);
+                break;
+            case 1:  // band [K0, K0 + nb kW) over L-row blocks
+                p.space = kSpaceBlocks;
+                c.G = (N + L - 1) / L;
+                c.slots = 2 * nb * c.G;
+                c.k0 = K0;
+                break;
+            case 2:  // band [K0, K0 + nb kW) over the groups
+                if (!groups || G < 1) fail(TSD_EINVAL, "groups required");
+                p.space = kSpaceBand;
+                c.G = G;
+                c.slots = 2 * nb * G;
+                c.k0 = K0;
+                break;
+            case 3: {  // every diagonal |k| >= m of the groups (full rows)
+                if (!groups || G < 1) fail(TSD_EINVAL, "groups required");
+                p.space = kSpaceFull;
+                c.G = G;
+                const int64_t maxc = (N - m + kW - 1) / kW;
+                c.slots = maxc > 0 ? 2 * maxc * G : 0;
+                break;
+            }
+            default:
+                fail(TSD_EINVAL, "unknown tile space");
+        }
+        // the kernels' cyclic deal: rank r fetches slots r, r + world, ...
+        const long long mine = world > 1 ? (c.slots > rank ? (c.slots - rank + world - 1) / world : 0) : c.slots;
+        int64_t k = 0;
+        for (long long f = 0; f < mine; ++f) {
+            TileDesc td;
+            if (!tile_decode(p, c, f * world + rank, td)) continue;
+            if (k < cap) {
+                int32_t* o = out + 5 * k;
+                o[0] = td.r0;
+                o[1] = td.rows;
+                o[2] = td.k0;
+                o[3] = td.dir;
+                o[4] = td.seed;
+            }
+            ++k;
+        }
+        *count = k;
+    });
 }
 
 int tsd_set_param(tsd_ctx* c, const char* key, double v) {
