@@ -194,31 +194,37 @@ __global__ void __launch_bounds__(kPfxThreads) k_dd_chunk_scan(const double* __r
 }
 
 // Statistics error a_i of window i (correlation units) and 1 + mu^2 / sigma^2:
-//   eps = |sigma_r - sigma| / sigma  (rolling sigma against the window's moments
-//         from the double-double prefix sums),
+//   ev  = |sigma_r^2 - var| / var  (rolling variance against the window's true
+//         variance from the double-double prefix sums; >= the relative sigma
+//         error, since |sqrt(a) - sqrt(b)| / sqrt(b) <= |a - b| / b),
 //   gam = |mu_r - mu| / sigma,
 //   eta = 3 (m + 1) u (1 + Om + sqrt(Om)), Om = mu^2 / sigma^2: the one-pass
 //         variance error of the exact distance's znormalize (sequential sums of
 //         m terms), relative;
-//   a   = 2 eps + 2 eta + kStatsRows gam  (+inf if the window has no variance).
+//   a   = 2 ev + 2 eta + kStatsRows gam  (+inf when the window has no variance).
+// Only the prefix differences and the cancelling m var = S2 - mu S1 need the
+// double-double; the bound itself is formed in FP32 (its 1e-7 relative
+// rounding is covered by the 1e-5 factor).
 __device__ __forceinline__ float stats_err(const double2* __restrict__ P1, const double2* __restrict__ P2, int i,
-                                           int m, double mu_r, double sg_r, float& b2) {
+                                           int m, double inv_m, double mu_r, double sg_r, float& b2) {
     const double2 x0 = P1[i], x1 = P1[i + m], y0 = P2[i], y1 = P2[i + m];
     const dd S1 = dd_add(dd{x1.x, x1.y}, dd_neg(dd{x0.x, x0.y}));
     const dd S2 = dd_add(dd{y1.x, y1.y}, dd_neg(dd{y0.x, y0.y}));
     const double md = (double)m;
-    const dd mu = dd_div_d(S1, md);
+    const double q1 = S1.hi * inv_m;  // mu = S1 / m as a double-double, without a division
+    const dd mu = dd_fast(q1, __dadd_rn(fma(-q1, md, S1.hi), S1.lo) * inv_m);
     const dd v = dd_add(S2, dd_neg(dd_mul(mu, S1)));  // m var
-    const double var = (v.hi + v.lo) / md;
+    const double var = (v.hi + v.lo) * inv_m;
     b2 = 0.f;
-    if (!(var > 0.0)) return __int_as_float(0x7f800000);
-    const double sa = sqrt(var), mua = mu.hi + mu.lo;
-    const double om = mua * mua / var;
-    const double eps_s = fabs(sg_r - sa) / sa;
-    const double gam = fabs(mu_r - mua) / sa;
-    const double eta = 3.0 * (md + 1.0) * kEps64 * (1.0 + om + sqrt(om));
-    b2 = (float)((1.0 + om) * (1.0 + 1e-6));
-    return (float)((2.0 * eps_s + 2.0 * eta + kStatsRows * gam) * (1.0 + 1e-6) + 1e-300);
+    if (!(var > 1e-30)) return __int_as_float(0x7f800000);
+    const double mua = mu.hi + mu.lo;
+    const float ivar = 1.f / (float)var;
+    const float ev = (float)fabs(fma(sg_r, sg_r, -var)) * ivar;
+    const float gam = (float)fabs(mu_r - mua) * rsqrtf((float)var);
+    const float om = (float)(mua * mua) * ivar;
+    const float eta = 3.f * (float)(m + 1) * 1.1102230e-16f * (1.f + om + sqrtf(om));
+    b2 = (1.f + om) * (1.f + 1e-5f);
+    return (2.f * ev + 2.f * eta + (float)kStatsRows * gam) * (1.f + 1e-5f) + 1e-30f;
 }
 
 // block max of two non-negative floats (as int bits) into cr[3], cr[4]
@@ -273,14 +279,14 @@ __global__ void k_derive(const double* __restrict__ t, int m, int cnt, const dou
                          float* __restrict__ dg, float* __restrict__ nrm, int* __restrict__ cr,
                          int* __restrict__ deg, const double2* __restrict__ P1, const double2* __restrict__ P2) {
     pdl_enter();
-    const double sqm = sqrt((double)m);
+    const double sqm = sqrt((double)m), inv_m = 1.0 / (double)m;
     float amax = 0.f, bmax = 0.f;
     const int cnt_w = (cnt + 31) & ~31;  // warp-uniform bound (the commit reduces over warps)
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt_w; i += gridDim.x * blockDim.x) {
         if (i >= cnt) continue;
         const double s = sig[i];
         float b2 = 0.f;
-        const float a = stats_err(P1, P2, i, m, mu[i], s, b2);
+        const float a = stats_err(P1, P2, i, m, inv_m, mu[i], s, b2);
         const bool dgn = s < kSigmaEps || !(a <= (float)kStatsUnreliable);
         nrm[i] = dgn ? 0.f : (float)(1.0 / (sqm * s));
         if (dgn) {
@@ -323,7 +329,7 @@ __device__ __forceinline__ void advance1(const double* __restrict__ t, int m, in
     sg1 = __dsqrt_rn(var > 0.0 ? var : 0.0);
 }
 
-__global__ void k_next_length(const double* __restrict__ t, int n, int m, const double* __restrict__ mu_in,
+__global__ void __launch_bounds__(256, 6) k_next_length(const double* __restrict__ t, int n, int m, const double* __restrict__ mu_in,
                               const double* __restrict__ sig_in, double* __restrict__ mu_out,
                               double* __restrict__ sig_out, float* __restrict__ df, float* __restrict__ dg,
                               float* __restrict__ nrm, int* __restrict__ cr, int* __restrict__ cr_next, int L, int kA,
@@ -333,20 +339,22 @@ __global__ void k_next_length(const double* __restrict__ t, int n, int m, const 
     const int m1 = m + 1, cnt = n - m;
     if (blockIdx.x == 0 && threadIdx.x < kCrInts) cr_next[threadIdx.x] = 0;
     float amax = 0.f, bmax = 0.f;
-    const double sqm = sqrt((double)m1);
+    const double sqm = sqrt((double)m1), inv_m1 = 1.0 / (double)m1;
     const int lane = threadIdx.x & 31;
-    // the loop bound is warp-uniform (the shuffle below needs every lane)
-    const int cnt_w = (cnt + 31) & ~31;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt_w; i += gridDim.x * blockDim.x) {
+    // each warp advances 32 consecutive windows and stores the last 31: lane 0's
+    // window is the halo whose new mean the next lane needs for dg (every lane
+    // runs exactly one advance; no lane recomputes a neighbour's)
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int base = gw * 31; base < cnt; base += nw * 31) {  // warp-uniform
+        const int i = base + lane - 1;
         double u = 0.0, s = 0.0;
-        if (i < cnt) advance1(t, m, i, mu_in, sig_in, u, s);
-        // mu_{i-1} of length m+1 from the neighbouring lane (lane 0 recomputes it)
-        double up = __shfl_up_sync(0xffffffffu, u, 1);
-        if (i >= cnt) continue;
+        if (i >= 0 && i < cnt) advance1(t, m, i, mu_in, sig_in, u, s);
+        const double up = __shfl_up_sync(0xffffffffu, u, 1);
+        if (lane == 0 || i >= cnt) continue;
         mu_out[i] = u;
         sig_out[i] = s;
         float b2 = 0.f;
-        const float ae = stats_err(P1, P2, i, m1, u, s, b2);
+        const float ae = stats_err(P1, P2, i, m1, inv_m1, u, s, b2);
         const bool dgn = s < kSigmaEps || !(ae <= (float)kStatsUnreliable);
         nrm[i] = dgn ? 0.f : (float)(1.0 / (sqm * s));
         if (dgn) {
@@ -361,10 +369,6 @@ __global__ void k_next_length(const double* __restrict__ t, int n, int m, const 
             df[0] = 0.f;
             dg[0] = 0.f;
         } else {
-            if (lane == 0) {
-                double sp;
-                advance1(t, m, i - 1, mu_in, sig_in, up, sp);  // same rounding as the neighbour's
-            }
             const double a = t[i + m1 - 1], b = t[i - 1];
             df[i] = (float)((a - b) * 0.5);
             dg[i] = (float)((a - u) + (b - up));
