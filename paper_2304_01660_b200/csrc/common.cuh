@@ -126,6 +126,7 @@ struct TryCtl {
     int tK0, tnb;   // next tracked chunk
     int tphase;     // 0 far chunks, 1 near chunk, 2 done
     int tpasses;    // tracked chunks that ran
+    unsigned tepoch;  // try counter (k_try_init): tags the per-(row, band) bounds of this try
     double lk;      // top-k filter: need_top-th largest nn lower bound
     double cost[6]; // compaction: grouping cost per span (16..512), self-resetting
 };
@@ -209,8 +210,19 @@ struct ScanParams {
     int pair;            // band 0 (kSpaceSeed, both sides): one paired walk per row block (k_band0_pair)
     const double* seedqt;  // resident raw dot products QT(i, i+k) of the band-0 tiles (kW per tile)
     const int* cr;         // per-length slot of this length (kCrInts ints; statistics error in [3], [4])
+    // per-(row, band) correlation upper bounds of the full-row stage, read by the
+    // collection to skip bands that cannot hold a row's nearest neighbour
+    // (nullptr: off).  Entry ((li * 2 + side) * nbands + band) for the row at
+    // list index li; value (tepoch << 32) | f2key(bound).
+    unsigned long long* ub;
+    long long ub_cap;      // entries available
+    const int* list;       // the sorted list of the full-row stage (ctl->alive rows)
+    int* exli;             // survivors' list index by row (k_survivors), read by the collection
     unsigned long long* acc;  // accounting: [0] cells walked, [1] cells evaluated, [2] seed dots
 };
+
+// canonical diagonal band of |k| for the per-(row, band) bounds: [m + b kW, m + (b+1) kW)
+__host__ __device__ __forceinline__ int ub_nbands(int N, int m) { return N > m ? (N - m + kW - 1) / kW : 0; }
 
 // Widening of every certified band of this length (correlation units) for
 // the statistics error: twice the largest per-window error a_i, plus, for

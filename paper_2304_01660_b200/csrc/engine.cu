@@ -129,6 +129,11 @@ struct tsd_ctx {
     DBuf<float> ythr;
     DBuf<unsigned long long> nnkey, acc;  // acc: [0] cells, [1] seeds
     DBuf<int> blk, list;
+    // per-(row, band) corr upper bounds of the full-row stage (collection skip)
+    DBuf<unsigned long long> ubk;
+    DBuf<int> exli;
+    int collect_skip = 1;
+    long long ub_entries = 1ll << 22;  // 32 MB
     DBuf<double> nnout;
     DBuf<int2> groups, slots;  // groups of the current stage; per-span candidate groups
     DBuf<double> bcost;        // per-CTA span costs of a compaction
@@ -538,6 +543,12 @@ struct tsd_ctx {
         acc.ensure(3);
         nnout.ensure(N);
         list.ensure(N);
+        exli.ensure(N);
+        if (collect_skip && !ubk.p) {
+            ubk.ensure((size_t)ub_entries);
+            // epoch-tagged entries: zero is older than every try
+            ck(cudaMemsetAsync(ubk.p, 0, (size_t)ub_entries * sizeof(unsigned long long), st), "memset");
+        }
         groups.ensure(N);
         if (!ctl.p) {
             ctl.ensure(1);
@@ -650,6 +661,14 @@ struct tsd_ctx {
         // covers whatever chunks the enqueued count did not reach.
         ScanParams q = P;
         q.seed32 = seed32_track;
+        // collection skip: single catch-all full-row launch, one rank (a row's
+        // band may span two tiles dealt to different ranks)
+        if (collect_skip && ubk.p && world == 1 && (track_chunks <= 1)) {
+            q.ub = ubk.p;
+            q.ub_cap = (long long)ubk.cap;
+            q.list = list.p;
+            q.exli = exli.p;
+        }
         launch_track_init(C, N, (int)m, r_sq > 0.0 && enq_passes > 0, st);
         ck(cudaGetLastError(), "track init");
         ctr.kernel_launches += 1;
@@ -680,7 +699,7 @@ struct tsd_ctx {
         // CTA filters the list to the survivors, applies the MERLIN top-k
         // filter, resets their keys and groups them.
         launch_survivors(list.p, alive.p, C, ymax.p, emax.p, nrm.p, cr_cur, N, (int)m, (int)need_top, bnd_lo.p,
-                         bnd_hi.p, cand.p, ythr.p, nnkey.p, groups.p, sparse_rows, seed_w, st);
+                         bnd_hi.p, cand.p, ythr.p, nnkey.p, groups.p, sparse_rows, seed_w, exli.p, st);
         ck(cudaGetLastError(), "survivors");
         const int* ex = cand.p;  // rows whose exact nn is computed (count: C->ec)
         q.space = kSpaceFull;  // every diagonal of the exact-nn rows' groups
@@ -968,6 +987,8 @@ void tsd_ctx_destroy(tsd_ctx* c) {
     c->acc.release();
     c->blk.release();
     c->list.release();
+    c->ubk.release();
+    c->exli.release();
     c->nnout.release();
     c->groups.release();
     c->slots.release();
@@ -1786,6 +1807,7 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "band_fill") c->band_fill = std::max(0.0, v);
         else if (k == "band_passes") c->band_passes = std::max(1, std::min(64, (int)v));
         else if (k == "result_prefix") c->result_prefix = std::max(16, std::min(1 << 20, (int)v));
+        else if (k == "collect_skip") c->collect_skip = v != 0.0;
         else if (k == "queue_cap") c->queue_cap = std::max(1, std::min(kQueueCap, (int)v));
         else if (k == "coll_cap") c->coll_cap = std::max(1, std::min(kCollCap, (int)v));
         else fail(TSD_EINVAL, "unknown parameter " + k);

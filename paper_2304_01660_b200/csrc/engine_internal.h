@@ -69,7 +69,7 @@ void launch_ref_pairs(int mode, const double* t, int m, const int2* pairs, const
 void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const unsigned* ymax,
                       const unsigned* emax, const float* nrm, const int* crange, int N, int m, int need,
                       double* lo, double* hi, int* cand, float* ythr, unsigned long long* nnkey, int2* groups,
-                      int fixed_span, float seed_w, cudaStream_t st);
+                      int fixed_span, float seed_w, int* exli, cudaStream_t st);
 // degenerate rows (sigma < eps): every (alive row, degenerate row) and
 // (degenerate row, any q) pair by the exact distance — kills and exact-nn keys
 // knife-edge recheck + degenerate pairs in one launch

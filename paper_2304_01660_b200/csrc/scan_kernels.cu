@@ -257,8 +257,37 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
     bool work;
     if (MODE == kCollect || p.space == kSpaceSeed) {
         int any = 0;
-        if (valid)  // tiles whose rows are all decided are skipped
-            for (int s = tid; s < td.rows; s += kThreads) any |= p.alive[td.r0 + s];
+        if (valid) {  // tiles whose rows are all decided are skipped
+            if (MODE == kCollect && p.ub != nullptr) {
+                // ... and so are bands that cannot hold any of its rows' nearest
+                // neighbours: the full-row stage's upper bound of corr over the
+                // band is below the row's lower bound of its best corr
+                const int nbands = ub_nbands(p.N, p.m);
+                const long long nlist = p.ctl->alive;
+                const bool ub_on = nlist * 2 * nbands <= p.ub_cap;
+                const int kf = td.dir > 0 ? td.k0 : -(td.k0 + kW - 1);
+                const int b = (kf - p.m) / kW;
+                const unsigned long long etag = (unsigned long long)p.ctl->tepoch << 32;
+                for (int s = tid; s < td.rows; s += kThreads) {
+                    const int c = td.r0 + s;
+                    if (!p.alive[c]) continue;
+                    const float th = p.ythr[c];
+                    if (th == FLT_MAX) continue;  // not a collection row
+                    bool need = true;
+                    if (ub_on && b >= 0 && b < nbands) {
+                        const unsigned long long v =
+                            p.ub[((long long)p.exli[c] * 2 + (td.dir < 0)) * nbands + b];
+                        if ((v & 0xffffffff00000000ull) == etag) {
+                            const float lb = th * p.nrm[c];  // corr lower bound of the row's best q
+                            need = key2f((unsigned)v) >= lb - fabsf(lb) * 4.8e-7f - 1e-7f;
+                        }
+                    }
+                    any |= need;
+                }
+            } else {
+                for (int s = tid; s < td.rows; s += kThreads) any |= p.alive[td.r0 + s];
+            }
+        }
         work = __syncthreads_or(any);
     } else {
         // directly seeded tiles shrink to their first..last undecided row:
@@ -639,10 +668,35 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
 
     if (MODE == kPruneTrack) {
         __syncthreads();
+        // per-(row, band) bounds for the collection: the tile covers the canonical
+        // bands b_lo..b_hi of |k| on its side
+        const int nbands = ub_nbands(N, m);
+        const long long nlist = p.ctl->alive;
+        const bool ub_on = p.ub != nullptr && nlist * 2 * nbands <= p.ub_cap;
+        const int kf = dir > 0 ? td.k0 : -(td.k0 + kW - 1);  // smallest |k| of the tile
+        const int b_lo = max(0, (kf - m) / kW), b_hi = min(nbands - 1, (kf + kW - 1 - m) / kW);
+        const unsigned long long etag = (unsigned long long)p.ctl->tepoch << 32;
         for (int s = tid; s < rows; s += kThreads) {
             const unsigned k = S.ykey[s];
             if (k > 1u) {
                 const int c = dir > 0 ? td.r0 + s : r_end - s;
+                if (ub_on) {
+                    // list index of c (sorted list): binary search
+                    int lo = 0, hi = (int)nlist - 1;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (p.list[mid] < c) lo = mid + 1;
+                        else hi = mid;
+                    }
+                    if (hi >= 0 && p.list[lo] == c) {
+                        // corr upper bound of every q of this tile for row c
+                        const float ubc = (float)(((double)key2f(k) + E * (double)qn_max) * (double)S.crow[s].w + xs) *
+                                              (1.f + 4.8e-7f) + 1e-7f;
+                        const unsigned long long v = etag | f2key(ubc);
+                        for (int b = b_lo; b <= b_hi; ++b)
+                            atomicMax(&p.ub[((long long)lo * 2 + (dir < 0)) * nbands + b], v);
+                    }
+                }
                 // the tile's error term in x units of this row: E*qn_max + xs/cn (>= 0: bit order)
                 const unsigned ekey =
                     __float_as_uint((float)(E * (double)qn_max + xs / (double)S.crow[s].w) * (1.f + 4.8e-7f));
@@ -1168,6 +1222,7 @@ __global__ void k_try_init(uint8_t* __restrict__ alive, unsigned* __restrict__ y
         ctl->bK0 = band_k0;
         ctl->bnb = 0;
         ctl->lk = 0.0;
+        ctl->tepoch += 1;
         acc[0] = acc[1] = acc[2] = 0ull;
     }
 }
@@ -1741,7 +1796,8 @@ __global__ void __launch_bounds__(1024) k_survivors(const int* __restrict__ list
                                                     int N, int m, int need, double* __restrict__ lo,
                                                     double* __restrict__ hi, int* __restrict__ cand,
                                                     float* __restrict__ ythr, unsigned long long* __restrict__ nnkey,
-                                                    int2* __restrict__ groups, int fixed_span, float seed_w) {
+                                                    int2* __restrict__ groups, int fixed_span, float seed_w,
+                                                    int* __restrict__ exli) {
     pdl_enter();
     __shared__ int wsum[32];
     __shared__ int hist[256];
@@ -1759,7 +1815,10 @@ __global__ void __launch_bounds__(1024) k_survivors(const int* __restrict__ list
         const int f = (e < cnt && alive[r]) ? 1 : 0;
         int tot;
         const int pos = sc + block_exscan(f, wsum, &tot);
-        if (f) cand[pos] = r;
+        if (f) {
+            cand[pos] = r;
+            if (exli) exli[r] = e;  // list index: the collection's per-(row, band) bounds
+        }
         sc += tot;
     }
     __syncthreads();
@@ -2018,9 +2077,9 @@ void launch_recheck(const double* t, int m, int N, const int2* pairs, const int*
 void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const unsigned* ymax,
                       const unsigned* emax, const float* nrm, const int* crange, int N, int m, int need,
                       double* lo, double* hi, int* cand, float* ythr, unsigned long long* nnkey, int2* groups,
-                      int fixed_span, float seed_w, cudaStream_t st) {
+                      int fixed_span, float seed_w, int* exli, cudaStream_t st) {
     launch_pdl(k_survivors, 1, 1024, st, list, alive, ctl, ymax, emax, nrm, crange, N, m, need, lo, hi, cand, ythr,
-               nnkey, groups, fixed_span, seed_w);
+               nnkey, groups, fixed_span, seed_w, exli);
 }
 
 void launch_try_init(uint8_t* alive, unsigned* ymax, unsigned* emax, float* ythr, unsigned long long* nnkey, int N,
