@@ -25,8 +25,26 @@ constexpr double kStatsUnreliable = 1e-3;          // corr units
 constexpr double kStatsRows = 1040.0;              // 2 (kMaxRows + 8): walk steps a mean error acts over
 // per-length slot (two parity slots of kCrInts ints): [0] max(N - i), [1] max(i + 1)
 // over degenerate rows, [2] their count (listed in deg), [3] bits of the max
-// statistics error a_i (float >= 0), [4] bits of the max 1 + mu_i^2 / sigma_i^2
-constexpr int kCrInts = 5;
+// statistics error a_i (float >= 0), [4] bits of the max 1 + mu_i^2 / sigma_i^2,
+// [5] max(N - i) and [6] max(i + 1) over the degenerate windows whose one-pass
+// statistics are constant too (znormalize gives all zeros: the 0 / 2m
+// conventions decide their pairs), [7] their count (listed in degc), [8] the
+// count of the other degenerate windows (listed in deg2; decided exactly)
+constexpr int kCrInts = 9;
+
+// The reference's znormalize test for a window (src/distance.cpp:8-22):
+// sequential sums in index order, no contraction; true when z is all zeros.
+__device__ __forceinline__ bool onepass_const(const double* __restrict__ w, int m) {
+    double s = 0.0, q = 0.0;
+    for (int k = 0; k < m; ++k) {
+        const double v = w[k];
+        s = __dadd_rn(s, v);
+        q = __dadd_rn(q, __dmul_rn(v, v));
+    }
+    const double mean = __ddiv_rn(s, (double)m);
+    const double var = __dsub_rn(__ddiv_rn(q, (double)m), __dmul_rn(mean, mean));
+    return __dsqrt_rn(var > 0.0 ? var : 0.0) < kSigmaEps;
+}
 
 struct dd {  // double-double (unevaluated sum hi + lo)
     double hi, lo;

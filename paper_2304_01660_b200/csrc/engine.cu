@@ -114,6 +114,7 @@ struct tsd_ctx {
     // double-double prefix sums of t and t^2 (statistics error, common.cuh)
     DBuf<double2> pfx1, pfx2, pfx_tot1, pfx_tot2;
     DBuf<int> deg;     // degenerate rows (sigma < eps) of the derived length
+    DBuf<int> degc, deg2;  // ... split: one-pass constant (conventions) / the others (exact)
 
     // scan state
     DBuf<uint8_t> alive;
@@ -335,7 +336,10 @@ struct tsd_ctx {
         // both parity slots cleared: the fused length step after this one uses the other
         ck(cudaMemsetAsync(crange.p, 0, 2 * kCrInts * sizeof(int), st), "memset");
         cr_cur = crange.p + kCrInts * (m & 1);
-        launch_derive(t.p, (int)m, (int)N, mu.p, sig.p, df.p, dg.p, nrm.p, cr_cur, deg.p, pfx1.p, pfx2.p, st);
+        degc.ensure(N);
+        deg2.ensure(N);
+        launch_derive(t.p, (int)m, (int)N, mu.p, sig.p, df.p, dg.p, nrm.p, cr_cur, deg.p, pfx1.p, pfx2.p, degc.p,
+                      deg2.p, st);
         ctr.kernel_launches += 1;
         ck(cudaGetLastError(), "derive");
         derived_m = m;
@@ -355,8 +359,10 @@ struct tsd_ctx {
         int* cr = crange.p + kCrInts * (m1 & 1);
         int* crn = crange.p + kCrInts * ((m1 + 1) & 1);
         deg.ensure(N1);
+        degc.ensure(N1);
+        deg2.ensure(N1);
         launch_next_length(t.p, (int)n, (int)m, mu.p, sig.p, mu2.p, sig2.p, df.p, dg.p, nrm.p, cr, crn, seed_L, seed_kA,
-                           seed_nb, with_seed ? seedqt.p : nullptr, deg.p, pfx1.p, pfx2.p, st);
+                           seed_nb, with_seed ? seedqt.p : nullptr, deg.p, pfx1.p, pfx2.p, degc.p, deg2.p, st);
         ck(cudaGetLastError(), "next length");
         ctr.kernel_launches += 1;
         std::swap(mu.p, mu2.p);
@@ -690,7 +696,8 @@ struct tsd_ctx {
         reduce_maxima(N);
         // knife edges: the reference's FP64 distance decides (pardrag.cpp:255);
         // degenerate rows: every pair with one is decided exactly.  One launch.
-        launch_recheck(t.p, (int)m, N, queue.p, &C->queue, queue_cap, list.p, C, cr_cur, deg.p, r_sq, alive.p,
+        launch_recheck(t.p, (int)m, N, queue.p, &C->queue, queue_cap, list.p, C, cr_cur, degc.p, deg2.p, nrm.p,
+                       r_sq, alive.p,
                        nnkey.p, rank, world, peers, st);
         ck(cudaGetLastError(), "recheck");
         reduce_alive(N);
@@ -970,6 +977,8 @@ void tsd_ctx_destroy(tsd_ctx* c) {
     c->pfx_tot1.release();
     c->pfx_tot2.release();
     c->deg.release();
+    c->degc.release();
+    c->deg2.release();
     c->mu2.release();
     c->sig2.release();
     c->lbstat.release();

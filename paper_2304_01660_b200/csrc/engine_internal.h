@@ -46,7 +46,7 @@ void launch_init_stats(const double* t, int n, int m, double* mu, double* sig, d
 void launch_advance_stats(const double* t, int n, int m, double* mu, double* sig, cudaStream_t st);
 void launch_derive(const double* t, int m, int cnt, const double* mu, const double* sig, float* df,
                    float* dg, float* nrm, int* crange, int* deg, const double2* P1, const double2* P2,
-                   cudaStream_t st);
+                   int* degc, int* deg2, cudaStream_t st);
 // double-double prefix sums of t and t^2 (n + 1 entries each; tot: dd_prefix_blocks(n) scratch)
 int dd_prefix_blocks(int n);
 void launch_dd_prefix(const double* t, int n, double2* tot1, double2* tot2, double2* P1, double2* P2,
@@ -55,7 +55,8 @@ void launch_dd_prefix(const double* t, int n, double2* tot1, double2* tot2, doub
 // advance + derive (+ seed rows when qt != nullptr) of one MERLIN length step
 void launch_next_length(const double* t, int n, int m, const double* mu_in, const double* sig_in, double* mu_out,
                         double* sig_out, float* df, float* dg, float* nrm, int* cr, int* cr_next, int L, int kA,
-                        int nb, double* qt, int* deg, const double2* P1, const double2* P2, cudaStream_t st);
+                        int nb, double* qt, int* deg, const double2* P1, const double2* P2, int* degc, int* deg2,
+                        cudaStream_t st);
 
 size_t scan_smem_bytes();
 void scan_configure();
@@ -74,7 +75,8 @@ void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const 
 // (degenerate row, any q) pair by the exact distance — kills and exact-nn keys
 // knife-edge recheck + degenerate pairs in one launch
 void launch_recheck(const double* t, int m, int N, const int2* pairs, const int* count, int cap, const int* list,
-                    const TryCtl* ctl, const int* crange, const int* deg, double r_sq, uint8_t* alive,
+                    const TryCtl* ctl, const int* crange, const int* degc, const int* deg2, const float* nrm,
+                    double r_sq, uint8_t* alive,
                     unsigned long long* nnkey, int rank, int world, const Peers& peers, cudaStream_t st);
 // overflow fallback: every listed row (ctl->alive of them) still alive x every
 // admissible q by the exact routine (kills + exact-nn keys)

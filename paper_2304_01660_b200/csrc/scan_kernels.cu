@@ -1095,35 +1095,70 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_ref_pairs(const double* __r
     }
 }
 
-// Degenerate rows (sigma < eps by the rolling statistics): the reference's
-// distance for such a window depends on its own one-pass statistics
-// (znormalize: all-zero z -> the 0 / 2m conventions, else tiny equal z), so
-// every pair that involves one is decided by the exact routine:
-//   A: every listed row still alive x every degenerate q (|c - q| >= m);
-//   B: every degenerate row x every q (|c - q| >= m).
-// d < r^2 kills the row; every d feeds its exact-nn key.  One warp per pair.
-// every pair with a degenerate row, decided exactly (dealt over the ranks)
+// Degenerate rows (sigma < eps by the rolling statistics, or statistics too
+// unreliable for the FP32 filter): the reference's distance for such a window
+// depends on its own one-pass statistics (znormalize, src/distance.cpp:8-22:
+// all-zero z -> the 0 / 2m conventions of reference_sq_dist,
+// src/pardrag.cpp:57-69; else tiny equal z), so no pair with one goes through
+// the FP32 model.  The windows were split per length (stats_kernels.cu
+// degenerate_row):
+//   one-pass constant (degc, cr[7]; their index range in cr[5], cr[6]): every
+//     pair's distance is a convention -- 0 against another such window, 2m
+//     against anything else -- so each row is decided in O(1):
+//     A1  a listed regular row with such a partner at |c - q| >= m: d = 2m;
+//     B1  such a row: nn = 0 if another one is at |c - q| >= m, else 2m if any
+//         admissible q exists;
+//   the others (deg2, cr[8]): the exact routine, one warp per pair:
+//     A2  every listed regular row still alive x every such q;
+//     B2  every such row still alive x every q (a dead row stops counting).
+// d < r^2 kills the row; every d feeds its exact-nn key.  Dealt over the ranks.
 __device__ __forceinline__ void degenerate_body(const double* __restrict__ t, int m, int N,
                                                 const int* __restrict__ list, const TryCtl* __restrict__ ctl,
-                                                const int* __restrict__ cr, const int* __restrict__ deg, double r_sq,
-                                                uint8_t* alive, unsigned long long* nnkey, int rank, int world,
-                                                const Peers& peers, double* buf) {
-    const int D = cr[2];
-    if (D == 0) return;
+                                                const int* __restrict__ cr, const int* __restrict__ degc,
+                                                const int* __restrict__ deg2, const float* __restrict__ nrm,
+                                                double r_sq, uint8_t* alive, unsigned long long* nnkey, int rank,
+                                                int world, const Peers& peers, double* buf) {
+    if (cr[2] == 0) return;
+    const int Dc = cr[7], D2 = cr[8];
+    const int cmin = N - cr[5], cmax = cr[6] - 1;
     const long long nl = ctl->alive;
-    const long long totA = nl * D, tot = totA + (long long)D * N;
+    const double two_m = 2.0 * (double)m;
+    // A1 + B1: one thread per row
+    const long long gt = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * world + rank;
+    const long long gs = (long long)gridDim.x * blockDim.x * world;
+    if (Dc > 0) {
+        for (long long e = gt; e < nl; e += gs) {
+            const int c = list[e];
+            if (!alive[c] || nrm[c] == 0.f) continue;  // degenerate rows: B1 / B2
+            if (c - cmin >= m || cmax - c >= m) {
+                if (two_m < r_sq) peer_kill(peers, alive, c);
+                peer_min_key(peers, nnkey, c, (unsigned long long)__double_as_longlong(two_m));
+            }
+        }
+        for (long long e = gt; e < Dc; e += gs) {
+            const int c = degc[e];
+            if (!(c >= m || N - 1 - c >= m)) continue;  // no admissible partner: nn stays +inf
+            const double d = (c - cmin >= m || cmax - c >= m) ? 0.0 : two_m;
+            if (d < r_sq) peer_kill(peers, alive, c);
+            peer_min_key(peers, nnkey, c, (unsigned long long)__double_as_longlong(d));
+        }
+    }
+    if (D2 == 0) return;
+    // A2 + B2: one warp per pair
+    const long long totA = nl * D2, tot = totA + (long long)D2 * N;
     const int w = threadIdx.x >> 5;
     for (long long e = ((long long)blockIdx.x * kPairWarps + w) * world + rank; e < tot;
          e += (long long)gridDim.x * kPairWarps * world) {
         int c, q;
         if (e < totA) {
-            c = list[e / D];
-            q = deg[e % D];
-            if (!alive[c]) continue;
+            c = list[e / D2];
+            q = deg2[e % D2];
+            if (!alive[c] || nrm[c] == 0.f) continue;
         } else {
             const long long f = e - totA;
-            c = deg[f / N];
+            c = deg2[f / N];
             q = (int)(f % N);
+            if (!alive[c]) continue;
         }
         if (abs(c - q) < m) continue;
         const double d = ref_dist_warp(t, m, c, q, buf);
@@ -1142,7 +1177,9 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_recheck(const double* __res
                                                              const int* __restrict__ list,
                                                              const TryCtl* __restrict__ ctl,
                                                              const int* __restrict__ cr,
-                                                             const int* __restrict__ deg, double r_sq,
+                                                             const int* __restrict__ degc,
+                                                             const int* __restrict__ deg2,
+                                                             const float* __restrict__ nrm, double r_sq,
                                                              uint8_t* alive, unsigned long long* nnkey,
                                                              int rank, int world, const Peers peers) {
     pdl_enter();
@@ -1158,7 +1195,7 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_recheck(const double* __res
             peer_kill(peers, alive, pr.y);
         }
     }
-    degenerate_body(t, m, N, list, ctl, cr, deg, r_sq, alive, nnkey, rank, world, peers, buf[w]);
+    degenerate_body(t, m, N, list, ctl, cr, degc, deg2, nrm, r_sq, alive, nnkey, rank, world, peers, buf[w]);
 }
 
 // Overflow fallback, the analogue of the reference's full exact pass for a
@@ -2068,10 +2105,11 @@ void launch_ref_pairs(int mode, const double* t, int m, const int2* pairs, const
 }
 
 void launch_recheck(const double* t, int m, int N, const int2* pairs, const int* count, int cap, const int* list,
-                    const TryCtl* ctl, const int* crange, const int* deg, double r_sq, uint8_t* alive,
-                    unsigned long long* nnkey, int rank, int world, const Peers& peers, cudaStream_t st) {
-    launch_pdl(k_recheck, 148 * 4, kPairWarps * 32, st, t, m, N, pairs, count, cap, list, ctl, crange, deg, r_sq,
-               alive, nnkey, rank, world, peers);
+                    const TryCtl* ctl, const int* crange, const int* degc, const int* deg2, const float* nrm,
+                    double r_sq, uint8_t* alive, unsigned long long* nnkey, int rank, int world, const Peers& peers,
+                    cudaStream_t st) {
+    launch_pdl(k_recheck, 148 * 4, kPairWarps * 32, st, t, m, N, pairs, count, cap, list, ctl, crange, degc, deg2,
+               nrm, r_sq, alive, nnkey, rank, world, peers);
 }
 
 void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const unsigned* ymax,

@@ -227,6 +227,26 @@ __device__ __forceinline__ float stats_err(const double2* __restrict__ P1, const
     return (2.f * ev + 2.f * eta + (float)kStatsRows * gam) * (1.f + 1e-5f) + 1e-30f;
 }
 
+// A degenerate window (sigma < eps, or statistics too unreliable for the FP32
+// filter): listed for the exact stage, split by the reference's own one-pass
+// test -- all-zero z windows get the 0 / 2m conventions in O(1) per row,
+// the others are evaluated exactly (scan_kernels.cu degenerate_body).  The
+// regular-window threshold carries a 1% margin over kSigmaEps so that no
+// regular window can be one-pass constant.
+__device__ __forceinline__ void degenerate_row(const double* __restrict__ t, int i, int m, int cnt, int* cr,
+                                               int* deg, int* degc, int* deg2) {
+    atomicMax(&cr[0], cnt - i);
+    atomicMax(&cr[1], i + 1);
+    deg[atomicAdd(&cr[2], 1)] = i;
+    if (onepass_const(t + i, m)) {
+        atomicMax(&cr[5], cnt - i);
+        atomicMax(&cr[6], i + 1);
+        degc[atomicAdd(&cr[7], 1)] = i;
+    } else {
+        deg2[atomicAdd(&cr[8], 1)] = i;
+    }
+}
+
 // block max of two non-negative floats (as int bits) into cr[3], cr[4]
 __device__ __forceinline__ void stats_max_commit(float a, float b2, int* cr) {
     __shared__ int sa[32], sb[32];
@@ -277,7 +297,8 @@ __global__ void k_advance(const double* __restrict__ t, int n, int m, double* __
 __global__ void k_derive(const double* __restrict__ t, int m, int cnt, const double* __restrict__ mu,
                          const double* __restrict__ sig, float* __restrict__ df,
                          float* __restrict__ dg, float* __restrict__ nrm, int* __restrict__ cr,
-                         int* __restrict__ deg, const double2* __restrict__ P1, const double2* __restrict__ P2) {
+                         int* __restrict__ deg, const double2* __restrict__ P1, const double2* __restrict__ P2,
+                         int* __restrict__ degc, int* __restrict__ deg2) {
     pdl_enter();
     const double sqm = sqrt((double)m), inv_m = 1.0 / (double)m;
     float amax = 0.f, bmax = 0.f;
@@ -287,12 +308,10 @@ __global__ void k_derive(const double* __restrict__ t, int m, int cnt, const dou
         const double s = sig[i];
         float b2 = 0.f;
         const float a = stats_err(P1, P2, i, m, inv_m, mu[i], s, b2);
-        const bool dgn = s < kSigmaEps || !(a <= (float)kStatsUnreliable);
+        const bool dgn = s < 1.01 * kSigmaEps || !(a <= (float)kStatsUnreliable);
         nrm[i] = dgn ? 0.f : (float)(1.0 / (sqm * s));
         if (dgn) {
-            atomicMax(&cr[0], cnt - i);
-            atomicMax(&cr[1], i + 1);
-            deg[atomicAdd(&cr[2], 1)] = i;  // decided exactly, against every q
+            degenerate_row(t, i, m, cnt, cr, deg, degc, deg2);
         } else {
             amax = fmaxf(amax, a);
             bmax = fmaxf(bmax, b2);
@@ -334,7 +353,8 @@ __global__ void __launch_bounds__(256, 6) k_next_length(const double* __restrict
                               double* __restrict__ sig_out, float* __restrict__ df, float* __restrict__ dg,
                               float* __restrict__ nrm, int* __restrict__ cr, int* __restrict__ cr_next, int L, int kA,
                               int nb, double* __restrict__ qt, int* __restrict__ deg,
-                              const double2* __restrict__ P1, const double2* __restrict__ P2) {
+                              const double2* __restrict__ P1, const double2* __restrict__ P2,
+                              int* __restrict__ degc, int* __restrict__ deg2) {
     pdl_enter();
     const int m1 = m + 1, cnt = n - m;
     if (blockIdx.x == 0 && threadIdx.x < kCrInts) cr_next[threadIdx.x] = 0;
@@ -355,12 +375,10 @@ __global__ void __launch_bounds__(256, 6) k_next_length(const double* __restrict
         sig_out[i] = s;
         float b2 = 0.f;
         const float ae = stats_err(P1, P2, i, m1, inv_m1, u, s, b2);
-        const bool dgn = s < kSigmaEps || !(ae <= (float)kStatsUnreliable);
+        const bool dgn = s < 1.01 * kSigmaEps || !(ae <= (float)kStatsUnreliable);
         nrm[i] = dgn ? 0.f : (float)(1.0 / (sqm * s));
         if (dgn) {
-            atomicMax(&cr[0], cnt - i);
-            atomicMax(&cr[1], i + 1);
-            deg[atomicAdd(&cr[2], 1)] = i;  // decided exactly, against every q
+            degenerate_row(t, i, m1, cnt, cr, deg, degc, deg2);
         } else {
             amax = fmaxf(amax, ae);
             bmax = fmaxf(bmax, b2);
@@ -412,8 +430,9 @@ void launch_advance_stats(const double* t, int n, int m, double* mu, double* sig
 
 void launch_derive(const double* t, int m, int cnt, const double* mu, const double* sig, float* df,
                    float* dg, float* nrm, int* crange, int* deg, const double2* P1, const double2* P2,
-                   cudaStream_t st) {
-    launch_pdl(k_derive, grid_for(cnt, 256), 256, st, t, m, cnt, mu, sig, df, dg, nrm, crange, deg, P1, P2);
+                   int* degc, int* deg2, cudaStream_t st) {
+    launch_pdl(k_derive, grid_for(cnt, 256), 256, st, t, m, cnt, mu, sig, df, dg, nrm, crange, deg, P1, P2, degc,
+               deg2);
 }
 
 int dd_prefix_blocks(int n) { return std::max(1, std::min(148 * 4, (n + 4095) / 4096)); }
@@ -429,9 +448,10 @@ void launch_dd_prefix(const double* t, int n, double2* tot1, double2* tot2, doub
 
 void launch_next_length(const double* t, int n, int m, const double* mu_in, const double* sig_in, double* mu_out,
                         double* sig_out, float* df, float* dg, float* nrm, int* cr, int* cr_next, int L, int kA,
-                        int nb, double* qt, int* deg, const double2* P1, const double2* P2, cudaStream_t st) {
+                        int nb, double* qt, int* deg, const double2* P1, const double2* P2, int* degc, int* deg2,
+                        cudaStream_t st) {
     launch_pdl(k_next_length, grid_for(n - m, 256), 256, st, t, n, m, mu_in, sig_in, mu_out, sig_out, df, dg, nrm, cr,
-               cr_next, L, kA, nb, qt, deg, P1, P2);
+               cr_next, L, kA, nb, qt, deg, P1, P2, degc, deg2);
 }
 
 }  // namespace tsd
