@@ -77,6 +77,8 @@ typedef struct {
     double heatmap_ms;      /* device time of the last heatmap column-max pass */
     uint64_t fallbacks;     /* tries that overflowed the knife-edge queue or the near-pair
                                buffer and finished with the exact pass over their live rows */
+    uint64_t wit_tests;     /* rows that tested the kill witness of an earlier try */
+    uint64_t wit_kills;     /* ... and were killed by it (before any walk) */
 } tsd_counters;
 
 /* ---- context ------------------------------------------------------------ */
@@ -264,6 +266,7 @@ int tsd_fp32_peak_probe(int device, double* tflops);
  *   seed_w          cost-model weight of a seed element vs a walked row
  *   seed32_track, seed32_collect           FP32 seeds in those launches
  *   track_chunks    tracked full-row chunks (1: one catch-all launch)
+ *   witness         kill witnesses of earlier tries tested before band pass 0 (1)
  *   fused_peers     rank groups: peer stores inside the kernels (1)
  *   scan_events     bracket scans with events (per-phase timing; slower)
  *   result_prefix   records copied back with the try's single sync */

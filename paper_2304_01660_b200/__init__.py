@@ -59,7 +59,8 @@ class Counters(C.Structure):
                 ("scan_ms", C.c_double), ("dense_ms", C.c_double), ("sparse_ms", C.c_double),
                 ("collect_ms", C.c_double), ("total_ms", C.c_double),
                 ("host_wall_ms", C.c_double), ("host_wait_ms", C.c_double),
-                ("heatmap_ms", C.c_double), ("fallbacks", C.c_uint64)]
+                ("heatmap_ms", C.c_double), ("fallbacks", C.c_uint64),
+                ("wit_tests", C.c_uint64), ("wit_kills", C.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -145,6 +145,7 @@ struct TryCtl {
     int tphase;     // 0 far chunks, 1 near chunk, 2 done
     int tpasses;    // tracked chunks that ran
     unsigned tepoch;  // try counter (k_try_init): tags the per-(row, band) bounds of this try
+    int wn;         // kill-witness candidates listed after band pass 0 (k_witness_list)
     double lk;      // top-k filter: need_top-th largest nn lower bound
     double cost[6]; // compaction: grouping cost per span (16..512), self-resetting
 };
@@ -236,8 +237,17 @@ struct ScanParams {
     long long ub_cap;      // entries available
     const int* list;       // the sorted list of the full-row stage (ctl->alive rows)
     int* exli;             // survivors' list index by row (k_survivors), read by the collection
-    unsigned long long* acc;  // accounting: [0] cells walked, [1] cells evaluated, [2] seed dots
+    unsigned long long* acc;  // accounting: [0] cells walked, [1] cells evaluated, [2] seed dots,
+                              // [3] witness rows tested, [4] witness kills
+    // Kill witnesses (MERLIN's consecutive tries): per row, the first of 9
+    // diagonals k (q = c + k .. c + k + 8) that killed it in an earlier try, or
+    // kNoWit.  Written by the stages after band pass 0 (nullptr: not recorded),
+    // tested by k_witness at the start of the next try.  Hints only: a witness
+    // kill is certified like any other, so stale entries cost a test, nothing else.
+    int* wit;
 };
+
+constexpr int kNoWit = (int)0x80808080;  // memset byte 0x80
 
 // canonical diagonal band of |k| for the per-(row, band) bounds: [m + b kW, m + (b+1) kW)
 __host__ __device__ __forceinline__ int ub_nbands(int N, int m) { return N > m ? (N - m + kW - 1) / kW : 0; }

@@ -134,6 +134,11 @@ struct tsd_ctx {
     DBuf<unsigned long long> ubk;
     DBuf<int> exli;
     int collect_skip = 1;
+    // kill witnesses across tries (ScanParams::wit): int per series index
+    DBuf<int> wit;
+    DBuf<int2> wl;  // the try's witness candidate runs
+    int witness = 1;
+    int witness_pre = 0, witness_pass0 = 0;  // experiments
     long long ub_entries = 1ll << 22;  // 32 MB
     DBuf<double> nnout;
     DBuf<int2> groups, slots;  // groups of the current stage; per-span candidate groups
@@ -176,6 +181,17 @@ struct tsd_ctx {
     float band_keep = 0.85f;  // band loop stops when a pass leaves more than this fraction alive
     float seed_w = 0.25f;  // grouping cost: one group-diagonal seed = seed_w*m walked row-diagonals (FP32 seeds)
     int band_few = 256;       // ... or when at most max(band_few, N/4096) rows are left (C2: 64 -> 41.8 ms, 256 -> 41.2 ms)
+    // With kill witnesses the rows left after pass 0 are few but mostly have
+    // near killers: the band passes go on down to band_few_wit rows (the full
+    // rows walk far diagonals first and would seed every far tile of them).
+    // Measured (rows left after which the band passes stop): C4 720 / 702 /
+    // 772 ms at 16 / 64 / 256, C3 432 / 426 ms at 16 / 64, C2 33.4 / 32.5 /
+    // 31.2 ms at 16 / 64 / 256.  0: automatic (256 below N = 2^18, else 64).
+    int band_few_wit = 0;
+    int few_rows(int64_t N) const {
+        if (!witness) return std::max<int>(band_few, (int)(N / 4096));
+        return band_few_wit > 0 ? band_few_wit : (N < (1 << 18) ? 256 : 64);
+    }
     int result_prefix = 1024;  // records copied back with the try's single round trip
     // knife-edge queue / near-pair buffer capacities (settable below the
     // allocation for tests of the overflow fallback)
@@ -513,7 +529,7 @@ struct tsd_ctx {
         slots.ensure(group_slots(N));
         bcost.ensure((size_t)compact_blocks(N) * 6);
         launch_compact_group(alive.p, N, list.p, lbstat.p, epoch, ctl.p, gate, groups.p, slots.p, (int)m,
-                             sparse_rows, band_keep, band_few, seed_w, bcost.p, band_slots(N), st);
+                             sparse_rows, band_keep, few_rows(N), seed_w, bcost.p, band_slots(N), st);
         ck(cudaGetLastError(), "compact");
         ctr.kernel_launches += 1;
         // fused peers: no rank's next scan may store kills into this rank's
@@ -546,7 +562,12 @@ struct tsd_ctx {
         cand.ensure(N);
         ythr.ensure(N);
         nnkey.ensure(N);
-        acc.ensure(3);
+        acc.ensure(5);
+        wl.ensure(N);
+        if (wit.cap < (size_t)n) {
+            wit.ensure((size_t)n);
+            ck(cudaMemsetAsync(wit.p, 0x80, (size_t)n * sizeof(int), st), "memset");  // kNoWit
+        }
         nnout.ensure(N);
         list.ensure(N);
         exli.ensure(N);
@@ -562,7 +583,7 @@ struct tsd_ctx {
         }
         h_ctl.ensure(1);
         h_int.ensure(8);
-        h_acc.ensure(4);
+        h_acc.ensure(5);
         h_ex.ensure(result_prefix);
         h_nn.ensure(result_prefix);
     }
@@ -574,6 +595,8 @@ struct tsd_ctx {
         ctr.cells_eval += hacc[1];
         ctr.seed_dots += hacc[2];
         ctr.seed_flops += hacc[2] * 2ull * (unsigned long long)m;
+        ctr.wit_tests += hacc[3];
+        ctr.wit_kills += hacc[4];
     }
 
     // Core PD3: survivors {c : nn(c)^2 >= r_sq} with exact nn, sorted like
@@ -615,6 +638,14 @@ struct tsd_ctx {
         if (peers.n > 1) peer_barrier();
         const ScanParams P = params(m, r_sq);
         std::vector<tsd_record> out;
+        int* const W = witness ? wit.p : nullptr;
+        if (W && witness_pre && r_sq > 0.0) {  // experiment: every row with a witness, before pass 0
+            ScanParams w = P;
+            w.wit = W;
+            launch_witness(w, wl.p, st);
+            ck(cudaGetLastError(), "witness");
+            ctr.kernel_launches += 2;
+        }
 
         // ---- band passes (PD3 selection): diagonals |k| in [K0, K0 + nb*kW) on
         // both sides of every undecided row; only certain FP32 kills.  Pass 0
@@ -649,7 +680,17 @@ struct tsd_ctx {
                     q.space = kSpaceBand;  // groups and bands set by the previous compaction
                 }
                 q.half = pass == 0 ? half_pass0 : (m >= half_bands_m ? half_bands : 1);
+                q.wit = (pass == 0 && !witness_pass0) ? nullptr : W;
                 scan(kPrune, q);
+                if (pass == 0 && W) {
+                    // rows killed after pass 0 in earlier tries test their killer
+                    // before the later bands are walked (k_witness)
+                    ScanParams w = P;
+                    w.wit = W;
+                    launch_witness(w, wl.p, st);
+                    ck(cudaGetLastError(), "witness");
+                    ctr.kernel_launches += 2;
+                }
                 reduce_alive(N);
                 compact(N, pass, m);
                 trace("band", m, r_sq, pass);
@@ -667,6 +708,7 @@ struct tsd_ctx {
         // covers whatever chunks the enqueued count did not reach.
         ScanParams q = P;
         q.seed32 = seed32_track;
+        q.wit = W;
         // collection skip: single catch-all full-row launch, one rank (a row's
         // band may span two tiles dealt to different ranks)
         if (collect_skip && ubk.p && world == 1 && (track_chunks <= 1)) {
@@ -698,7 +740,7 @@ struct tsd_ctx {
         // degenerate rows: every pair with one is decided exactly.  One launch.
         launch_recheck(t.p, (int)m, N, queue.p, &C->queue, queue_cap, list.p, C, cr_cur, degc.p, deg2.p, nrm.p,
                        r_sq, alive.p,
-                       nnkey.p, rank, world, peers, st);
+                       nnkey.p, rank, world, peers, W, st);
         ck(cudaGetLastError(), "recheck");
         reduce_alive(N);
 
@@ -711,6 +753,7 @@ struct tsd_ctx {
         const int* ex = cand.p;  // rows whose exact nn is computed (count: C->ec)
         q.space = kSpaceFull;  // every diagonal of the exact-nn rows' groups
         q.seed32 = seed32_collect;
+        q.wit = nullptr;
         scan(kCollect, q);
         launch_ref_pairs(1, t.p, (int)m, coll.p, &C->coll, coll_cap, r_sq, alive.p, nnkey.p, C,
                          world == 1 ? ex : nullptr, nnout.p, peers, st);
@@ -728,7 +771,7 @@ struct tsd_ctx {
         // bounded prefix of the records (the rest only if there are more)
         const int pf = std::min(N, result_prefix);
         ck(cudaMemcpyAsync(h_ctl.p, C, sizeof(TryCtl), cudaMemcpyDeviceToHost, st), "D2H");
-        ck(cudaMemcpyAsync(h_acc.p, acc.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaMemcpyAsync(h_acc.p, acc.p, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "D2H");
         ck(cudaMemcpyAsync(h_ex.p, ex, pf * sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
         ck(cudaMemcpyAsync(h_nn.p, nnout.p, pf * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
         sync();
@@ -1070,6 +1113,7 @@ int tsd_series_set(tsd_ctx* c, const double* v, int64_t n) {
         c->stats_m = -1;
         c->derived_m = -1;
         c->seed_m = -1;
+        if (c->wit.p) ck(cudaMemset(c->wit.p, 0x80, c->wit.cap * sizeof(int)), "memset");  // witnesses of the old series
     });
 }
 
@@ -1817,6 +1861,10 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "band_passes") c->band_passes = std::max(1, std::min(64, (int)v));
         else if (k == "result_prefix") c->result_prefix = std::max(16, std::min(1 << 20, (int)v));
         else if (k == "collect_skip") c->collect_skip = v != 0.0;
+        else if (k == "witness") c->witness = v != 0.0;
+        else if (k == "witness_pre") c->witness_pre = v != 0.0;
+        else if (k == "witness_pass0") c->witness_pass0 = v != 0.0;
+        else if (k == "band_few_wit") c->band_few_wit = std::max(0, (int)v);
         else if (k == "queue_cap") c->queue_cap = std::max(1, std::min(kQueueCap, (int)v));
         else if (k == "coll_cap") c->coll_cap = std::max(1, std::min(kCollCap, (int)v));
         else fail(TSD_EINVAL, "unknown parameter " + k);

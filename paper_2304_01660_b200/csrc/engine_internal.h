@@ -77,12 +77,14 @@ void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const 
 void launch_recheck(const double* t, int m, int N, const int2* pairs, const int* count, int cap, const int* list,
                     const TryCtl* ctl, const int* crange, const int* degc, const int* deg2, const float* nrm,
                     double r_sq, uint8_t* alive,
-                    unsigned long long* nnkey, int rank, int world, const Peers& peers, cudaStream_t st);
+                    unsigned long long* nnkey, int rank, int world, const Peers& peers, int* wit, cudaStream_t st);
 // overflow fallback: every listed row (ctl->alive of them) still alive x every
 // admissible q by the exact routine (kills + exact-nn keys)
 void launch_exact_rows(const double* t, int m, int N, const int* list, const TryCtl* ctl, double r_sq,
                        uint8_t* alive, unsigned long long* nnkey, int rank, int world, const Peers& peers,
                        cudaStream_t st);
+// kill witnesses of earlier tries tested before band pass 0 (ScanParams::wit)
+void launch_witness(const ScanParams& p, int2* wl, cudaStream_t st);  // wl: N entries of scratch
 void launch_try_init(uint8_t* alive, unsigned* ymax, unsigned* emax, float* ythr, unsigned long long* nnkey, int N,
                      TryCtl* ctl, unsigned long long* acc, int band_k0, cudaStream_t st);
 int compact_blocks(int n);

@@ -138,7 +138,7 @@ struct F9 {
 __device__ __noinline__ void slow_track(const F9 x, const F9 qn, float tz, float cw, int c, int u0, int dir,
                                         int qbase, int N, int m, double r_sq, double thr0, double E, double xs,
                                         uint8_t* alive, uint8_t* const* peer_alive, int npeer, int2* queue,
-                                        int* queue_count, int queue_cap) {
+                                        int* queue_count, int queue_cap, int* wit) {
 #pragma unroll
     for (int j = 0; j < kDiag; ++j) {
         if (!(x.v[j] > tz)) continue;
@@ -159,6 +159,7 @@ __device__ __noinline__ void slow_track(const F9 x, const F9 qn, float tz, float
         if (corr - ec > thr0) {
             if (npeer > 1) for (int r = 0; r < npeer; ++r) peer_alive[r][c] = 0;
             else alive[c] = 0;
+            if (wit) wit[c] = q - c - kDiag / 2;  // the killer in the middle of the next try's 9
         } else if (corr + ec >= thr0) {
             const int at = atomicAdd(queue_count, 1);
             if (at < queue_cap) queue[at] = make_int2(c, q);
@@ -623,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
                         }
                         slow_track(xv, qv, cr.z, cr.w, dir > 0 ? td.r0 + ss : r_end - ss, ss + ub, dir, qbase, N,
                                    m, p.r_sq, p.thr0, E, xs, p.alive, s_peer_alive, p.peers.n, p.queue,
-                                   p.queue_count, p.queue_cap);
+                                   p.queue_count, p.queue_cap, p.wit);
                     }
                     if (S.ykey[ss] != 0u) {
                         // row max of the FP32 route value x = cov*qn over valid q (NaN for
@@ -662,6 +663,17 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
             if (lane < kDiag && ((h >> lane) & 1u)) {
                 const int ss = s0 + lane;
                 peer_kill(p.peers, p.alive, dir > 0 ? td.r0 + ss : r_end - ss);
+            }
+            if (p.wit != nullptr && hit != 0u) {
+                // witnesses for the next try: this thread's 9 diagonals killed the
+                // rows of its hit steps (benign races: any killer will do)
+                const int kb = dir > 0 ? td.k0 + ub : td.k0 + kW - kDiag - ub;
+                unsigned hh = hit;
+                while (hh) {
+                    const int ss = s0 + __ffs(hh) - 1;
+                    hh &= hh - 1u;
+                    if (ss < rows) p.wit[dir > 0 ? td.r0 + ss : r_end - ss] = kb;
+                }
             }
         }
     }
@@ -1181,7 +1193,7 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_recheck(const double* __res
                                                              const int* __restrict__ deg2,
                                                              const float* __restrict__ nrm, double r_sq,
                                                              uint8_t* alive, unsigned long long* nnkey,
-                                                             int rank, int world, const Peers peers) {
+                                                             int rank, int world, const Peers peers, int* wit) {
     pdl_enter();
     __shared__ double buf[kPairWarps][256];
     const int w = threadIdx.x >> 5;
@@ -1193,9 +1205,210 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_recheck(const double* __res
         if ((threadIdx.x & 31) == 0 && d < r_sq) {
             peer_kill(peers, alive, pr.x);
             peer_kill(peers, alive, pr.y);
+            if (wit) {
+                wit[pr.x] = pr.y - pr.x - kDiag / 2;
+                wit[pr.y] = pr.x - pr.y - kDiag / 2;
+            }
         }
     }
     degenerate_body(t, m, N, list, ctl, cr, degc, deg2, nrm, r_sq, alive, nnkey, rank, world, peers, buf[w]);
+}
+
+// ---------------------------------------------------------------------------
+// Kill witnesses (MERLIN: consecutive tries over lengths m, m+1, ... and the
+// retries of one length see nearly the same distance matrix).  A row that was
+// killed after band pass 0 in an earlier try remembers the 9 diagonals of its
+// killer (ScanParams::wit: q = c + w .. c + w + 8).  Right after band pass 0 of
+// the next try, the rows still alive that have a witness test those 9 cells
+// before any later band is walked.  Witnesses come in runs (one diagonal
+// kills consecutive rows), so k_witness_list cuts the candidates into runs of
+// consecutive rows with the same witness (within 32-row chunks), and
+// k_witness takes one run per warp:
+//   seed  QT(c0, q) = sum_p (t[c0+p] - A)(t[q+p] - B) at the run's first row
+//         (A = mu_c0, B = mu of the middle q: small products under a DC
+//         offset), the warp staging chunks of both windows in shared memory;
+//   walk  lanes 0..8 carry one diagonal each down the run in FP64:
+//         QT(c+1, q+1) = QT(c, q) - (t[c]-A)(t[q]-B) + (t[c+m]-A)(t[q+m]-B),
+//         D(c+1) = D(c) - (t[c]-A) + (t[c+m]-A) with D(c) = sum_p (t[c+p]-A);
+//   cov(c, q) = QT - (mu_q - B) D(c)  (exact identity with the true means; the
+//         rolling means' error is in the statistics band), rounding bounded by
+//         (m + 8 + 4 s) u m wa (wb + |mu_q - B|) + 4u(|QT| + |cov|), wa / wb the
+//         largest |t - A| / |t - B| touched;
+//   corr = cov / (m sigma_c sigma_q) kills c and q when
+//         corr - (rounding + kSlack + statistics band) > thr0 (d(c, q) < r:
+//         neither is a range discord), like a certain kill of the walk.
+// Degenerate and constant windows never take part.  A row that survives its
+// witness loses it.  The result is unchanged (every kill is certain); the later
+// band passes and the full rows walk fewer groups, and the direct seeds those
+// groups need are the bulk of their cost.
+constexpr int kWitWarps = 8;
+constexpr int kWitChunk = 256;
+
+// candidate runs (first row, length): alive rows with the same witness,
+// consecutive within a 32-row chunk (warp-aggregated append)
+__global__ void k_witness_list(const ScanParams p, int2* __restrict__ wl) {
+    pdl_enter();
+    const int lane = threadIdx.x & 31;
+    for (int c0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; c0 < p.N; c0 += gridDim.x * blockDim.x) {
+        const int c = c0 + lane;
+        int wv = kNoWit;
+        if (c < p.N && p.alive[c] && p.nrm[c] > 0.f) wv = p.wit[c];  // not constant / degenerate
+        const bool want = wv != kNoWit;
+        const unsigned wm = __ballot_sync(0xffffffffu, want);
+        if (!wm) continue;
+        const int pw = __shfl_up_sync(0xffffffffu, wv, 1);
+        const bool start = want && (lane == 0 || pw != wv);
+        const unsigned sm = __ballot_sync(0xffffffffu, start);
+        int at = 0;
+        if (lane == 0) at = atomicAdd(&p.ctl->wn, __popc(sm));
+        at = __shfl_sync(0xffffffffu, at, 0);
+        if (start) {
+            const unsigned brk = lane < 31 ? (sm | ~wm) >> (lane + 1) : 0u;  // lanes that end the run
+            const int len = brk ? __ffs(brk) : 32 - lane;
+            wl[at + __popc(sm & ((1u << lane) - 1u))] = make_int2(c, len);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kWitWarps * 32) k_witness(const ScanParams p, const int2* __restrict__ wl) {
+    pdl_enter();
+    __shared__ __align__(16) double s_a[kWitWarps][kWitChunk];
+    __shared__ __align__(16) double s_w[kWitWarps][kWitChunk + 16];
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    double* const sa = s_a[wp];
+    double* const sw = s_w[wp];
+    const int N = p.N, m = p.m;
+    const double xs = stats_band(p, false) + kSlack + 1e-12;
+    const int total = p.ctl->wn;
+    unsigned long long tests = 0, kills = 0;
+    for (int e = blockIdx.x * kWitWarps + wp; e < total; e += gridDim.x * kWitWarps) {
+        const int2 run = wl[e];
+        const int c0 = run.x;
+        const int kb = p.wit[c0];
+        if (kb == kNoWit) continue;  // defensive: the run's rows share this witness
+        const int q0 = c0 + kb;
+        const double A = p.mu[c0];
+        const double B = p.mu[min(max(q0 + kDiag / 2, 0), N - 1)];
+        double acc[kDiag];
+#pragma unroll
+        for (int j = 0; j < kDiag; ++j) acc[j] = 0.0;
+        double delta = 0.0, wa = 0.0, wb = 0.0;
+        for (int pc = 0; pc < m; pc += kWitChunk) {
+            const int len = min(kWitChunk, m - pc);
+            // all loads of the chunk in flight before the first shared store
+            constexpr int kWv = (kWitChunk + 16 + 31) / 32;  // window loads per lane (ceil)
+            double av[kWitChunk / 32], wv0[kWv];
+#pragma unroll
+            for (int i = 0; i < kWitChunk / 32; ++i) {
+                const int x = lane + 32 * i;
+                av[i] = x < len ? p.t[c0 + pc + x] - A : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < kWv; ++i) {
+                const int x = lane + 32 * i;
+                const int g = q0 + pc + x;
+                wv0[i] = (x < len + kDiag - 1 && g >= 0 && g < p.n) ? p.t[g] - B : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < kWitChunk / 32; ++i) {
+                sa[lane + 32 * i] = av[i];
+                delta += av[i];
+                wa = fmax(wa, fabs(av[i]));
+            }
+#pragma unroll
+            for (int i = 0; i < kWv; ++i) {
+                if (lane + 32 * i < kWitChunk + 16) sw[lane + 32 * i] = wv0[i];
+                wb = fmax(wb, fabs(wv0[i]));
+            }
+            __syncwarp();
+            // lane l: p = 4l .. 4l+3 of each 128-element half
+#pragma unroll
+            for (int h = 0; h < kWitChunk; h += 128) {
+                double a4[4], w12[12];
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const double2 v = reinterpret_cast<const double2*>(sa + h + 4 * lane)[i];
+                    a4[2 * i] = v.x;
+                    a4[2 * i + 1] = v.y;
+                }
+#pragma unroll
+                for (int i = 0; i < 6; ++i) {
+                    const double2 v = reinterpret_cast<const double2*>(sw + h + 4 * lane)[i];
+                    w12[2 * i] = v.x;
+                    w12[2 * i + 1] = v.y;
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < kDiag; ++j) acc[j] = fma(a4[i], w12[i + j], acc[j]);
+            }
+            __syncwarp();
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+            for (int j = 0; j < kDiag; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+            delta += __shfl_xor_sync(0xffffffffu, delta, o);
+            wa = fmax(wa, __shfl_xor_sync(0xffffffffu, wa, o));
+            wb = fmax(wb, __shfl_xor_sync(0xffffffffu, wb, o));
+        }
+        // lane j < 9 walks diagonal q = c + kb + j down the run
+        double qt = 0.0;
+#pragma unroll
+        for (int j = 0; j < kDiag; ++j)
+            if (j == lane) qt = acc[j];
+        const double u_m = (double)m * kEps64;
+        for (int s = 0; s < run.y; ++s) {
+            const int c = c0 + s;
+            const int q = c + kb + lane;
+            if (s > 0) {
+                const double to = p.t[c - 1] - A, tn = p.t[c + m - 1] - A;
+                double qo = 0.0, qn = 0.0;
+                if (lane < kDiag) {
+                    const int g0 = q - 1, g1 = q + m - 1;
+                    qo = (g0 >= 0 && g0 < p.n) ? p.t[g0] - B : 0.0;
+                    qn = (g1 >= 0 && g1 < p.n) ? p.t[g1] - B : 0.0;
+                }
+                qt = fma(tn, qn, fma(-to, qo, qt));
+                delta = delta - to + tn;
+                wa = fmax(wa, fabs(tn));
+                wb = fmax(wb, fabs(qn));
+            }
+            if (!p.alive[c]) continue;  // killed as an earlier witness's partner (warp-uniform)
+            bool kill = false;
+            if (lane < kDiag && q >= 0 && q < N && abs(q - c) >= m && p.nrm[q] > 0.f) {
+                const double dmu = p.mu[q] - B;
+                const double cov = qt - dmu * delta;
+                const double den = (double)m * p.sig[c] * p.sig[q];
+                const double err = ((double)(m + 8 + 4 * s) * u_m * wa * (wb + fabs(dmu)) +
+                                    4.0 * kEps64 * (fabs(qt) + fabs(cov))) /
+                                   den;
+                kill = cov / den - (err + xs) > p.thr0;
+            }
+            const unsigned km = __ballot_sync(0xffffffffu, kill);
+            if (km) {
+                if (lane == __ffs(km) - 1) {
+                    peer_kill(p.peers, p.alive, c);
+                    peer_kill(p.peers, p.alive, q);
+                    p.wit[c] = q - c - kDiag / 2;  // re-centred on the killing diagonal
+                    p.wit[q] = c - q - kDiag / 2;  // the partner's witness for the next try
+                }
+                ++kills;
+            } else if (lane == 0) {
+                p.wit[c] = kNoWit;
+            }
+            ++tests;
+        }
+    }
+    if (lane == 0 && tests) {
+        atomicAdd(&p.acc[3], tests);
+        atomicAdd(&p.acc[4], kills);
+    }
+}
+
+void launch_witness(const ScanParams& p, int2* wl, cudaStream_t st) {
+    launch_pdl(k_witness_list, std::max(1, std::min((p.N + 255) / 256, 148 * 8)), 256, st, p, wl);
+    launch_pdl(k_witness, 148 * 2, kWitWarps * 32, st, p, (const int2*)wl);
 }
 
 // Overflow fallback, the analogue of the reference's full exact pass for a
@@ -1259,8 +1472,9 @@ __global__ void k_try_init(uint8_t* __restrict__ alive, unsigned* __restrict__ y
         ctl->bK0 = band_k0;
         ctl->bnb = 0;
         ctl->lk = 0.0;
+        ctl->wn = 0;
         ctl->tepoch += 1;
-        acc[0] = acc[1] = acc[2] = 0ull;
+        acc[0] = acc[1] = acc[2] = acc[3] = acc[4] = 0ull;
     }
 }
 
@@ -1690,7 +1904,7 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
             const int prev = ctl->alive;
             ctl->prev = prev;
             ctl->passes = gate + 1;
-            if (total == 0 || total <= max(band_few, n / 4096)) {
+            if (total == 0 || total <= band_few) {
                 ctl->stop = gate;
                 ctl->stop_why = 1;
             } else if ((double)total > (double)band_keep * (double)prev) {
@@ -2107,9 +2321,9 @@ void launch_ref_pairs(int mode, const double* t, int m, const int2* pairs, const
 void launch_recheck(const double* t, int m, int N, const int2* pairs, const int* count, int cap, const int* list,
                     const TryCtl* ctl, const int* crange, const int* degc, const int* deg2, const float* nrm,
                     double r_sq, uint8_t* alive, unsigned long long* nnkey, int rank, int world, const Peers& peers,
-                    cudaStream_t st) {
+                    int* wit, cudaStream_t st) {
     launch_pdl(k_recheck, 148 * 4, kPairWarps * 32, st, t, m, N, pairs, count, cap, list, ctl, crange, degc, deg2,
-               nrm, r_sq, alive, nnkey, rank, world, peers);
+               nrm, r_sq, alive, nnkey, rank, world, peers, wit);
 }
 
 void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const unsigned* ymax,

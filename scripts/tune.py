@@ -33,4 +33,5 @@ for combo in itertools.product(*grid.values()) if grid else [()]:
     base = base or key
     c = best
     print(dict(zip(grid.keys(), combo)), f"total {c['total_ms']:.2f} ms scan {c['scan_ms']:.2f} dense {c['dense_ms']:.2f} "
-          f"sparse {c['sparse_ms']:.2f} collect {c['collect_ms']:.2f} syncs {c['host_syncs']} same={same}", flush=True)
+          f"sparse {c['sparse_ms']:.2f} collect {c['collect_ms']:.2f} syncs {c['host_syncs']} "
+          f"launches {c['kernel_launches']} seeds {c['seed_dots']} wit {c['wit_kills']}/{c['wit_tests']} same={same}", flush=True)
