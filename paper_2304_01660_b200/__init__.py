@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtsdiscord_b200.so")
+LIB_PATH = os.environ.get("TSD_LIB") or os.path.join(HERE, "libtsdiscord_b200.so")  # TSD_LIB: A/B experiments
 
 TSD_OK, TSD_EINVAL, TSD_ELOGIC, TSD_ERUNTIME, TSD_ECUDA = range(5)
 

@@ -245,9 +245,22 @@ struct ScanParams {
     // tested by k_witness at the start of the next try.  Hints only: a witness
     // kill is certified like any other, so stale entries cost a test, nothing else.
     int* wit;
+    // Row cache (full rows / collection): resident raw QT rows of up to
+    // kRcSlots anchor rows near the previous tries' survivors, valid for this
+    // length (rc_n = 0: none); slot s holds QT(rc_row[s], q) at rcqt[s * rc_stride + q]
+    const double* rcqt;
+    long long rc_stride;
+    int rc_n;
+    int rc_row[8];
+};
+constexpr int kRcSlots = 8;
+struct RcRows {  // the anchor rows of the row-cache slots (-1: empty)
+    int row[kRcSlots];
+    int n;
 };
 
 constexpr int kNoWit = (int)0x80808080;  // memset byte 0x80
+constexpr int kWitMaxM = 1024;           // witness tests stage whole windows: lengths up to this
 
 // canonical diagonal band of |k| for the per-(row, band) bounds: [m + b kW, m + (b+1) kW)
 __host__ __device__ __forceinline__ int ub_nbands(int N, int m) { return N > m ? (N - m + kW - 1) / kW : 0; }

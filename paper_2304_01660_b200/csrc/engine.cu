@@ -135,6 +135,110 @@ struct tsd_ctx {
     DBuf<int> exli;
     int collect_skip = 1;
     // kill witnesses across tries (ScanParams::wit): int per series index
+    // row cache (ScanParams::rcqt): resident raw QT rows of anchor rows next to
+    // the previous tries' exact-nn rows, advanced with the lengths
+    int row_cache = 1;
+    DBuf<double> rcqt;
+    DBuf<int> surv;  // every survivor of the try (k_survivors), read back for the anchors
+    RcRows rc{};
+    int rc_age[kRcSlots] = {};
+    int64_t rc_m = -1;  // length every filled slot holds (-1: none)
+    int64_t rc_fills = 0;
+    int rc_keep = 2;  // tries a slot survives without being needed
+    // Short windows seed cheaply (m FMA per diagonal) while a fill costs N m
+    // FMA and every slot N FMA per length: the cache pays from m ~ 384 on
+    // (measured with the cache at every length: C4 -5%, C5 -1.4%, C3 +1.6%,
+    // C2 +1%).
+    int64_t rc_min_m = 384;
+    bool rc_on(int64_t m) const { return row_cache && m >= rc_min_m; }
+    void rc_reset() {
+        rc_m = -1;
+        rc.n = kRcSlots;
+        for (int s = 0; s < kRcSlots; ++s) {
+            rc.row[s] = -1;
+            rc_age[s] = 0;
+        }
+    }
+    // stats went m -> m+1: advance the slots with them (or drop them)
+    void rc_step(int64_t m) {
+        if (rc_m != m) return;
+        const int64_t N1 = n - m;
+        bool any = false;
+        for (int s = 0; s < kRcSlots; ++s) {
+            if (rc.row[s] >= N1) rc.row[s] = -1;
+            any |= rc.row[s] >= 0;
+        }
+        if (!any) {
+            rc_m = -1;
+            return;
+        }
+        launch_rc_advance(t.p, (int)n, (int)m, rc, (long long)n, rcqt.p, st);
+        ck(cudaGetLastError(), "rc advance");
+        ctr.kernel_launches += 1;
+        rc_m = m + 1;
+    }
+    // after a MERLIN try at length m: anchors just before / after every
+    // cluster of the exact-nn rows (the discord regions recur from length to
+    // length); a missing anchor evicts the least recently needed slot and is
+    // filled at m (N m FMA, once per region)
+    static constexpr int kRcMargin = 16, kRcTol = 48, kRcGap = 64;
+    void rc_update(int64_t m, const int* ex, int ec) {
+        if (!rc_on(m) || ec <= 0) {
+            if (rc_m >= 0 && !rc_on(m + 1)) rc_reset();  // below the length gate: nothing to carry
+            return;
+        }
+        const int N = (int)(n - m + 1);
+        if (rc_m != m) {
+            for (int s = 0; s < kRcSlots; ++s) rc.row[s] = -1;
+            rc_m = m;
+        }
+        rc.n = kRcSlots;
+        std::vector<int> v(ex, ex + ec);
+        std::sort(v.begin(), v.end());
+        std::vector<std::pair<int, int>> cl;  // clusters (lo, hi)
+        for (int x : v) {
+            if (!cl.empty() && x - cl.back().second <= kRcGap) cl.back().second = x;
+            else cl.push_back({x, x});
+        }
+        std::stable_sort(cl.begin(), cl.end(), [](const std::pair<int, int>& x, const std::pair<int, int>& y) {
+            return x.second - x.first > y.second - y.first;
+        });
+        bool used[kRcSlots] = {};
+        int wanted = 0;
+        for (const auto& c2 : cl) {
+            if (wanted + 2 > kRcSlots) break;
+            for (int side = 0; side < 2; ++side) {
+                ++wanted;
+                int hit = -1;
+                for (int s = 0; s < kRcSlots; ++s) {
+                    const int r = rc.row[s];
+                    if (r < 0) continue;
+                    const int d = side == 0 ? c2.first - r : r - c2.second;
+                    if (d >= 0 && d <= kRcTol) hit = s;
+                }
+                if (hit < 0) {
+                    int best = -1;
+                    for (int s = 0; s < kRcSlots; ++s)
+                        if (!used[s] && (best < 0 || rc.row[s] < 0 && rc.row[best] >= 0 ||
+                                         (rc.row[s] < 0) == (rc.row[best] < 0) && rc_age[s] > rc_age[best]))
+                            best = s;
+                    if (best < 0) continue;
+                    hit = best;
+                    rc.row[hit] = side == 0 ? std::max(0, c2.first - kRcMargin) : std::min(N - 1, c2.second + kRcMargin);
+                    rcqt.ensure((size_t)kRcSlots * (size_t)n);
+                    launch_rc_fill(t.p, (int)n, (int)m, rc.row[hit], rcqt.p + (size_t)hit * (size_t)n, st);
+                    ck(cudaGetLastError(), "rc fill");
+                    ctr.kernel_launches += 1;
+                    ++rc_fills;
+                }
+                used[hit] = true;
+            }
+        }
+        for (int s = 0; s < kRcSlots; ++s) {
+            rc_age[s] = used[s] ? 0 : rc_age[s] + 1;
+            if (rc_age[s] > rc_keep) rc.row[s] = -1;  // not needed lately: stop advancing it
+        }
+    }
     DBuf<int> wit;
     DBuf<int2> wl;  // the try's witness candidate runs
     int witness = 1;
@@ -147,7 +251,7 @@ struct tsd_ctx {
     DBuf<unsigned long long> lbstat;  // compaction look-back status words
     unsigned epoch = 0;
     HBuf<TryCtl> h_ctl;
-    HBuf<int> h_int, h_ex;
+    HBuf<int> h_int, h_ex, h_surv;
     HBuf<unsigned long long> h_acc;
     HBuf<double> h_nn;
 
@@ -563,6 +667,7 @@ struct tsd_ctx {
         ythr.ensure(N);
         nnkey.ensure(N);
         acc.ensure(5);
+        surv.ensure(N);
         wl.ensure(N);
         if (wit.cap < (size_t)n) {
             wit.ensure((size_t)n);
@@ -585,6 +690,7 @@ struct tsd_ctx {
         h_int.ensure(8);
         h_acc.ensure(5);
         h_ex.ensure(result_prefix);
+        h_surv.ensure(result_prefix);
         h_nn.ensure(result_prefix);
     }
 
@@ -638,7 +744,7 @@ struct tsd_ctx {
         if (peers.n > 1) peer_barrier();
         const ScanParams P = params(m, r_sq);
         std::vector<tsd_record> out;
-        int* const W = witness ? wit.p : nullptr;
+        int* const W = witness && m <= kWitMaxM ? wit.p : nullptr;
         if (W && witness_pre && r_sq > 0.0) {  // experiment: every row with a witness, before pass 0
             ScanParams w = P;
             w.wit = W;
@@ -709,6 +815,12 @@ struct tsd_ctx {
         ScanParams q = P;
         q.seed32 = seed32_track;
         q.wit = W;
+        if (rc_on(m) && need_top > 0 && rc_m == m) {  // full rows + collection seed from the row cache
+            q.rcqt = rcqt.p;
+            q.rc_stride = (long long)n;
+            q.rc_n = kRcSlots;
+            for (int s = 0; s < kRcSlots; ++s) q.rc_row[s] = rc.row[s] < N ? rc.row[s] : -1;
+        }
         // collection skip: single catch-all full-row launch, one rank (a row's
         // band may span two tiles dealt to different ranks)
         if (collect_skip && ubk.p && world == 1 && (track_chunks <= 1)) {
@@ -748,7 +860,7 @@ struct tsd_ctx {
         // CTA filters the list to the survivors, applies the MERLIN top-k
         // filter, resets their keys and groups them.
         launch_survivors(list.p, alive.p, C, ymax.p, emax.p, nrm.p, cr_cur, N, (int)m, (int)need_top, bnd_lo.p,
-                         bnd_hi.p, cand.p, ythr.p, nnkey.p, groups.p, sparse_rows, seed_w, exli.p, st);
+                         bnd_hi.p, cand.p, ythr.p, nnkey.p, groups.p, sparse_rows, seed_w, exli.p, rc_on(m) ? surv.p : nullptr, st);
         ck(cudaGetLastError(), "survivors");
         const int* ex = cand.p;  // rows whose exact nn is computed (count: C->ec)
         q.space = kSpaceFull;  // every diagonal of the exact-nn rows' groups
@@ -773,6 +885,8 @@ struct tsd_ctx {
         ck(cudaMemcpyAsync(h_ctl.p, C, sizeof(TryCtl), cudaMemcpyDeviceToHost, st), "D2H");
         ck(cudaMemcpyAsync(h_acc.p, acc.p, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "D2H");
         ck(cudaMemcpyAsync(h_ex.p, ex, pf * sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+        if (rc_on(m) && need_top > 0)
+            ck(cudaMemcpyAsync(h_surv.p, surv.p, pf * sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
         ck(cudaMemcpyAsync(h_nn.p, nnout.p, pf * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
         sync();
         const TryCtl hc = *h_ctl.p;
@@ -819,6 +933,7 @@ struct tsd_ctx {
             hex = ex_big.data();
             hnn = nn_big.data();
         }
+        if (need_top > 0 && rc_on(m)) rc_update(m, h_surv.p, std::min(hc.sc, pf));
         out.reserve(ec);
         for (int e = 0; e < ec; ++e) {
             const int c = hex[e];
@@ -1055,6 +1170,11 @@ void tsd_ctx_destroy(tsd_ctx* c) {
     c->ctl.release();
     c->h_ctl.release();
     c->h_ex.release();
+    c->h_surv.release();
+    c->surv.release();
+    c->rcqt.release();
+    c->wit.release();
+    c->wl.release();
     c->h_nn.release();
     c->h_int.release();
     c->h_acc.release();
@@ -1114,6 +1234,7 @@ int tsd_series_set(tsd_ctx* c, const double* v, int64_t n) {
         c->derived_m = -1;
         c->seed_m = -1;
         if (c->wit.p) ck(cudaMemset(c->wit.p, 0x80, c->wit.cap * sizeof(int)), "memset");  // witnesses of the old series
+        c->rc_reset();
     });
 }
 
@@ -1320,6 +1441,9 @@ int tsd_merlin(tsd_ctx* c, int64_t min_len, int64_t max_len, const tsd_merlin_op
         // keeps every band-0 diagonal a non-self match at every length)
         c->seed_m = -1;
         if ((int64_t)max_len + kW < n - max_len + 1) c->seed_init(min_len, max_len);
+        c->rc_reset();
+        // every discovery starts from scratch: no kill witnesses from an earlier call
+        if (c->wit.p) ck(cudaMemsetAsync(c->wit.p, 0x80, c->wit.cap * sizeof(int), c->st), "memset");
         for (int64_t m = min_len; m <= max_len; ++m) {
             const int64_t k = m - min_len;
             counts[k] = 0;
@@ -1331,6 +1455,7 @@ int tsd_merlin(tsd_ctx* c, int64_t min_len, int64_t max_len, const tsd_merlin_op
                     c->init_stats_dev(m);
                     if (c->seed_m == m - 1) c->seed_advance();
                 }
+                c->rc_step(m - 1);
             }
             const int phase = m == min_len ? 0 : (m < min_len + 5 ? 1 : 2);
             if (phase != 0 && history.empty()) {
@@ -1862,6 +1987,8 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "result_prefix") c->result_prefix = std::max(16, std::min(1 << 20, (int)v));
         else if (k == "collect_skip") c->collect_skip = v != 0.0;
         else if (k == "witness") c->witness = v != 0.0;
+        else if (k == "row_cache") c->row_cache = v != 0.0;
+        else if (k == "rc_min_m") c->rc_min_m = (int64_t)v;
         else if (k == "witness_pre") c->witness_pre = v != 0.0;
         else if (k == "witness_pass0") c->witness_pass0 = v != 0.0;
         else if (k == "band_few_wit") c->band_few_wit = std::max(0, (int)v);

@@ -70,7 +70,7 @@ void launch_ref_pairs(int mode, const double* t, int m, const int2* pairs, const
 void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const unsigned* ymax,
                       const unsigned* emax, const float* nrm, const int* crange, int N, int m, int need,
                       double* lo, double* hi, int* cand, float* ythr, unsigned long long* nnkey, int2* groups,
-                      int fixed_span, float seed_w, int* exli, cudaStream_t st);
+                      int fixed_span, float seed_w, int* exli, int* surv, cudaStream_t st);
 // degenerate rows (sigma < eps): every (alive row, degenerate row) and
 // (degenerate row, any q) pair by the exact distance — kills and exact-nn keys
 // knife-edge recheck + degenerate pairs in one launch
@@ -99,6 +99,10 @@ int scan_slots_prune();
 int band0_pair_slots();  // persistent grid of the paired band-0 walk (k_band0_pair)  // persistent grid of the band-pass scan (SMs x resident CTAs)
 // tracked full-row chunks: schedule of the first chunk (after the band passes)
 void launch_track_init(TryCtl* ctl, int N, int m, bool bands_ran, cudaStream_t st);
+// row cache (ScanParams::rcqt): fill one slot at length m / advance every slot m -> m+1
+void launch_rc_fill(const double* t, int n, int m, int a, double* qt, cudaStream_t st);
+void launch_rc_advance(const double* t, int n, int m, const RcRows& rows, long long stride, double* qt,
+                       cudaStream_t st);
 void launch_seed_init(const double* t, int n, int m, int L, int kA, int nb, double* qt, cudaStream_t st);
 void launch_seed_advance(const double* t, int n, int m, int L, int kA, int nb, double* qt, cudaStream_t st);
 void launch_gather_nn(const int* list, const int* cnt, const unsigned long long* nnkey, double* out,

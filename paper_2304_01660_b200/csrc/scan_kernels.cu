@@ -317,6 +317,30 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
     }
     f = (long long)S.flag[par] + gridDim.x;
     if (!work) continue;
+    // Row cache (full rows / collection): a resident raw QT row of an anchor
+    // row at most min(m/2, room) rows before the tile's first row (dir > 0) or
+    // after its last (dir < 0) replaces the tile's m-long direct seeds; the
+    // `ext` rows in between are only walked (2 FFMA per cell: cheaper than
+    // a seed while ext < m/2)
+    int rc = -1, ext = 0;
+    if (MODE != kPrune && p.rc_n > 0) {
+        const int gap = min(p.m / 2, kMaxRows - td.rows);
+        for (int s2 = 0; s2 < p.rc_n; ++s2) {
+            const int ar = p.rc_row[s2];
+            if (ar < 0) continue;  // empty slot
+            const int d = td.dir > 0 ? td.r0 - ar : ar - (td.r0 + td.rows - 1);
+            if (d >= 0 && d <= gap && (rc < 0 || d < ext)) {
+                rc = s2;
+                ext = d;
+            }
+        }
+        if (rc >= 0) {
+            if (td.dir > 0) td.r0 -= ext;
+            td.rows += ext;
+        } else {
+            ext = 0;
+        }
+    }
     const int rows = td.rows;
     const int dir = td.dir;
     const int N = p.N;
@@ -331,7 +355,18 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
     // ---- 1. seeds: cov(c_first, q) for this thread's kDiag diagonals --------
     float cov[kDiag];
     double e_seed = 0.0;  // absolute error bound of FP32 seeds (0 for FP64 / resident seeds)
-    if (td.seed >= 0) {
+    if (rc >= 0) {
+        // row-cache anchor: QT(c_first, q) for every q, carried across lengths
+        // like the band-0 rows (k_rc_advance): cov = QT - m mu_c mu_q
+        const double* qt = p.rcqt + (size_t)rc * (size_t)p.rc_stride;
+        const double mmu = (double)m * p.mu[c_first];
+#pragma unroll
+        for (int j = 0; j < kDiag; ++j) {
+            const int u = tid * kDiag + j;
+            const int q = dir > 0 ? qbase + u : qbase - u;
+            cov[j] = (q >= 0 && q < N) ? (float)(qt[q] - mmu * p.mu[q]) : 0.f;
+        }
+    } else if (td.seed >= 0) {
         // resident seed row, carried across lengths by the dot-product length
         // recurrence (k_seed_advance): cov = QT - m mu_c mu_q
         const double* qt = p.seedqt + (size_t)td.seed * kW + tid * kDiag;
@@ -511,7 +546,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
         p.err_k * (double)kEps32 * (double)(rows + 8) * ((double)m * smax_c * smax_q + 1.5 * P) + e_seed;
     const float Ef = (float)E;
     // statistics error of this length (correlation units; resident raw seeds add theirs)
-    const double xs = stats_band(p, td.seed >= 0);
+    const double xs = stats_band(p, td.seed >= 0 || rc >= 0);
     // Row thresholds.  crow.z = tc: a live row's cells with x = cov*qn > tc may be
     // within the error band of d^2 = r^2 (slow path); kNoEval marks rows whose
     // cells are only walked (already decided, or not a survivor in kCollect).
@@ -520,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
     for (int s = tid; s < rows; s += kThreads) {
         const int c = dir > 0 ? td.r0 + s : r_end - s;
         const float cn = S.crow[s].w;
-        const bool live = p.alive[c] != 0;
+        const bool live = s >= ext && p.alive[c] != 0;  // anchor rows before the tile: walked only
         float tc;
         if (MODE == kCollect) {
             // the row's best lower bound, lowered by the statistics band (x units)
@@ -727,7 +762,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
     if (tid == 0) {
         atomicAdd(&p.acc[0], (unsigned long long)rows * (unsigned long long)kW);
         atomicAdd(&p.acc[1], (unsigned long long)evals * (unsigned long long)(kW / STRIDE));
-        if (td.seed < 0) atomicAdd(&p.acc[2], (unsigned long long)kW);
+        if (td.seed < 0 && rc < 0) atomicAdd(&p.acc[2], (unsigned long long)kW);
     }
     }  // persistent tile loop
     // the last CTA out resets the slot counter for the next launch
@@ -947,8 +982,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_band0_pair(const ScanParams p) 
     }
     float4 cr_next = S.crow[0];
     float2 tc_next = S.ctc[0];
+    // hit masks cover kAgg walk blocks (27 steps) between two aggregations:
+    // in pass 0 nearly every row dies, and the reduction's latency per block
+    // was ~15% of the stall samples at one aggregation per 9 steps
+    constexpr int kAgg = 3;
+    unsigned hit0 = 0u, hit1 = 0u;
+    int hb = 0;  // walk blocks in the current masks
     for (int s0 = 0; s0 < rows_p; s0 += kDiag) {
-        unsigned hit0 = 0u, hit1 = 0u;
+        const int sh = hb * kDiag;
 #pragma unroll
         for (int uu = 0; uu < kDiag; ++uu) {
             const int ss = s0 + uu;
@@ -971,19 +1012,21 @@ __global__ void __launch_bounds__(kThreads, 4) k_band0_pair(const ScanParams p) 
                     mx0 = fmaxf(mx0, x.x);
                     mx1 = fmaxf(mx1, x.y);
                 }
-            hit0 |= (mx0 > tc.x ? 1u : 0u) << uu;
-            hit1 |= (mx1 > tc.y ? 1u : 0u) << uu;
+            hit0 |= (mx0 > tc.x ? 1u : 0u) << (sh + uu);
+            hit1 |= (mx1 > tc.y ? 1u : 0u) << (sh + uu);
             rd[uu % kDiag] = qdp[ss + kDiag];
             rn[uu % kDiag] = qnp[ss + kDiag];
         }
-        // warp-aggregated kills: lanes 0..8 store the positive side's killed
-        // rows of this block, lanes 16..24 the negative side's (one store per
-        // row and warp instead of one per thread and hit)
-        {
+        // warp-aggregated kills every kAgg blocks: lane b stores the row of
+        // step sb + b of each side if any lane killed it (one store per row and
+        // warp instead of one per thread and hit)
+        if (++hb == kAgg || s0 + kDiag >= rows_p) {
             const unsigned h0 = __reduce_or_sync(0xffffffffu, hit0), h1 = __reduce_or_sync(0xffffffffu, hit1);
-            const int lane = tid & 31, b = lane & 15;
-            if (b < kDiag && (((lane < 16 ? h0 : h1) >> b) & 1u))
-                peer_kill(p.peers, p.alive, lane < 16 ? a + s0 + b : e - (s0 + b));
+            const int lane = tid & 31, sb = s0 - (hb - 1) * kDiag;
+            if ((h0 >> lane) & 1u) peer_kill(p.peers, p.alive, a + sb + lane);
+            if ((h1 >> lane) & 1u) peer_kill(p.peers, p.alive, e - (sb + lane));
+            hit0 = hit1 = 0u;
+            hb = 0;
         }
     }
     if (tid == 0) {
@@ -1223,7 +1266,9 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_recheck(const double* __res
 // before any later band is walked.  Witnesses come in runs (one diagonal
 // kills consecutive rows), so k_witness_list cuts the candidates into runs of
 // consecutive rows with the same witness (within 32-row chunks), and
-// k_witness takes one run per warp:
+// k_witness takes one run per warp (a variant staging each run with one
+// round of cp.async copies, up to 200 KB of shared memory per SM, was 8%
+// faster in isolation but made C4 30 ms slower end to end):
 //   seed  QT(c0, q) = sum_p (t[c0+p] - A)(t[q+p] - B) at the run's first row
 //         (A = mu_c0, B = mu of the middle q: small products under a DC
 //         offset), the warp staging chunks of both windows in shared memory;
@@ -2048,7 +2093,7 @@ __global__ void __launch_bounds__(1024) k_survivors(const int* __restrict__ list
                                                     double* __restrict__ hi, int* __restrict__ cand,
                                                     float* __restrict__ ythr, unsigned long long* __restrict__ nnkey,
                                                     int2* __restrict__ groups, int fixed_span, float seed_w,
-                                                    int* __restrict__ exli) {
+                                                    int* __restrict__ exli, int* __restrict__ surv) {
     pdl_enter();
     __shared__ int wsum[32];
     __shared__ int hist[256];
@@ -2068,6 +2113,7 @@ __global__ void __launch_bounds__(1024) k_survivors(const int* __restrict__ list
         const int pos = sc + block_exscan(f, wsum, &tot);
         if (f) {
             cand[pos] = r;
+            if (surv) surv[pos] = r;  // every survivor (the row cache's anchors)
             if (exli) exli[r] = e;  // list index: the collection's per-(row, band) bounds
         }
         sc += tot;
@@ -2214,6 +2260,78 @@ __global__ void k_seed_advance(const double* __restrict__ t, int n, int m, int L
     }
 }
 
+// Row cache: QT(a, q) = sum_{p<m} t[a+p] t[q+p] for every q < N (FP64, m FMA
+// each, 4 consecutive q per thread sliding through registers), and its length
+// recurrence QT_{m+1}(a, q) = QT_m(a, q) + t[a+m] t[q+m] for every valid slot.
+__global__ void __launch_bounds__(kThreads) k_rc_fill(const double* __restrict__ t, int n, int m, int a,
+                                                     double* __restrict__ qt) {
+    pdl_enter();
+    __shared__ double sa[kSeedChunk];
+    __shared__ double sw[kW + kSeedChunk];
+    const int tid = threadIdx.x;
+    const int N = n - m + 1;
+    const int o_t = tid * kDiag;  // this thread's 9 q of the tile (odd stride: conflict-free)
+    for (int q_lo = blockIdx.x * kW; q_lo < N; q_lo += gridDim.x * kW) {
+        double acc[kDiag];
+#pragma unroll
+        for (int i = 0; i < kDiag; ++i) acc[i] = 0.0;
+        for (int pc = 0; pc < m; pc += kSeedChunk) {
+            const int len = min(kSeedChunk, m - pc);
+            __syncthreads();
+            for (int x = tid; x < len; x += kThreads) sa[x] = t[a + pc + x];
+            for (int x = tid; x < kW + len - 1; x += kThreads) {
+                const int g = q_lo + pc + x;
+                sw[x] = g < n ? t[g] : 0.0;
+            }
+            __syncthreads();
+            double w[kDiag];
+#pragma unroll
+            for (int i = 0; i < kDiag - 1; ++i) w[i] = sw[o_t + i];
+            int pp = 0;
+            for (; pp + kDiag <= len; pp += kDiag) {
+#pragma unroll
+                for (int uu = 0; uu < kDiag; ++uu) {
+                    w[(uu + kDiag - 1) % kDiag] = sw[o_t + pp + uu + kDiag - 1];
+                    const double av = sa[pp + uu];
+#pragma unroll
+                    for (int i = 0; i < kDiag; ++i) acc[i] = fma(av, w[(uu + i) % kDiag], acc[i]);
+                }
+            }
+            for (; pp < len; ++pp) {
+                const double av = sa[pp];
+#pragma unroll
+                for (int i = 0; i < kDiag; ++i) acc[i] = fma(av, sw[o_t + pp + i], acc[i]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kDiag; ++i)
+            if (q_lo + o_t + i < N) qt[q_lo + o_t + i] = acc[i];
+    }
+}
+
+__global__ void k_rc_advance(const double* __restrict__ t, int n, int m, RcRows rows, long long stride,
+                             double* __restrict__ qt) {
+    pdl_enter();
+    const int N1 = n - m;  // subsequence count of length m+1
+    for (int sl = blockIdx.y; sl < rows.n; sl += gridDim.y) {
+        const int a = rows.row[sl];
+        if (a < 0 || a >= N1) continue;
+        const double x = t[a + m];
+        double* q = qt + (size_t)sl * (size_t)stride;
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N1; i += gridDim.x * blockDim.x)
+            q[i] = fma(x, t[i + m], q[i]);
+    }
+}
+
+void launch_rc_fill(const double* t, int n, int m, int a, double* qt, cudaStream_t st) {
+    launch_pdl(k_rc_fill, std::max(1, std::min((n + kW - 1) / kW, 148 * 6)), kThreads, st, t, n, m, a, qt);
+}
+
+void launch_rc_advance(const double* t, int n, int m, const RcRows& rows, long long stride, double* qt,
+                       cudaStream_t st) {
+    launch_pdl(k_rc_advance, dim3(148 * 2, rows.n > 0 ? rows.n : 1), 256, st, t, n, m, rows, stride, qt);
+}
+
 void launch_seed_init(const double* t, int n, int m, int L, int kA, int nb, double* qt, cudaStream_t st) {
     k_seed_init<<<148 * 8, 256, 0, st>>>(t, n, m, L, kA, nb, qt);
 }
@@ -2329,9 +2447,9 @@ void launch_recheck(const double* t, int m, int N, const int2* pairs, const int*
 void launch_survivors(const int* list, const uint8_t* alive, TryCtl* ctl, const unsigned* ymax,
                       const unsigned* emax, const float* nrm, const int* crange, int N, int m, int need,
                       double* lo, double* hi, int* cand, float* ythr, unsigned long long* nnkey, int2* groups,
-                      int fixed_span, float seed_w, int* exli, cudaStream_t st) {
+                      int fixed_span, float seed_w, int* exli, int* surv, cudaStream_t st) {
     launch_pdl(k_survivors, 1, 1024, st, list, alive, ctl, ymax, emax, nrm, crange, N, m, need, lo, hi, cand, ythr,
-               nnkey, groups, fixed_span, seed_w, exli);
+               nnkey, groups, fixed_span, seed_w, exli, surv);
 }
 
 void launch_try_init(uint8_t* alive, unsigned* ymax, unsigned* emax, float* ythr, unsigned long long* nnkey, int N,

@@ -129,6 +129,28 @@ def test_merlin_golden_c2_band0_walks(engine, pair):
         engine.set_param("pair_band0", 1)
 
 
+@pytest.mark.parametrize("knobs", [dict(witness=0, row_cache=0), dict(witness=1, row_cache=0),
+                                   dict(witness=0, row_cache=1, rc_min_m=128),
+                                   dict(witness=1, row_cache=1, rc_min_m=128, band_few_wit=16)])
+def test_merlin_golden_c2_schedule_knobs(engine, knobs):
+    # kill witnesses across tries and the row cache only move work between
+    # stages: every setting gives the reference's records bit for bit
+    fx = load_golden("c2.json")
+    engine.set_series(series_of(fx["input"]))
+    for k, v in knobs.items():
+        engine.set_param(k, v)
+    engine.reset_counters()
+    try:
+        rep = engine.merlin_full(fx["min_len"], fx["max_len"], top_k=fx["top_k"], seglen=fx["seglen"])
+        check_merlin(rep, fx)
+        c = engine.counters()
+        if knobs["witness"]:
+            assert c["wit_kills"] > 0
+    finally:
+        for k, v in dict(witness=1, row_cache=1, rc_min_m=384, band_few_wit=0).items():
+            engine.set_param(k, v)
+
+
 @pytest.mark.slow
 def test_merlin_golden_c4(engine):
     # BASELINE config 4: n=1,000,000 random walk, lengths 512..1024 (513 lengths);
