@@ -279,6 +279,9 @@ struct tsd_ctx {
     // 1013 ms with 1/3 in pass 0 and 1/2 in the later band passes.
     int half_pass0 = 3, half_bands = 3;
     long long half_bands_m = 128;
+    int pass0_pk = 1;  // band 0 walks every pair once and kills both ends (k_band0_pk)
+    int pk_rows = 0;   // rows per block of the pair-kill walk (0: 384)
+    int half_pk = 3;   // its evaluation stride ((2j + step) % 3: spread over rows and partners)
     int pair_band0 = 1;  // both sides of band 0 in one packed-FP32x2 walk  // later passes use half_bands only from this length on
     int seed32_track = 1;    // FP32 seeds in the full-row launch (wider error band, half the seed cost; C4 -3.4%)
     int seed32_collect = 1;  // ... and in the collection launch
@@ -498,6 +501,21 @@ struct tsd_ctx {
     // Rows per band-0 block: 512 when the blocks fill the persistent grid, else
     // smaller blocks (256/128) so that small series still occupy every SM
     // (measured at C2: 256 rows 55.5 ms, 128 rows 56.8 ms, 512 rows 57.8 ms).
+    // Rows per block of the pair-kill walk: the slots (block pairs) should fill
+    // the persistent grid to just past a whole number of waves (a last, sparse
+    // wave runs at a higher per-CTA rate) or just below one wave.  Measured:
+    // C4 (N = 1e6) 384 rows 620 ms / 448: 648 / 512: 649; C3 (N = 5e5) 448
+    // rows 421 ms / 384: 464 / 512: 428; C5 (N = 2e6) 512 rows 800 ms / 384:
+    // 807.  The first target wave count with L <= 512 (nearest multiple of 32) wins.
+    int pk_block_rows(int64_t N) const {
+        const double g = (double)band0_pk_slots();
+        for (double w : {0.9, 2.2, 3.3, 4.4, 5.5, 6.6, 7.7}) {
+            const int L = (int)std::lround((double)N / (2.0 * g * w) / 32.0) * 32;
+            if (L <= kMaxRows && L >= 128) return L;
+            if (L < 128) break;
+        }
+        return kMaxRows;
+    }
     int block_rows(int64_t N, bool paired = false) const {
         if (dense_rows > 0) return dense_rows;
         // ~one wave of the band-pass scan grid: two tiles per block (one per
@@ -515,8 +533,14 @@ struct tsd_ctx {
         // the paired walk only when its largest blocks still fill a wave
         // (measured: C4 / C5 gain 1-2%; at C2 the smaller blocks it would need
         // cost more in staging than the walk saves)
-        seed_pair = pair_band0 != 0 && band0_sides == 2 && block_rows(N, true) == kMaxRows;
-        seed_L = block_rows(N, seed_pair);
+        if (pass0_pk && pair_band0 != 0 && band0_sides == 2 && N >= (1 << 18)) {
+            // pair-kill walk: a slot is two blocks' positive sides
+            seed_pair = true;
+            seed_L = pk_rows > 0 ? pk_rows : pk_block_rows(N);
+        } else {
+            seed_pair = pair_band0 != 0 && band0_sides == 2 && block_rows(N, true) == kMaxRows;
+            seed_L = block_rows(N, seed_pair);
+        }
         seed_kA = (int)kA;
         seed_nb = 2 * (int)((N + seed_L - 1) / seed_L);
         seedqt.ensure((size_t)seed_nb * kW);
@@ -776,7 +800,7 @@ struct tsd_ctx {
                     q.L = seed_L;
                     q.kA = seed_kA;
                     q.nb = band0_sides;
-                    q.pair = seed_pair;
+                    q.pair = seed_pair ? (pass0_pk ? 2 : 1) : 0;
                 } else if (pass == 0) {
                     q.space = kSpaceBlocks;
                     q.L = block_rows(N);
@@ -785,7 +809,7 @@ struct tsd_ctx {
                 } else {
                     q.space = kSpaceBand;  // groups and bands set by the previous compaction
                 }
-                q.half = pass == 0 ? half_pass0 : (m >= half_bands_m ? half_bands : 1);
+                q.half = pass == 0 ? (q.pair == 2 ? half_pk : half_pass0) : (m >= half_bands_m ? half_bands : 1);
                 q.wit = (pass == 0 && !witness_pass0) ? nullptr : W;
                 scan(kPrune, q);
                 if (pass == 0 && W) {
@@ -1980,6 +2004,9 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "half_bands") c->half_bands = std::max(1, std::min(3, (int)v));
         else if (k == "half_bands_m") c->half_bands_m = (long long)v;
         else if (k == "pair_band0") c->pair_band0 = v != 0.0;
+        else if (k == "pass0_pk") c->pass0_pk = v != 0.0;
+        else if (k == "half_pk") c->half_pk = std::max(1, std::min(3, (int)v));
+        else if (k == "pk_rows") c->pk_rows = v <= 0 ? 0 : std::max(16, std::min(kMaxRows, (int)v));
         else if (k == "seed_w") c->seed_w = (float)std::max(0.01, v);
         else if (k == "band_keep") c->band_keep = (float)std::max(0.0, std::min(1.0, v));
         else if (k == "band_fill") c->band_fill = std::max(0.0, v);

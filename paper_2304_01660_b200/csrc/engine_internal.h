@@ -96,6 +96,7 @@ void launch_compact_group(const uint8_t* a, int n, int* out, unsigned long long*
                           int band_few, float seed_w, double* bcost, int band_slots, cudaStream_t st);
 int group_slots(int n);
 int scan_slots_prune();
+int band0_pk_slots();    // persistent grid of the pair-kill band-0 walk (k_band0_pk)
 int band0_pair_slots();  // persistent grid of the paired band-0 walk (k_band0_pair)  // persistent grid of the band-pass scan (SMs x resident CTAs)
 // tracked full-row chunks: schedule of the first chunk (after the band passes)
 void launch_track_init(TryCtl* ctl, int N, int m, bool bands_ran, cudaStream_t st);

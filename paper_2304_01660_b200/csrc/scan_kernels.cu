@@ -1042,6 +1042,272 @@ __global__ void __launch_bounds__(kThreads, 4) k_band0_pair(const ScanParams p) 
 }
 
 // ---------------------------------------------------------------------------
+// Band 0, every unordered pair once (pair-kill walk).
+//
+// A pair {c, q} with |q - c| in band 0 is a positive-side cell of c and a
+// negative-side cell of q, so walking both sides of every row computes every
+// pair twice.  Here each CTA walks the positive sides of two row blocks A and
+// B together (lane .x of every register pair: block A, .y: block B; FFMA2 /
+// FMUL2 on pairs as in k_band0_pair), and a certain hit at (c, q) kills both
+// ends: d(c, q) < r means neither is a range discord.  The row kills are
+// aggregated per warp as before; the partner kills are byte flags per q step
+// in shared memory (plain racy stores of 1), written to `alive` after the walk.
+// Every row is evaluated whether or not it is still alive: a dead row's cells
+// still kill its partners.  The per-cell arithmetic, the error bound and the
+// certainty rule are k_band0_pair's (the bound is symmetric in c and q: the
+// tile's E covers the cell whichever end it is read from).  Half the walk of
+// the two-sided band; the resident seed rows of the positive sides only.
+struct __align__(16) PkSmem {
+    float4 crow[kRowsPad];  // per row step: {cdf_A, cdf_B, cdg_A, cdg_B}
+    float2 ctc[kRowsPad];   // per row step: thresholds {tc_A, tc_B} (first: norms)
+    float4 qd[kQPad];       // per q step: {qdf_A, qdf_B, qdg_A, qdg_B}
+    float2 qn[kQPad];       // per q step: norms (NaN: invalid q)
+    unsigned char qhit[2][kQPad];  // per q step: killed as a partner (A, B)
+    float red[7][kThreads / 32];
+    int flag[2];
+};
+
+template <int STRIDE>
+__global__ void __launch_bounds__(kThreads, 4) k_band0_pk(const ScanParams p) {
+    pdl_enter();
+    extern __shared__ __align__(16) unsigned char pk_smem[];
+    PkSmem& S = *reinterpret_cast<PkSmem*>(pk_smem);
+    const int tid = threadIdx.x;
+    const int N = p.N, m = p.m, L = p.L, kA = p.kA;
+    const int nblk = (N + L - 1) / L;
+    const long long slots = (nblk + 1) / 2;
+    const long long mine = p.world > 1 ? (slots > p.rank ? (slots - p.rank + p.world - 1) / p.world : 0) : slots;
+    int par = 0;
+    for (long long f = blockIdx.x;; par ^= 1) {
+    if (f >= mine) break;
+    if (tid == 0) S.flag[par] = atomicAdd(&p.ctl->next, 1);
+    const int jp = (int)(f * p.world + p.rank);
+    const int bA = 2 * jp, bB = 2 * jp + 1;
+    const bool hasB = bB < nblk;
+    const int aA = bA * L, aB = bB * L;
+    const int rowsA = min(N, aA + L) - aA, rowsB = hasB ? min(N, aB + L) - aB : 0;
+    const bool vA = (long long)aA + kA < N, vB = hasB && (long long)aB + kA < N;
+    int any = 0;
+    if (vA)
+        for (int s = tid; s < rowsA; s += kThreads) any |= p.alive[aA + s];
+    if (vB)
+        for (int s = tid; s < rowsB; s += kThreads) any |= p.alive[aB + s];
+    const bool work = __syncthreads_or(any);
+    f = (long long)S.flag[par] + gridDim.x;
+    if (!work) continue;
+    const int rows = rowsA;  // >= rowsB (B follows A)
+    const int qbA = aA + kA, qbB = aB + kA;  // q of step 0, u = 0
+    const int nqA = rowsA - 1 + kW, nqB = rowsB - 1 + kW;
+
+    // ---- seeds: resident positive-side rows of both blocks
+    float2 cov[kDiag];
+    {
+        const double* qtA = p.seedqt + (size_t)(2 * bA) * kW + tid * kDiag;
+        const double* qtB = p.seedqt + (size_t)(2 * bB) * kW + tid * kDiag;
+        const double mA = (double)m * p.mu[aA];
+        const double mB = vB ? (double)m * p.mu[aB] : 0.0;
+#pragma unroll
+        for (int j = 0; j < kDiag; ++j) {
+            const int qA = qbA + tid * kDiag + j, qB = qbB + tid * kDiag + j;
+            const float x = (vA && qA < N) ? (float)(qtA[j] - mA * p.mu[qA]) : 0.f;
+            const float y = (vB && qB < N) ? (float)(qtB[j] - mB * p.mu[qB]) : 0.f;
+            cov[j] = make_float2(x, y);
+        }
+    }
+
+    // ---- stage the walk operands of both blocks
+    float cn_min = FLT_MAX, qn_min = FLT_MAX, qn_max = 0.f;
+    float dc = 0.f, gc = 0.f, dq = 0.f, gq = 0.f;
+#pragma unroll 4
+    for (int s = tid; s < rows; s += kThreads) {
+        const bool inB = s < rowsB;
+        const int cA = aA + s, cB = inB ? aB + s : aA;
+        float4 v;
+        v.x = (s == 0 || !vA) ? 0.f : p.df[cA];
+        v.z = (s == 0 || !vA) ? 0.f : p.dg[cA];
+        v.y = (s == 0 || !vB || !inB) ? 0.f : p.df[cB];
+        v.w = (s == 0 || !vB || !inB) ? 0.f : p.dg[cB];
+        const float nA = p.nrm[cA], nB = inB ? p.nrm[cB] : 0.f;
+        if (nA != 0.f) cn_min = fminf(cn_min, nA);
+        if (nB != 0.f) cn_min = fminf(cn_min, nB);
+        dc = fmaxf(dc, fmaxf(fabsf(v.x), fabsf(v.y)));
+        gc = fmaxf(gc, fmaxf(fabsf(v.z), fabsf(v.w)));
+        S.crow[s] = v;
+        S.ctc[s] = make_float2(nA, nB);
+    }
+    const int rows_p = (rows + kDiag - 1) / kDiag * kDiag;
+    for (int s = rows + tid; s <= rows_p; s += kThreads) {
+        S.crow[s] = make_float4(0.f, 0.f, 0.f, 0.f);
+        S.ctc[s] = make_float2(FLT_MAX, FLT_MAX);
+    }
+    const float qnan = __int_as_float(0x7fffffff);
+#pragma unroll 4
+    for (int u = tid; u < rows_p + kW + kDiag; u += kThreads) {
+        const int qA = qbA + u, qB = qbB + u;
+        const bool okA = vA && u < nqA && qA < N;
+        const bool okB = vB && u < nqB && qB < N;
+        const int qcA = okA ? qA : 0, qcB = okB ? qB : 0;
+        float a0 = p.df[qcA], b0 = p.dg[qcA], a1 = p.df[qcB], b1 = p.dg[qcB];
+        const float nA = p.nrm[qcA], nB = p.nrm[qcB];
+        if (!okA) a0 = b0 = 0.f;
+        if (!okB) a1 = b1 = 0.f;
+        if (okA && nA != 0.f) {
+            qn_min = fminf(qn_min, nA);
+            qn_max = fmaxf(qn_max, nA);
+        }
+        if (okB && nB != 0.f) {
+            qn_min = fminf(qn_min, nB);
+            qn_max = fmaxf(qn_max, nB);
+        }
+        dq = fmaxf(dq, fmaxf(fabsf(a0), fabsf(a1)));
+        gq = fmaxf(gq, fmaxf(fabsf(b0), fabsf(b1)));
+        S.qd[u] = make_float4(a0, a1, b0, b1);
+        S.qn[u] = make_float2((okA && nA != 0.f) ? nA : qnan, (okB && nB != 0.f) ? nB : qnan);
+        S.qhit[0][u] = 0;
+        S.qhit[1][u] = 0;
+    }
+    cn_min = -warp_max(-cn_min);
+    qn_min = -warp_max(-qn_min);
+    qn_max = warp_max(qn_max);
+    dc = warp_max(dc);
+    gc = warp_max(gc);
+    dq = warp_max(dq);
+    gq = warp_max(gq);
+    if ((tid & 31) == 0) {
+        S.red[0][tid >> 5] = cn_min;
+        S.red[1][tid >> 5] = qn_min;
+        S.red[2][tid >> 5] = qn_max;
+        S.red[3][tid >> 5] = dc;
+        S.red[4][tid >> 5] = gc;
+        S.red[5][tid >> 5] = dq;
+        S.red[6][tid >> 5] = gq;
+    }
+    __syncthreads();
+    cn_min = FLT_MAX;
+    qn_min = FLT_MAX;
+    qn_max = 0.f;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+        cn_min = fminf(cn_min, S.red[0][w]);
+        qn_min = fminf(qn_min, S.red[1][w]);
+        qn_max = fmaxf(qn_max, S.red[2][w]);
+        dc = fmaxf(dc, S.red[3][w]);
+        gc = fmaxf(gc, S.red[4][w]);
+        dq = fmaxf(dq, S.red[5][w]);
+        gq = fmaxf(gq, S.red[6][w]);
+    }
+    const double inv_sqm = 1.0 / sqrt((double)m);
+    const double smax_c = cn_min < FLT_MAX ? inv_sqm / (double)cn_min * (1.0 + 1e-6) : 0.0;
+    const double smax_q = qn_min < FLT_MAX ? inv_sqm / (double)qn_min * (1.0 + 1e-6) : 0.0;
+    const double P = (double)dc * (double)gq + (double)dq * (double)gc;
+    const double E = p.err_k * (double)kEps32 * (double)(rows + 8) * ((double)m * smax_c * smax_q + 1.5 * P);
+    const double xs = stats_band(p, true);  // statistics error, resident raw seeds included
+    constexpr float kNoEval = FLT_MAX;
+    int evals = 0;
+    for (int s = tid; s < rows; s += kThreads) {
+        // every row is evaluated, alive or not: its hits also kill the partners
+        const float2 cn = S.ctc[s];
+        float2 tc;
+        if (!vA || cn.x == 0.f) {
+            tc.x = kNoEval;
+        } else {
+            const double eps_row = E * (double)cn.x * (double)qn_max + kSlack + 8.0 * (double)kEps32 + xs;
+            tc.x = (float)((p.thr0 + eps_row) / (double)cn.x);
+            tc.x = tc.x + fabsf(tc.x) * 2.4e-7f;  // round toward +inf (conservative)
+        }
+        if (!vB || s >= rowsB || cn.y == 0.f) {
+            tc.y = kNoEval;
+        } else {
+            const double eps_row = E * (double)cn.y * (double)qn_max + kSlack + 8.0 * (double)kEps32 + xs;
+            tc.y = (float)((p.thr0 + eps_row) / (double)cn.y);
+            tc.y = tc.y + fabsf(tc.y) * 2.4e-7f;
+        }
+        S.ctc[s] = tc;
+        evals += (tc.x != kNoEval) + (tc.y != kNoEval);
+    }
+    evals = __syncthreads_count(evals);
+
+    // ---- walk
+    float4 rd[kDiag];
+    float2 rn[kDiag];
+    const int ub = tid * kDiag;
+    const float4* qdp = S.qd + ub;
+    const float2* qnp = S.qn + ub;
+    unsigned char* const hA = S.qhit[0] + ub;
+    unsigned char* const hB = S.qhit[1] + ub;
+#pragma unroll
+    for (int j = 0; j < kDiag; ++j) {
+        rd[j] = qdp[j];
+        rn[j] = qnp[j];
+    }
+    float4 cr_next = S.crow[0];
+    float2 tc_next = S.ctc[0];
+    constexpr int kAgg = 3;  // walk blocks per row-kill aggregation (27 steps)
+    unsigned hit0 = 0u, hit1 = 0u;
+    int hb = 0;
+    for (int s0 = 0; s0 < rows_p; s0 += kDiag) {
+        const int sh = hb * kDiag;
+#pragma unroll
+        for (int uu = 0; uu < kDiag; ++uu) {
+            const int ss = s0 + uu;
+            const float4 cr = cr_next;
+            const float2 tc = tc_next;
+            cr_next = S.crow[ss + 1];
+            tc_next = S.ctc[ss + 1];
+            const float2 cdf = make_float2(cr.x, cr.y), cdg = make_float2(cr.z, cr.w);
+#pragma unroll
+            for (int j = 0; j < kDiag; ++j) {
+                const int rj = (j + uu) % kDiag;
+                cov[j] = __ffma2_rn(cdf, make_float2(rd[rj].z, rd[rj].w), cov[j]);
+                cov[j] = __ffma2_rn(make_float2(rd[rj].x, rd[rj].y), cdg, cov[j]);
+            }
+            float mx0 = -FLT_MAX, mx1 = -FLT_MAX;
+#pragma unroll
+            for (int j = 0; j < kDiag; ++j)
+                // sampled cells: (2j + step) % 3 == 0 spreads the samples over
+                // every row's cells AND every partner's cells (a partner's
+                // cells have j + step constant, so (j + step) % 3 would test
+                // a third of the partners fully and the rest never)
+                if ((2 * j + uu) % STRIDE == 0) {
+                    const float2 x = __fmul2_rn(cov[j], rn[(j + uu) % kDiag]);
+                    mx0 = fmaxf(mx0, x.x);
+                    mx1 = fmaxf(mx1, x.y);
+                    // the partner q of this cell (u = ss + ub + j) dies with the row
+                    if (x.x > tc.x) hA[ss + j] = 1;
+                    if (x.y > tc.y) hB[ss + j] = 1;
+                }
+            hit0 |= (mx0 > tc.x ? 1u : 0u) << (sh + uu);
+            hit1 |= (mx1 > tc.y ? 1u : 0u) << (sh + uu);
+            rd[uu % kDiag] = qdp[ss + kDiag];
+            rn[uu % kDiag] = qnp[ss + kDiag];
+        }
+        if (++hb == kAgg || s0 + kDiag >= rows_p) {
+            const unsigned h0 = __reduce_or_sync(0xffffffffu, hit0), h1 = __reduce_or_sync(0xffffffffu, hit1);
+            const int lane = tid & 31, sb = s0 - (hb - 1) * kDiag;
+            if ((h0 >> lane) & 1u) peer_kill(p.peers, p.alive, aA + sb + lane);
+            if ((h1 >> lane) & 1u) peer_kill(p.peers, p.alive, aB + sb + lane);
+            hit0 = hit1 = 0u;
+            hb = 0;
+        }
+    }
+    __syncthreads();
+    // partner kills (a hit needs a valid q: invalid q carry NaN norms)
+    for (int u = tid; u < nqA; u += kThreads)
+        if (S.qhit[0][u]) peer_kill(p.peers, p.alive, qbA + u);
+    for (int u = tid; u < nqB; u += kThreads)
+        if (S.qhit[1][u]) peer_kill(p.peers, p.alive, qbB + u);
+    if (tid == 0) {
+        atomicAdd(&p.acc[0], (unsigned long long)kW * (unsigned long long)((vA ? rowsA : 0) + (vB ? rowsB : 0)));
+        atomicAdd(&p.acc[1], (unsigned long long)evals * (unsigned long long)(kW / STRIDE));
+    }
+    }  // persistent tile loop
+    if (tid == 0 && atom_add_acq_rel(&p.ctl->ctas_done, 1) == (int)gridDim.x - 1) {
+        p.ctl->next = 0;
+        p.ctl->ctas_done = 0;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // reference_sq_dist, bit-exact, one warp per pair.  buf: 256 doubles per warp.
 __device__ double ref_dist_warp(const double* __restrict__ t, int m, int i, int j, double* buf) {
     const int lane = threadIdx.x & 31;
@@ -2393,6 +2659,35 @@ int band0_pair_slots() {
     return g_pair_grid;
 }
 
+static int g_pk_grid = 0;
+
+int band0_pk_slots() {
+    if (g_pk_grid == 0) {
+        int dev = 0, sms = 148, per = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int bytes = (int)sizeof(PkSmem);
+        cudaFuncSetAttribute(k_band0_pk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        cudaFuncSetAttribute(k_band0_pk<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        cudaFuncSetAttribute(k_band0_pk<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        cudaFuncSetAttribute(k_band0_pk<1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_band0_pk<2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_band0_pk<3>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_band0_pk<3>, kThreads, bytes);
+        if (const char* e = std::getenv("TSD_SCAN_CTAS")) per = std::min(per, std::max(1, std::atoi(e)));
+        g_pk_grid = sms * (per > 0 ? per : 1);
+    }
+    return g_pk_grid;
+}
+
+static void launch_band0_pk(const ScanParams& p, cudaStream_t st) {
+    const int grid = band0_pk_slots();
+    const size_t bytes = sizeof(PkSmem);
+    if (p.half == 2) launch_pdl_smem(k_band0_pk<2>, grid, kThreads, bytes, st, p);
+    else if (p.half >= 3) launch_pdl_smem(k_band0_pk<3>, grid, kThreads, bytes, st, p);
+    else launch_pdl_smem(k_band0_pk<1>, grid, kThreads, bytes, st, p);
+}
+
 static void launch_band0_pair(const ScanParams& p, cudaStream_t st) {
     const int grid = band0_pair_slots();
     const size_t bytes = sizeof(PairSmem);
@@ -2404,6 +2699,10 @@ static void launch_band0_pair(const ScanParams& p, cudaStream_t st) {
 void launch_scan(int mode, const ScanParams& p, cudaStream_t st) {
     switch (mode) {
         case kPrune:
+            if (p.space == kSpaceSeed && p.pair == 2) {  // every pair of band 0 once, both ends killed
+                launch_band0_pk(p, st);
+                break;
+            }
             if (p.space == kSpaceSeed && p.pair) {  // both sides of band 0 in one walk
                 launch_band0_pair(p, st);
                 break;

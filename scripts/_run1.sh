@@ -1,4 +1,5 @@
 cd $GRAFT_REPO_ROOT
-python scripts/tune.py c3 rc_min_m=100000,256,384,512 2>&1 | tail -4
-python scripts/tune.py c5 rc_min_m=100000,256,384,512 2>&1 | tail -4
-python scripts/tune.py c4 rc_min_m=100000,384 2>&1 | tail -2
+python scripts/cmp_golden.py c4.json
+python scripts/cmp_golden.py c3.json
+for c in c4 c3 c5 c2; do python scripts/tune.py $c pass0_pk=0,1 2>&1 | tail -2; done
+timeout 1500 python -m pytest tests -q -m gpu -x 2>&1 | tail -3
