@@ -2500,34 +2500,39 @@ __device__ __forceinline__ bool seed_pair(int b, int u, int L, int kA, int N, in
     return i < N && q >= 0 && q < N;
 }
 
-__global__ void k_seed_init(const double* __restrict__ t, int n, int m, int L, int kA, int nb,
+__global__ void k_seed_init(const double* __restrict__ t, int n, int m, int L, int kA, int nb, int bstep,
                             double* __restrict__ qt) {
     const int N = n - m + 1;
     const long long total = (long long)nb * kW;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
+        const int b = (int)(e / kW);
+        if (b % bstep) continue;  // rows the pair-kill walk never reads
         int i, q;
         double s = 0.0;
-        if (seed_pair((int)(e / kW), (int)(e % kW), L, kA, N, i, q))
+        if (seed_pair(b, (int)(e % kW), L, kA, N, i, q))
             for (int k = 0; k < m; ++k) s = fma(t[i + k], t[q + k], s);
         qt[e] = s;
     }
 }
 
-__global__ void k_seed_advance(const double* __restrict__ t, int n, int m, int L, int kA, int nb,
+__global__ void k_seed_advance(const double* __restrict__ t, int n, int m, int L, int kA, int nb, int bstep,
                                double* __restrict__ qt) {
     pdl_enter();
     const int N1 = n - m;  // subsequence count of length m+1
     const long long total = (long long)nb * kW;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
+        const int b = (int)(e / kW);
+        if (b % bstep) continue;
         int i, q;
-        if (seed_pair((int)(e / kW), (int)(e % kW), L, kA, N1, i, q)) qt[e] = fma(t[i + m], t[q + m], qt[e]);
+        if (seed_pair(b, (int)(e % kW), L, kA, N1, i, q)) qt[e] = fma(t[i + m], t[q + m], qt[e]);
     }
 }
 
 // Row cache: QT(a, q) = sum_{p<m} t[a+p] t[q+p] for every q < N (FP64, m FMA
-// each, 4 consecutive q per thread sliding through registers), and its length
+// each; 9 consecutive q per thread slide through registers over windows
+// staged in shared memory, as in seed_fp64), and its length
 // recurrence QT_{m+1}(a, q) = QT_m(a, q) + t[a+m] t[q+m] for every valid slot.
 __global__ void __launch_bounds__(kThreads) k_rc_fill(const double* __restrict__ t, int n, int m, int a,
                                                      double* __restrict__ qt) {
@@ -2598,12 +2603,13 @@ void launch_rc_advance(const double* t, int n, int m, const RcRows& rows, long l
     launch_pdl(k_rc_advance, dim3(148 * 2, rows.n > 0 ? rows.n : 1), 256, st, t, n, m, rows, stride, qt);
 }
 
-void launch_seed_init(const double* t, int n, int m, int L, int kA, int nb, double* qt, cudaStream_t st) {
-    k_seed_init<<<148 * 8, 256, 0, st>>>(t, n, m, L, kA, nb, qt);
+void launch_seed_init(const double* t, int n, int m, int L, int kA, int nb, int bstep, double* qt, cudaStream_t st) {
+    k_seed_init<<<148 * 8, 256, 0, st>>>(t, n, m, L, kA, nb, bstep, qt);
 }
 
-void launch_seed_advance(const double* t, int n, int m, int L, int kA, int nb, double* qt, cudaStream_t st) {
-    launch_pdl(k_seed_advance, 148 * 8, 256, st, t, n, m, L, kA, nb, qt);
+void launch_seed_advance(const double* t, int n, int m, int L, int kA, int nb, int bstep, double* qt,
+                         cudaStream_t st) {
+    launch_pdl(k_seed_advance, 148 * 8, 256, st, t, n, m, L, kA, nb, bstep, qt);
 }
 
 static int grid_for(long long work, int threads) {

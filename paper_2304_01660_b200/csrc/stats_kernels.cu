@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(256, 6) k_next_length(const double* __restrict
                               const double* __restrict__ sig_in, double* __restrict__ mu_out,
                               double* __restrict__ sig_out, float* __restrict__ df, float* __restrict__ dg,
                               float* __restrict__ nrm, int* __restrict__ cr, int* __restrict__ cr_next, int L, int kA,
-                              int nb, double* __restrict__ qt, int* __restrict__ deg,
+                              int nb, int bstep, double* __restrict__ qt, int* __restrict__ deg,
                               const double2* __restrict__ P1, const double2* __restrict__ P2,
                               int* __restrict__ degc, int* __restrict__ deg2) {
     pdl_enter();
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(256, 6) k_next_length(const double* __restrict
     if (qt != nullptr) {
         // one seed row per block iteration: no 64-bit index division, the row
         // value t[i+m] is a broadcast, qt and t[q+m] are coalesced
-        for (int b = blockIdx.x; b < nb; b += gridDim.x) {
+        for (int b = blockIdx.x * bstep; b < nb; b += gridDim.x * bstep) {  // bstep 2: positive sides only
             const int j = b >> 1;
             const int i = (b & 1) ? j * L + L - 1 : j * L;
             if (i >= cnt) continue;
@@ -448,10 +448,10 @@ void launch_dd_prefix(const double* t, int n, double2* tot1, double2* tot2, doub
 
 void launch_next_length(const double* t, int n, int m, const double* mu_in, const double* sig_in, double* mu_out,
                         double* sig_out, float* df, float* dg, float* nrm, int* cr, int* cr_next, int L, int kA,
-                        int nb, double* qt, int* deg, const double2* P1, const double2* P2, int* degc, int* deg2,
+                        int nb, int bstep, double* qt, int* deg, const double2* P1, const double2* P2, int* degc, int* deg2,
                         cudaStream_t st) {
     launch_pdl(k_next_length, grid_for(n - m, 256), 256, st, t, n, m, mu_in, sig_in, mu_out, sig_out, df, dg, nrm, cr,
-               cr_next, L, kA, nb, qt, deg, P1, P2, degc, deg2);
+               cr_next, L, kA, nb, bstep, qt, deg, P1, P2, degc, deg2);
 }
 
 }  // namespace tsd
