@@ -122,8 +122,7 @@ struct TryCtl {
     int prev;       // the count before it (band-pass break rule)
     int stop;       // band passes with index > stop are skipped (INT_MAX: none yet)
     int G;          // groups of the current stage (ScanParams::groups)
-    int next;       // persistent-scan slot counter (self-resetting)
-    int ctas_done;  // persistent-scan exit ticket (self-resetting)
+    int slotc[32];  // persistent-scan slot counters, one per scan launch of the try (k_try_init zeroes them)
     int queue;      // knife-edge pairs queued
     int coll;       // near pairs collected
     int crange[2];  // first / last constant row
@@ -215,8 +214,10 @@ struct ScanParams {
     int2* coll;          // kCollect output pairs
     int* coll_count;
     int coll_cap;
-    // tile space of this launch (persistent CTAs fetch slots from ctl->next)
+    // tile space of this launch (persistent CTAs fetch slots from *next, a
+    // counter of its own: no exit ticket, no reset)
     TryCtl* ctl;
+    int* next;
     const int2* groups;  // kSpaceBand / kSpaceFull: (first, last) row of each group
     int space;           // TileSpace
     int pass;            // band pass index (kSpaceBand: skipped when ctl->stop < pass)
@@ -245,6 +246,7 @@ struct ScanParams {
     // tested by k_witness at the start of the next try.  Hints only: a witness
     // kill is certified like any other, so stale entries cost a test, nothing else.
     int* wit;
+    unsigned long long* dbg;  // TSD_DEBUG: [mode*2] slots fetched, [mode*2+1] slots with work (nullptr: off)
     // Row cache (full rows / collection): resident raw QT rows of up to
     // kRcSlots anchor rows near the previous tries' survivors, valid for this
     // length (rc_n = 0: none); slot s holds QT(rc_row[s], q) at rcqt[s * rc_stride + q]

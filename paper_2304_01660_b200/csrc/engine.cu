@@ -240,6 +240,7 @@ struct tsd_ctx {
         }
     }
     DBuf<int> wit;
+    DBuf<unsigned long long> dbgc;  // TSD_DEBUG slot counters (ScanParams::dbg)
     DBuf<int2> wl;  // the try's witness candidate runs
     int witness = 1;
     int witness_pre = 0, witness_pass0 = 0;  // experiments
@@ -591,6 +592,10 @@ struct tsd_ctx {
         p.world = world;
         p.acc = acc.p;
         p.peers = peers;
+        if (debug) {
+            dbgc.ensure(8);
+            p.dbg = dbgc.p;
+        }
         return p;
     }
 
@@ -607,7 +612,11 @@ struct tsd_ctx {
     // Off by default: an event between two kernels breaks the programmatic
     // dependent launch chain (C2: 53.7 ms with events, 43.1 ms without)
     bool scan_events = false;
-    void scan(int mode, const ScanParams& p) {
+    int scan_idx = 0;  // scan launches of the current try (slot counter index)
+    void scan(int mode, const ScanParams& p0) {
+        ScanParams p = p0;
+        if (scan_idx >= 32) fail(TSD_ERUNTIME, "too many scan launches in one try");
+        p.next = &ctl.p->slotc[scan_idx++];
         if (!scan_events) {
             launch_scan(mode, p, st);
             ck(cudaGetLastError(), "scan launch");
@@ -673,6 +682,12 @@ struct tsd_ctx {
         ck(cudaMemcpyAsync(h_ctl.p, ctl.p, sizeof(TryCtl), cudaMemcpyDeviceToHost, st), "D2H");
         sync();
         const TryCtl& c = *h_ctl.p;
+        if (dbgc.p) {
+            unsigned long long d[8] = {};
+            ck(cudaMemcpy(d, dbgc.p, sizeof d, cudaMemcpyDeviceToHost), "D2H");
+            fprintf(stderr, "[tsd] slots prune %llu/%llu track %llu/%llu collect %llu/%llu\n", d[1], d[0], d[3], d[2],
+                    d[5], d[4]);
+        }
         fprintf(stderr,
                 "[tsd] m=%lld r2=%.6g %s pass=%d groups=%d span=%d alive=%d stop=%d queue=%d band=[%d,+%d) "
                 "track=[%d,+%d) phase=%d\n",
@@ -710,7 +725,7 @@ struct tsd_ctx {
         groups.ensure(N);
         if (!ctl.p) {
             ctl.ensure(1);
-            ck(cudaMemsetAsync(ctl.p, 0, sizeof(TryCtl), st), "memset");  // next / ctas_done start at 0
+            ck(cudaMemsetAsync(ctl.p, 0, sizeof(TryCtl), st), "memset");  // self-resetting tickets start at 0
         }
         h_ctl.ensure(1);
         h_int.ensure(8);
@@ -754,6 +769,7 @@ struct tsd_ctx {
         derive(m);
         ensure_scan_buffers(N);
         ev_used = 0;
+        scan_idx = 0;
         ctr.pardrag_calls += 1;
         peer_publish();
         TryCtl* C = ctl.p;
@@ -893,6 +909,7 @@ struct tsd_ctx {
         q.seed32 = seed32_collect;
         q.wit = nullptr;
         scan(kCollect, q);
+        trace("collected", m, r_sq, 0);
         launch_ref_pairs(1, t.p, (int)m, coll.p, &C->coll, coll_cap, r_sq, alive.p, nnkey.p, C,
                          world == 1 ? ex : nullptr, nnout.p, peers, st);
         ck(cudaGetLastError(), "exact");

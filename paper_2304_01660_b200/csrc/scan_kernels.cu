@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
     int par = 0;
     for (long long f = blockIdx.x;; par ^= 1) {
     if (f >= mine) break;
-    if (tid == 0) S.flag[par] = atomicAdd(&p.ctl->next, 1);
+    if (tid == 0) S.flag[par] = atomicAdd(p.next, 1);
     TileDesc td;
     const bool valid = tile_decode(p, cx, f * p.world + p.rank, td);
     bool work;
@@ -316,6 +316,10 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
         }
     }
     f = (long long)S.flag[par] + gridDim.x;
+    if (p.dbg && tid == 0) {
+        if (valid) atomicAdd(&p.dbg[2 * MODE], 1ull);
+        if (work) atomicAdd(&p.dbg[2 * MODE + 1], 1ull);
+    }
     if (!work) continue;
     // Row cache (full rows / collection): a resident raw QT row of an anchor
     // row at most min(m/2, room) rows before the tile's first row (dir > 0) or
@@ -765,11 +769,6 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
         if (td.seed < 0 && rc < 0) atomicAdd(&p.acc[2], (unsigned long long)kW);
     }
     }  // persistent tile loop
-    // the last CTA out resets the slot counter for the next launch
-    if (tid == 0 && atom_add_acq_rel(&p.ctl->ctas_done, 1) == (int)gridDim.x - 1) {
-        p.ctl->next = 0;
-        p.ctl->ctas_done = 0;
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -812,7 +811,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_band0_pair(const ScanParams p) 
     int par = 0;
     for (long long f = blockIdx.x;; par ^= 1) {
     if (f >= mine) break;
-    if (tid == 0) S.flag[par] = atomicAdd(&p.ctl->next, 1);
+    if (tid == 0) S.flag[par] = atomicAdd(p.next, 1);
     const int jb = (int)(f * p.world + p.rank);
     const int a = jb * L, e = min(N, a + L) - 1, rows = e - a + 1;
     const bool v0 = (long long)a + kA < N, v1 = (long long)e - kA >= 0;
@@ -1035,10 +1034,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_band0_pair(const ScanParams p) 
         if (direct1) atomicAdd(&p.acc[2], (unsigned long long)kW);
     }
     }  // persistent tile loop
-    if (tid == 0 && atom_add_acq_rel(&p.ctl->ctas_done, 1) == (int)gridDim.x - 1) {
-        p.ctl->next = 0;
-        p.ctl->ctas_done = 0;
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1080,7 +1075,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_band0_pk(const ScanParams p) {
     int par = 0;
     for (long long f = blockIdx.x;; par ^= 1) {
     if (f >= mine) break;
-    if (tid == 0) S.flag[par] = atomicAdd(&p.ctl->next, 1);
+    if (tid == 0) S.flag[par] = atomicAdd(p.next, 1);
     const int jp = (int)(f * p.world + p.rank);
     const int bA = 2 * jp, bB = 2 * jp + 1;
     const bool hasB = bB < nblk;
@@ -1301,10 +1296,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_band0_pk(const ScanParams p) {
         atomicAdd(&p.acc[1], (unsigned long long)evals * (unsigned long long)(kW / STRIDE));
     }
     }  // persistent tile loop
-    if (tid == 0 && atom_add_acq_rel(&p.ctl->ctas_done, 1) == (int)gridDim.x - 1) {
-        p.ctl->next = 0;
-        p.ctl->ctas_done = 0;
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1784,6 +1775,7 @@ __global__ void k_try_init(uint8_t* __restrict__ alive, unsigned* __restrict__ y
         ctl->bnb = 0;
         ctl->lk = 0.0;
         ctl->wn = 0;
+        for (int k = 0; k < 32; ++k) ctl->slotc[k] = 0;
         ctl->tepoch += 1;
         acc[0] = acc[1] = acc[2] = acc[3] = acc[4] = 0ull;
     }
