@@ -241,7 +241,7 @@ struct tsd_ctx {
     }
     DBuf<int> wit;
     DBuf<unsigned long long> dbgc;  // TSD_DEBUG slot counters (ScanParams::dbg)
-    DBuf<int2> wl;  // the try's witness candidate runs
+    DBuf<int4> wl;  // the try's witness candidate runs (first row, length, witness)
     int witness = 1;
     int witness_pre = 0, witness_pass0 = 0;  // experiments
     long long ub_entries = 1ll << 22;  // 32 MB

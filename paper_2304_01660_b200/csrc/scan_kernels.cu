@@ -1548,18 +1548,33 @@ constexpr int kWitChunk = 256;
 
 // candidate runs (first row, length): alive rows with the same witness,
 // consecutive within a 32-row chunk (warp-aggregated append)
-__global__ void k_witness_list(const ScanParams p, int2* __restrict__ wl) {
+__global__ void k_witness_list(const ScanParams p, int4* __restrict__ wl) {
     pdl_enter();
     const int lane = threadIdx.x & 31;
     for (int c0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; c0 < p.N; c0 += gridDim.x * blockDim.x) {
         const int c = c0 + lane;
-        int wv = kNoWit;
-        if (c < p.N && p.alive[c] && p.nrm[c] > 0.f) wv = p.wit[c];  // not constant / degenerate
-        const bool want = wv != kNoWit;
+        const bool ok = c < p.N && p.alive[c] && p.nrm[c] > 0.f;  // alive, not constant / degenerate
+        if (!__any_sync(0xffffffffu, ok)) continue;
+        // a row without a witness borrows the nearest one of its chunk (before,
+        // else after it): one diagonal often kills a run of consecutive rows
+        const int own = c < p.N ? p.wit[c] : kNoWit;
+        int wv = own;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, wv, o);
+            if (wv == kNoWit && lane >= o) wv = u;
+        }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_down_sync(0xffffffffu, wv, o);
+            if (wv == kNoWit && lane + o < 32) wv = u;
+        }
+        const bool want = ok && wv != kNoWit;
         const unsigned wm = __ballot_sync(0xffffffffu, want);
         if (!wm) continue;
         const int pw = __shfl_up_sync(0xffffffffu, wv, 1);
-        const bool start = want && (lane == 0 || pw != wv);
+        const bool pwant = __shfl_up_sync(0xffffffffu, want, 1);
+        const bool start = want && (lane == 0 || !pwant || pw != wv);
         const unsigned sm = __ballot_sync(0xffffffffu, start);
         int at = 0;
         if (lane == 0) at = atomicAdd(&p.ctl->wn, __popc(sm));
@@ -1567,139 +1582,231 @@ __global__ void k_witness_list(const ScanParams p, int2* __restrict__ wl) {
         if (start) {
             const unsigned brk = lane < 31 ? (sm | ~wm) >> (lane + 1) : 0u;  // lanes that end the run
             const int len = brk ? __ffs(brk) : 32 - lane;
-            wl[at + __popc(sm & ((1u << lane) - 1u))] = make_int2(c, len);
+            wl[at + __popc(sm & ((1u << lane) - 1u))] = make_int4(c, len, wv, 0);
         }
     }
 }
 
-__global__ void __launch_bounds__(kWitWarps * 32) k_witness(const ScanParams p, const int2* __restrict__ wl) {
+// The 9 diagonals q = c + kb .. c + kb + 8 of a run of L rows sharing the
+// witness kb: seeds at the first row (both windows staged in shared memory in
+// 256-element chunks; lane l: p = 4l .. 4l+3 of each 128-element half, 36 DFMA
+// per 16 shared loads), then lanes 0..8 walk one diagonal each down the run.
+__device__ __forceinline__ void wit_run9(const ScanParams& p, int c0, int L, int kb, double* sa, double* sw, double xs,
+                                      unsigned long long& tests, unsigned long long& kills) {
+    const int lane = threadIdx.x & 31;
+    const int N = p.N, m = p.m;
+        const int q0 = c0 + kb;
+    const double A = p.mu[c0];
+    const double B = p.mu[min(max(q0 + kDiag / 2, 0), N - 1)];
+    double acc[kDiag];
+#pragma unroll
+    for (int j = 0; j < kDiag; ++j) acc[j] = 0.0;
+    double delta = 0.0, wa = 0.0, wb = 0.0;
+    for (int pc = 0; pc < m; pc += kWitChunk) {
+        const int len = min(kWitChunk, m - pc);
+        // all loads of the chunk in flight before the first shared store
+        constexpr int kWv = (kWitChunk + 16 + 31) / 32;  // window loads per lane (ceil)
+        double av[kWitChunk / 32], wv0[kWv];
+#pragma unroll
+        for (int i = 0; i < kWitChunk / 32; ++i) {
+            const int x = lane + 32 * i;
+            av[i] = x < len ? p.t[c0 + pc + x] - A : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < kWv; ++i) {
+            const int x = lane + 32 * i;
+            const int g = q0 + pc + x;
+            wv0[i] = (x < len + kDiag - 1 && g >= 0 && g < p.n) ? p.t[g] - B : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < kWitChunk / 32; ++i) {
+            sa[lane + 32 * i] = av[i];
+            delta += av[i];
+            wa = fmax(wa, fabs(av[i]));
+        }
+#pragma unroll
+        for (int i = 0; i < kWv; ++i) {
+            if (lane + 32 * i < kWitChunk + 16) sw[lane + 32 * i] = wv0[i];
+            wb = fmax(wb, fabs(wv0[i]));
+        }
+        __syncwarp();
+        // lane l: p = 4l .. 4l+3 of each 128-element half
+#pragma unroll
+        for (int h = 0; h < kWitChunk; h += 128) {
+            double a4[4], w12[12];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const double2 v = reinterpret_cast<const double2*>(sa + h + 4 * lane)[i];
+                a4[2 * i] = v.x;
+                a4[2 * i + 1] = v.y;
+            }
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
+                const double2 v = reinterpret_cast<const double2*>(sw + h + 4 * lane)[i];
+                w12[2 * i] = v.x;
+                w12[2 * i + 1] = v.y;
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < kDiag; ++j) acc[j] = fma(a4[i], w12[i + j], acc[j]);
+        }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int j = 0; j < kDiag; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+        delta += __shfl_xor_sync(0xffffffffu, delta, o);
+        wa = fmax(wa, __shfl_xor_sync(0xffffffffu, wa, o));
+        wb = fmax(wb, __shfl_xor_sync(0xffffffffu, wb, o));
+    }
+    // lane j < 9 walks diagonal q = c + kb + j down the run
+    double qt = 0.0;
+#pragma unroll
+    for (int j = 0; j < kDiag; ++j)
+        if (j == lane) qt = acc[j];
+    const double u_m = (double)m * kEps64;
+    for (int s = 0; s < L; ++s) {
+        const int c = c0 + s;
+        const int q = c + kb + lane;
+        if (s > 0) {
+            const double to = p.t[c - 1] - A, tn = p.t[c + m - 1] - A;
+            double qo = 0.0, qn = 0.0;
+            if (lane < kDiag) {
+                const int g0 = q - 1, g1 = q + m - 1;
+                qo = (g0 >= 0 && g0 < p.n) ? p.t[g0] - B : 0.0;
+                qn = (g1 >= 0 && g1 < p.n) ? p.t[g1] - B : 0.0;
+            }
+            qt = fma(tn, qn, fma(-to, qo, qt));
+            delta = delta - to + tn;
+            wa = fmax(wa, fabs(tn));
+            wb = fmax(wb, fabs(qn));
+        }
+        if (!p.alive[c]) continue;  // killed meanwhile (warp-uniform)
+        bool kill = false;
+        if (lane < kDiag && q >= 0 && q < N && abs(q - c) >= m && p.nrm[q] > 0.f) {
+            const double dmu = p.mu[q] - B;
+            const double cov = qt - dmu * delta;
+            const double den = (double)m * p.sig[c] * p.sig[q];
+            const double err = ((double)(m + 8 + 4 * s) * u_m * wa * (wb + fabs(dmu)) +
+                                4.0 * kEps64 * (fabs(qt) + fabs(cov))) /
+                               den;
+            kill = cov / den - (err + xs) > p.thr0;
+        }
+        const unsigned km = __ballot_sync(0xffffffffu, kill);
+        if (km) {
+            if (lane == __ffs(km) - 1) {
+                peer_kill(p.peers, p.alive, c);
+                peer_kill(p.peers, p.alive, q);
+                p.wit[c] = q - c - kDiag / 2;  // re-centred on the killing diagonal
+                p.wit[q] = c - q - kDiag / 2;  // the partner's witness for the next try
+            }
+            ++kills;
+        } else if (lane == 0) {
+            p.wit[c] = kNoWit;
+        }
+        ++tests;
+    }
+    }
+
+// One run per warp.  Phase 1 tests the middle diagonal of the 9 (a witness
+// is re-centred on its killing diagonal, so this is usually the killer) for
+// every row of the run at once: one m-long seed at the first row, the walk
+// increments of rows 1..L-1 loaded by lane s and summed by a warp prefix scan
+// (QT(c0+s) = QT(c0) + sum_{i<=s} ((t[c+m-1]-A)(t[q+m-1]-B) - (t[c-1]-A)(t[q-1]-B))),
+// so every lane decides its own row.  The rows it does not kill take the
+// 9-diagonal test (phase 2, wit_run9, one row at a time).  Rounding: the
+// seed's m-term sum and the scan of s increments of at most 2 wa wb each are
+// bounded by (m + 8 + 16 s) u m wa (wb + |mu_q - B|) + 4u (|QT| + |cov|).
+__global__ void __launch_bounds__(kWitWarps * 32) k_witness(const ScanParams p, const int4* __restrict__ wl) {
     pdl_enter();
     __shared__ __align__(16) double s_a[kWitWarps][kWitChunk];
     __shared__ __align__(16) double s_w[kWitWarps][kWitChunk + 16];
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-    double* const sa = s_a[wp];
-    double* const sw = s_w[wp];
-    const int N = p.N, m = p.m;
+    const int N = p.N, m = p.m, n = p.n;
     const double xs = stats_band(p, false) + kSlack + 1e-12;
     const int total = p.ctl->wn;
     unsigned long long tests = 0, kills = 0;
     for (int e = blockIdx.x * kWitWarps + wp; e < total; e += gridDim.x * kWitWarps) {
-        const int2 run = wl[e];
-        const int c0 = run.x;
-        const int kb = p.wit[c0];
-        if (kb == kNoWit) continue;  // defensive: the run's rows share this witness
-        const int q0 = c0 + kb;
-        const double A = p.mu[c0];
-        const double B = p.mu[min(max(q0 + kDiag / 2, 0), N - 1)];
-        double acc[kDiag];
-#pragma unroll
-        for (int j = 0; j < kDiag; ++j) acc[j] = 0.0;
-        double delta = 0.0, wa = 0.0, wb = 0.0;
-        for (int pc = 0; pc < m; pc += kWitChunk) {
-            const int len = min(kWitChunk, m - pc);
-            // all loads of the chunk in flight before the first shared store
-            constexpr int kWv = (kWitChunk + 16 + 31) / 32;  // window loads per lane (ceil)
-            double av[kWitChunk / 32], wv0[kWv];
-#pragma unroll
-            for (int i = 0; i < kWitChunk / 32; ++i) {
-                const int x = lane + 32 * i;
-                av[i] = x < len ? p.t[c0 + pc + x] - A : 0.0;
+        const int4 run = wl[e];
+        const int c0 = run.x, L = run.y, kb = run.z;  // kb: the run's (own or borrowed) witness
+        const int qc = c0 + kb + kDiag / 2;  // middle diagonal's q of the first row
+        const bool diag_ok = qc >= 0 && qc + L - 1 < N && abs(kb + kDiag / 2) >= m;  // warp-uniform
+        const int c = c0 + lane;
+        const bool mine = lane < L;
+        bool alive = mine && p.alive[c] != 0;
+        bool kill = false;
+        if (diag_ok) {
+            const double A = p.mu[c0], B = p.mu[qc];
+            // ---- seed at the first row
+            double acc = 0.0, delta = 0.0, wa = 0.0, wb = 0.0;
+#pragma unroll 4
+            for (int pp = lane; pp < m; pp += 32) {
+                const double a = p.t[c0 + pp] - A, w = p.t[qc + pp] - B;
+                acc = fma(a, w, acc);
+                delta += a;
+                wa = fmax(wa, fabs(a));
+                wb = fmax(wb, fabs(w));
             }
 #pragma unroll
-            for (int i = 0; i < kWv; ++i) {
-                const int x = lane + 32 * i;
-                const int g = q0 + pc + x;
-                wv0[i] = (x < len + kDiag - 1 && g >= 0 && g < p.n) ? p.t[g] - B : 0.0;
+            for (int o = 16; o > 0; o >>= 1) {
+                acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                delta += __shfl_xor_sync(0xffffffffu, delta, o);
+                wa = fmax(wa, __shfl_xor_sync(0xffffffffu, wa, o));
+                wb = fmax(wb, __shfl_xor_sync(0xffffffffu, wb, o));
             }
-#pragma unroll
-            for (int i = 0; i < kWitChunk / 32; ++i) {
-                sa[lane + 32 * i] = av[i];
-                delta += av[i];
-                wa = fmax(wa, fabs(av[i]));
-            }
-#pragma unroll
-            for (int i = 0; i < kWv; ++i) {
-                if (lane + 32 * i < kWitChunk + 16) sw[lane + 32 * i] = wv0[i];
-                wb = fmax(wb, fabs(wv0[i]));
-            }
-            __syncwarp();
-            // lane l: p = 4l .. 4l+3 of each 128-element half
-#pragma unroll
-            for (int h = 0; h < kWitChunk; h += 128) {
-                double a4[4], w12[12];
-#pragma unroll
-                for (int i = 0; i < 2; ++i) {
-                    const double2 v = reinterpret_cast<const double2*>(sa + h + 4 * lane)[i];
-                    a4[2 * i] = v.x;
-                    a4[2 * i + 1] = v.y;
-                }
-#pragma unroll
-                for (int i = 0; i < 6; ++i) {
-                    const double2 v = reinterpret_cast<const double2*>(sw + h + 4 * lane)[i];
-                    w12[2 * i] = v.x;
-                    w12[2 * i + 1] = v.y;
-                }
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int j = 0; j < kDiag; ++j) acc[j] = fma(a4[i], w12[i + j], acc[j]);
-            }
-            __syncwarp();
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-            for (int j = 0; j < kDiag; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
-            delta += __shfl_xor_sync(0xffffffffu, delta, o);
-            wa = fmax(wa, __shfl_xor_sync(0xffffffffu, wa, o));
-            wb = fmax(wb, __shfl_xor_sync(0xffffffffu, wb, o));
-        }
-        // lane j < 9 walks diagonal q = c + kb + j down the run
-        double qt = 0.0;
-#pragma unroll
-        for (int j = 0; j < kDiag; ++j)
-            if (j == lane) qt = acc[j];
-        const double u_m = (double)m * kEps64;
-        for (int s = 0; s < run.y; ++s) {
-            const int c = c0 + s;
-            const int q = c + kb + lane;
-            if (s > 0) {
+            // ---- walk increments of row s = lane, inclusive prefix scan
+            const int q = qc + lane;
+            double term = 0.0, dterm = 0.0, ta = 0.0, tb = 0.0;
+            if (lane >= 1 && mine) {
                 const double to = p.t[c - 1] - A, tn = p.t[c + m - 1] - A;
-                double qo = 0.0, qn = 0.0;
-                if (lane < kDiag) {
-                    const int g0 = q - 1, g1 = q + m - 1;
-                    qo = (g0 >= 0 && g0 < p.n) ? p.t[g0] - B : 0.0;
-                    qn = (g1 >= 0 && g1 < p.n) ? p.t[g1] - B : 0.0;
-                }
-                qt = fma(tn, qn, fma(-to, qo, qt));
-                delta = delta - to + tn;
-                wa = fmax(wa, fabs(tn));
-                wb = fmax(wb, fabs(qn));
+                const double qo = p.t[q - 1] - B, qn = p.t[q + m - 1] - B;
+                term = fma(tn, qn, -to * qo);
+                dterm = tn - to;
+                ta = fabs(tn);
+                tb = fabs(qn);
             }
-            if (!p.alive[c]) continue;  // killed as an earlier witness's partner (warp-uniform)
-            bool kill = false;
-            if (lane < kDiag && q >= 0 && q < N && abs(q - c) >= m && p.nrm[q] > 0.f) {
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double u1 = __shfl_up_sync(0xffffffffu, term, o), u2 = __shfl_up_sync(0xffffffffu, dterm, o);
+                const double u3 = __shfl_up_sync(0xffffffffu, ta, o), u4 = __shfl_up_sync(0xffffffffu, tb, o);
+                if (lane >= o) {
+                    term += u1;
+                    dterm += u2;
+                    ta = fmax(ta, u3);
+                    tb = fmax(tb, u4);
+                }
+            }
+            if (alive && p.nrm[q] > 0.f) {
+                const double qt = acc + term, dl = delta + dterm;
+                const double WA = fmax(wa, ta), WB = fmax(wb, tb);
                 const double dmu = p.mu[q] - B;
-                const double cov = qt - dmu * delta;
+                const double cov = qt - dmu * dl;
                 const double den = (double)m * p.sig[c] * p.sig[q];
-                const double err = ((double)(m + 8 + 4 * s) * u_m * wa * (wb + fabs(dmu)) +
+                const double err = ((double)(m + 8 + 16 * lane) * kEps64 * (double)m * WA * (WB + fabs(dmu)) +
                                     4.0 * kEps64 * (fabs(qt) + fabs(cov))) /
                                    den;
                 kill = cov / den - (err + xs) > p.thr0;
             }
-            const unsigned km = __ballot_sync(0xffffffffu, kill);
-            if (km) {
-                if (lane == __ffs(km) - 1) {
-                    peer_kill(p.peers, p.alive, c);
-                    peer_kill(p.peers, p.alive, q);
-                    p.wit[c] = q - c - kDiag / 2;  // re-centred on the killing diagonal
-                    p.wit[q] = c - q - kDiag / 2;  // the partner's witness for the next try
-                }
-                ++kills;
-            } else if (lane == 0) {
-                p.wit[c] = kNoWit;
+            if (kill) {
+                peer_kill(p.peers, p.alive, c);
+                peer_kill(p.peers, p.alive, q);
+                p.wit[c] = kb;                 // (a borrowed witness becomes the row's own)
+                p.wit[q] = c - q - kDiag / 2;  // the partner's witness for the next try
             }
-            ++tests;
+            tests += __popc(__ballot_sync(0xffffffffu, alive));
+            kills += __popc(__ballot_sync(0xffffffffu, kill));
+        }
+        // ---- phase 2: the rest of the run, 9 diagonals, one row at a time
+        unsigned rest = __ballot_sync(0xffffffffu, alive && !kill);
+        if (diag_ok) {
+            tests -= __popc(rest);  // counted again by wit_run9
+        }
+        while (rest) {
+            const int s2 = __ffs(rest) - 1;
+            rest &= rest - 1u;
+            wit_run9(p, c0 + s2, 1, kb, s_a[wp], s_w[wp], xs, tests, kills);
         }
     }
     if (lane == 0 && tests) {
@@ -1708,9 +1815,9 @@ __global__ void __launch_bounds__(kWitWarps * 32) k_witness(const ScanParams p, 
     }
 }
 
-void launch_witness(const ScanParams& p, int2* wl, cudaStream_t st) {
+void launch_witness(const ScanParams& p, int4* wl, cudaStream_t st) {
     launch_pdl(k_witness_list, std::max(1, std::min((p.N + 255) / 256, 148 * 8)), 256, st, p, wl);
-    launch_pdl(k_witness, 148 * 2, kWitWarps * 32, st, p, (const int2*)wl);
+    launch_pdl(k_witness, 148 * 2, kWitWarps * 32, st, p, (const int4*)wl);
 }
 
 // Overflow fallback, the analogue of the reference's full exact pass for a
