@@ -380,15 +380,34 @@ struct tsd_ctx {
     std::vector<void*> ipc_opened;                 // peer mappings to close
     int64_t ipc_rows = 0;                          // capacity of the shared arrays
     bool ipc_host_sync = std::getenv("TSD_IPC_SYNC") != nullptr;
+    // Device-side barriers (k_flag_barrier): every rank owns kMaxGroup u64
+    // flag slots in device memory (in-process groups: `bflags`; IPC: the tail
+    // of the shared nnkey array), and a barrier is one single-thread kernel per
+    // rank that publishes an epoch into every rank's slot and spins on its own
+    // slots, so the host never blocks on the other ranks.  dev_barrier: 1 on,
+    // 0 off (host barrier + cross-stream event waits), -1 auto (on).
+    int dev_barrier = -1;
+    bool use_dev_bar = false;
+    DBuf<unsigned long long> bflags;
+    FlagPtrs fptr{};
+    unsigned long long bar_epoch = 0;
     void peer_publish() {
         if (ipc_bar) return;  // fixed at join
         peers.n = 0;
         if (!group || !fused || world <= 1) return;
         PeerGroup& g = *group;
+        if (!bflags.p) {
+            // zeroed before any rank can see the pointer (else a peer's early
+            // epoch store could be wiped by this memset)
+            bflags.ensure(kMaxGroup);
+            ck(cudaMemsetAsync(bflags.p, 0, kMaxGroup * sizeof(unsigned long long), st), "memset");
+            sync();
+        }
         g.p_alive[rank] = alive.p;
         g.p_ymax[rank] = ymax.p;
         g.p_emax[rank] = emax.p;
         g.p_nnkey[rank] = nnkey.p;
+        g.p_flags[rank] = bflags.p;
         g.bar.wait();
         peers.n = g.n;
         for (int r = 0; r < g.n; ++r) {
@@ -396,10 +415,22 @@ struct tsd_ctx {
             peers.ymax[r] = static_cast<unsigned*>(g.p_ymax[r]);
             peers.emax[r] = static_cast<unsigned*>(g.p_emax[r]);
             peers.nnkey[r] = static_cast<unsigned long long*>(g.p_nnkey[r]);
+            fptr.p[r] = g.p_flags[r];
         }
+        // In one process, ranks sharing a device cannot use device barriers: an
+        // implicitly device-synchronising call (cudaFree) on one rank's thread
+        // would wait for another rank's barrier kernel, which waits for this
+        // rank's next enqueue.  Distinct devices (and separate processes) are safe.
+        use_dev_bar = dev_barrier == 1 || (dev_barrier == -1 && g.distinct);
         g.bar.wait();  // the tables stay put until every rank has read them
     }
     void peer_barrier() {  // every rank's preceding kernels (and their remote stores) are done
+        if (use_dev_bar) {
+            launch_flag_barrier(fptr, world, rank, ++bar_epoch, st);
+            ck(cudaGetLastError(), "flag barrier");
+            ctr.kernel_launches += 1;
+            return;
+        }
         if (ipc_bar) {
             ck(cudaEventRecord(ipc_ev, st), "event");
             if (ipc_host_sync) sync();  // this rank's work done on the device before the host barrier
@@ -1218,6 +1249,7 @@ void tsd_ctx_destroy(tsd_ctx* c) {
     c->rcqt.release();
     c->wit.release();
     c->wl.release();
+    c->bflags.release();
     c->h_nn.release();
     c->h_int.release();
     c->h_acc.release();
@@ -1667,7 +1699,9 @@ int tsd_ipc_export(tsd_ctx* c, int64_t rows, uint8_t out[5 * 64]) {
         c->alive.ensure(rows);
         c->ymax.ensure(rows);
         c->emax.ensure(rows);
-        c->nnkey.ensure(rows);
+        c->nnkey.ensure(rows + kMaxGroup);  // + the device barrier's flag slots (same rows on every rank)
+        ck(cudaMemset(c->nnkey.p + rows, 0, kMaxGroup * sizeof(unsigned long long)), "memset");
+        ck(cudaDeviceSynchronize(), "sync");  // zeroed before the handles are shared
         c->ipc_rows = rows;
         if (!c->ipc_ev)
             ck(cudaEventCreateWithFlags(&c->ipc_ev, cudaEventDisableTiming | cudaEventInterprocess), "ipc event");
@@ -1682,6 +1716,8 @@ int tsd_ipc_export(tsd_ctx* c, int64_t rows, uint8_t out[5 * 64]) {
         std::memcpy(out + 256, &eh, sizeof(eh) < 64 ? sizeof(eh) : 64);
     });
 }
+
+static int64_t rows_of(const tsd_ctx* c) { return c->ipc_rows; }
 
 int tsd_ipc_join(tsd_ctx* c, int rank, int world, const uint8_t* handles, const char* shm_name) {
     return guard(c, [&] {
@@ -1719,6 +1755,9 @@ int tsd_ipc_join(tsd_ctx* c, int rank, int world, const uint8_t* handles, const 
             c->peers.nnkey[r] = static_cast<unsigned long long*>(p[3]);
         }
         c->ipc_bar = new ShmBarrier(shm_name ? shm_name : "/tsd_ipc", world, rank == 0);
+        for (int r = 0; r < world; ++r) c->fptr.p[r] = c->peers.nnkey[r] + rows_of(c);
+        c->use_dev_bar = c->dev_barrier != 0;
+        c->bar_epoch = 0;
     });
 }
 
@@ -1737,6 +1776,10 @@ int tsd_group_create(const int* devices, int n, tsd_group** out) {
     }
     tsd_group* g = new tsd_group();
     g->pg = new PeerGroup(n);
+    g->pg->distinct = true;
+    for (int a = 0; a < n; ++a)
+        for (int b = 0; b < a; ++b)
+            if (devices[a] == devices[b]) g->pg->distinct = false;
     for (int r = 0; r < n; ++r) {
         tsd_ctx* c = nullptr;
         const int rc = tsd_ctx_create(devices[r], &c);
@@ -2034,6 +2077,10 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "collect_skip") c->collect_skip = v != 0.0;
         else if (k == "witness") c->witness = v != 0.0;
         else if (k == "row_cache") c->row_cache = v != 0.0;
+        else if (k == "dev_barrier") {
+            c->dev_barrier = v < 0 ? -1 : (v != 0.0 ? 1 : 0);
+            c->use_dev_bar = c->world > 1 && c->peers.n > 1 && c->dev_barrier != 0;
+        }
         else if (k == "rc_min_m") c->rc_min_m = (int64_t)v;
         else if (k == "witness_pre") c->witness_pre = v != 0.0;
         else if (k == "witness_pass0") c->witness_pass0 = v != 0.0;

@@ -95,6 +95,46 @@ __global__ void k_peer_reduce(PeerPtrs in, int nranks, T* __restrict__ out, size
     }
 }
 
+// Device-side barrier of a rank group over peer memory (no host round trip):
+// one thread fences the rank's preceding work (its peer stores included)
+// system-wide, publishes `epoch` in its slot of every rank's flag array, and
+// spins until every rank's slot in its own array has reached `epoch`.  Epochs
+// only grow, so the flags never need resetting.  A rank that never arrives
+// makes the kernel trap after ~10 s (a loud error instead of a hang).
+__global__ void k_flag_barrier(FlagPtrs f, int world, int rank, unsigned long long epoch) {
+    // no early launch of the dependents: their CTAs would occupy the SMs while
+    // this kernel spins, and ranks sharing a device need them to arrive
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x != 0) return;
+    __threadfence_system();
+    for (int r = 0; r < world; ++r)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f.p[r] + rank), "l"(epoch) : "memory");
+    unsigned long long spins = 0;
+    for (int r = 0; r < world; ++r) {
+        for (;;) {
+            unsigned long long v;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f.p[rank] + r) : "memory");
+            if (v >= epoch) break;
+            __nanosleep(64);
+            if (++spins > (1ull << 27)) __trap();
+        }
+    }
+    __threadfence_system();
+}
+
+void launch_flag_barrier(const FlagPtrs& f, int world, int rank, unsigned long long epoch, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(32);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_flag_barrier, f, world, rank, epoch);
+}
+
 void launch_peer_reduce(int kind, PeerPtrs in, int nranks, void* out, size_t cnt, cudaStream_t st) {
     if (cnt == 0) return;
     size_t b = (cnt + 255) / 256;

@@ -27,6 +27,13 @@ struct PeerPtrs {
 // out[i] = reduce_r in_r[i]; kind 0: u8 min, 1: u32 max, 2: u64 min
 void launch_peer_reduce(int kind, PeerPtrs in, int nranks, void* out, size_t cnt, cudaStream_t st);
 
+// every rank's barrier flag array (kMaxGroup u64 slots, one per rank)
+struct FlagPtrs {
+    unsigned long long* p[kMaxGroup];
+};
+// device-side barrier of `world` ranks: all ranks' preceding stream work done
+void launch_flag_barrier(const FlagPtrs& f, int world, int rank, unsigned long long epoch, cudaStream_t st);
+
 class HostBarrier {
 public:
     explicit HostBarrier(int n) : n_(n) {}
@@ -71,13 +78,15 @@ private:
 
 struct PeerGroup {
     int n = 0;
+    bool distinct = false;  // every rank on its own device (device barriers allowed)
     HostBarrier bar;
     std::vector<const void*> ptrs;
     std::vector<void*> p_alive, p_ymax, p_emax, p_nnkey;  // fused transport: every rank's arrays
+    std::vector<unsigned long long*> p_flags;                // device barrier flags of every rank
     std::vector<cudaEvent_t> ev_in, ev_red;
     explicit PeerGroup(int ranks)
-        : n(ranks), bar(ranks), ptrs(ranks), p_alive(ranks), p_ymax(ranks), p_emax(ranks), p_nnkey(ranks), ev_in(ranks),
-          ev_red(ranks) {}
+        : n(ranks), bar(ranks), ptrs(ranks), p_alive(ranks), p_ymax(ranks), p_emax(ranks), p_nnkey(ranks),
+          p_flags(ranks), ev_in(ranks), ev_red(ranks) {}
 };
 
 }  // namespace tsd
