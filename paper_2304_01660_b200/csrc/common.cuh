@@ -145,6 +145,8 @@ struct TryCtl {
     int tpasses;    // tracked chunks that ran
     unsigned tepoch;  // try counter (k_try_init): tags the per-(row, band) bounds of this try
     int wn;         // kill-witness candidates listed after band pass 0 (k_witness_list)
+    int wn2;        // ... rows left for the 9-diagonal phase (k_witness9)
+    int wrun, wrun2;  // witness phases: runs / rows fetched (dynamic)
     double lk;      // top-k filter: need_top-th largest nn lower bound
     double cost[6]; // compaction: grouping cost per span (16..512), self-resetting
 };
@@ -246,6 +248,13 @@ struct ScanParams {
     // tested by k_witness at the start of the next try.  Hints only: a witness
     // kill is certified like any other, so stale entries cost a test, nothing else.
     int* wit;
+    // run-seed cache of the witness test (k_witness): per row, the raw FP64
+    // dot product QT(c, wc_q[c]) at length wc_m[c] (0: none); with pfx1, the
+    // double-double prefix sums of t that convert it to the shifted seed
+    double* wc_qt;
+    int* wc_m;
+    int* wc_q;
+    const double2* pfx1;
     unsigned long long* dbg;  // TSD_DEBUG: [mode*2] slots fetched, [mode*2+1] slots with work (nullptr: off)
     // Row cache (full rows / collection): resident raw QT rows of up to
     // kRcSlots anchor rows near the previous tries' survivors, valid for this

@@ -240,10 +240,14 @@ struct tsd_ctx {
         }
     }
     DBuf<int> wit;
+    // run-seed cache of the witness test (ScanParams::wc_*)
+    int wit_cache = 1;
+    DBuf<double> wc_qt;
+    DBuf<int> wc_m, wc_q;
     DBuf<unsigned long long> dbgc;  // TSD_DEBUG slot counters (ScanParams::dbg)
     DBuf<int4> wl;  // the try's witness candidate runs (first row, length, witness)
+    DBuf<int2> wl2;  // rows left for the 9-diagonal phase (row, witness)
     int witness = 1;
-    int witness_pre = 0, witness_pass0 = 0;  // experiments
     long long ub_entries = 1ll << 22;  // 32 MB
     DBuf<double> nnout;
     DBuf<int2> groups, slots;  // groups of the current stage; per-span candidate groups
@@ -716,8 +720,8 @@ struct tsd_ctx {
         if (dbgc.p) {
             unsigned long long d[8] = {};
             ck(cudaMemcpy(d, dbgc.p, sizeof d, cudaMemcpyDeviceToHost), "D2H");
-            fprintf(stderr, "[tsd] slots prune %llu/%llu track %llu/%llu collect %llu/%llu\n", d[1], d[0], d[3], d[2],
-                    d[5], d[4]);
+            fprintf(stderr, "[tsd] slots prune %llu/%llu track %llu/%llu collect %llu/%llu witness runs %llu cached %llu\n",
+                    d[1], d[0], d[3], d[2], d[5], d[4], d[6], d[7]);
         }
         fprintf(stderr,
                 "[tsd] m=%lld r2=%.6g %s pass=%d groups=%d span=%d alive=%d stop=%d queue=%d band=[%d,+%d) "
@@ -741,6 +745,7 @@ struct tsd_ctx {
         acc.ensure(5);
         surv.ensure(N);
         wl.ensure(N);
+        wl2.ensure(N);
         if (wit.cap < (size_t)n) {
             wit.ensure((size_t)n);
             ck(cudaMemsetAsync(wit.p, 0x80, (size_t)n * sizeof(int), st), "memset");  // kNoWit
@@ -818,13 +823,6 @@ struct tsd_ctx {
         const ScanParams P = params(m, r_sq);
         std::vector<tsd_record> out;
         int* const W = witness && m <= kWitMaxM ? wit.p : nullptr;
-        if (W && witness_pre && r_sq > 0.0) {  // experiment: every row with a witness, before pass 0
-            ScanParams w = P;
-            w.wit = W;
-            launch_witness(w, wl.p, st);
-            ck(cudaGetLastError(), "witness");
-            ctr.kernel_launches += 2;
-        }
 
         // ---- band passes (PD3 selection): diagonals |k| in [K0, K0 + nb*kW) on
         // both sides of every undecided row; only certain FP32 kills.  Pass 0
@@ -859,16 +857,28 @@ struct tsd_ctx {
                     q.space = kSpaceBand;  // groups and bands set by the previous compaction
                 }
                 q.half = pass == 0 ? (q.pair == 2 ? half_pk : half_pass0) : (m >= half_bands_m ? half_bands : 1);
-                q.wit = (pass == 0 && !witness_pass0) ? nullptr : W;
+                q.wit = pass == 0 ? nullptr : W;
                 scan(kPrune, q);
                 if (pass == 0 && W) {
                     // rows killed after pass 0 in earlier tries test their killer
                     // before the later bands are walked (k_witness)
                     ScanParams w = P;
                     w.wit = W;
-                    launch_witness(w, wl.p, st);
+                    if (wit_cache) {
+                        if (wc_m.cap < (size_t)n) {
+                            wc_m.ensure((size_t)n);
+                            ck(cudaMemsetAsync(wc_m.p, 0, (size_t)n * sizeof(int), st), "memset");  // empty
+                        }
+                        wc_qt.ensure((size_t)n);
+                        wc_q.ensure((size_t)n);
+                        w.wc_qt = wc_qt.p;
+                        w.wc_m = wc_m.p;
+                        w.wc_q = wc_q.p;
+                        w.pfx1 = pfx1.p;
+                    }
+                    launch_witness(w, wl.p, wl2.p, st);
                     ck(cudaGetLastError(), "witness");
-                    ctr.kernel_launches += 2;
+                    ctr.kernel_launches += N < (1 << 18) ? 2 : 3;
                 }
                 reduce_alive(N);
                 compact(N, pass, m);
@@ -1249,7 +1259,11 @@ void tsd_ctx_destroy(tsd_ctx* c) {
     c->rcqt.release();
     c->wit.release();
     c->wl.release();
+    c->wl2.release();
     c->bflags.release();
+    c->wc_qt.release();
+    c->wc_m.release();
+    c->wc_q.release();
     c->h_nn.release();
     c->h_int.release();
     c->h_acc.release();
@@ -1310,6 +1324,7 @@ int tsd_series_set(tsd_ctx* c, const double* v, int64_t n) {
         c->seed_m = -1;
         if (c->wit.p) ck(cudaMemset(c->wit.p, 0x80, c->wit.cap * sizeof(int)), "memset");  // witnesses of the old series
         c->rc_reset();
+        if (c->wc_m.p) ck(cudaMemset(c->wc_m.p, 0, c->wc_m.cap * sizeof(int)), "memset");
     });
 }
 
@@ -1519,6 +1534,7 @@ int tsd_merlin(tsd_ctx* c, int64_t min_len, int64_t max_len, const tsd_merlin_op
         c->rc_reset();
         // every discovery starts from scratch: no kill witnesses from an earlier call
         if (c->wit.p) ck(cudaMemsetAsync(c->wit.p, 0x80, c->wit.cap * sizeof(int), c->st), "memset");
+        if (c->wc_m.p) ck(cudaMemsetAsync(c->wc_m.p, 0, c->wc_m.cap * sizeof(int), c->st), "memset");
         for (int64_t m = min_len; m <= max_len; ++m) {
             const int64_t k = m - min_len;
             counts[k] = 0;
@@ -2077,13 +2093,12 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "collect_skip") c->collect_skip = v != 0.0;
         else if (k == "witness") c->witness = v != 0.0;
         else if (k == "row_cache") c->row_cache = v != 0.0;
+        else if (k == "wit_cache") c->wit_cache = v != 0.0;
         else if (k == "dev_barrier") {
             c->dev_barrier = v < 0 ? -1 : (v != 0.0 ? 1 : 0);
             c->use_dev_bar = c->world > 1 && c->peers.n > 1 && c->dev_barrier != 0;
         }
         else if (k == "rc_min_m") c->rc_min_m = (int64_t)v;
-        else if (k == "witness_pre") c->witness_pre = v != 0.0;
-        else if (k == "witness_pass0") c->witness_pass0 = v != 0.0;
         else if (k == "band_few_wit") c->band_few_wit = std::max(0, (int)v);
         else if (k == "queue_cap") c->queue_cap = std::max(1, std::min(kQueueCap, (int)v));
         else if (k == "coll_cap") c->coll_cap = std::max(1, std::min(kCollCap, (int)v));

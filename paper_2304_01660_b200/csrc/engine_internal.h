@@ -84,7 +84,7 @@ void launch_exact_rows(const double* t, int m, int N, const int* list, const Try
                        uint8_t* alive, unsigned long long* nnkey, int rank, int world, const Peers& peers,
                        cudaStream_t st);
 // kill witnesses of earlier tries tested before band pass 0 (ScanParams::wit)
-void launch_witness(const ScanParams& p, int4* wl, cudaStream_t st);  // wl: N entries of scratch
+void launch_witness(const ScanParams& p, int4* wl, int2* wl2, cudaStream_t st);  // wl, wl2: N entries of scratch
 void launch_try_init(uint8_t* alive, unsigned* ymax, unsigned* emax, float* ythr, unsigned long long* nnkey, int N,
                      TryCtl* ctl, unsigned long long* acc, int band_k0, cudaStream_t st);
 int compact_blocks(int n);

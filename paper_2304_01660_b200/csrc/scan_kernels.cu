@@ -1719,16 +1719,27 @@ __device__ __forceinline__ void wit_run9(const ScanParams& p, int c0, int L, int
 // 9-diagonal test (phase 2, wit_run9, one row at a time).  Rounding: the
 // seed's m-term sum and the scan of s increments of at most 2 wa wb each are
 // bounded by (m + 8 + 16 s) u m wa (wb + |mu_q - B|) + 4u (|QT| + |cov|).
-__global__ void __launch_bounds__(kWitWarps * 32) k_witness(const ScanParams p, const int4* __restrict__ wl) {
+template <bool INLINE2>
+__global__ void __launch_bounds__(256) k_witness(const ScanParams p, const int4* __restrict__ wl,
+                                                 int2* __restrict__ wl2) {
     pdl_enter();
-    __shared__ __align__(16) double s_a[kWitWarps][kWitChunk];
-    __shared__ __align__(16) double s_w[kWitWarps][kWitChunk + 16];
-    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    // INLINE2: the 9-diagonal phase in this kernel (small series: one launch
+    // less per try); else deferred to k_witness9 (fewer registers here, more
+    // warps for phase 1's load latency)
+    __shared__ __align__(16) double s_a[INLINE2 ? 8 : 1][INLINE2 ? kWitChunk : 1];
+    __shared__ __align__(16) double s_w[INLINE2 ? 8 : 1][INLINE2 ? kWitChunk + 16 : 1];
+    const int lane = threadIdx.x & 31;
     const int N = p.N, m = p.m, n = p.n;
     const double xs = stats_band(p, false) + kSlack + 1e-12;
+    const double xs_res = stats_band(p, true) + kSlack + 1e-12;  // cached raw seeds: the resident term
     const int total = p.ctl->wn;
     unsigned long long tests = 0, kills = 0;
-    for (int e = blockIdx.x * kWitWarps + wp; e < total; e += gridDim.x * kWitWarps) {
+    for (;;) {
+        // runs are fetched one at a time per warp (their costs vary widely)
+        int e = 0;
+        if (lane == 0) e = atomicAdd(&p.ctl->wrun, 1);
+        e = __shfl_sync(0xffffffffu, e, 0);
+        if (e >= total) break;
         const int4 run = wl[e];
         const int c0 = run.x, L = run.y, kb = run.z;  // kb: the run's (own or borrowed) witness
         const int qc = c0 + kb + kDiag / 2;  // middle diagonal's q of the first row
@@ -1739,55 +1750,103 @@ __global__ void __launch_bounds__(kWitWarps * 32) k_witness(const ScanParams p, 
         bool kill = false;
         if (diag_ok) {
             const double A = p.mu[c0], B = p.mu[qc];
-            // ---- seed at the first row
-            double acc = 0.0, delta = 0.0, wa = 0.0, wb = 0.0;
-#pragma unroll 4
-            for (int pp = lane; pp < m; pp += 32) {
-                const double a = p.t[c0 + pp] - A, w = p.t[qc + pp] - B;
-                acc = fma(a, w, acc);
-                delta += a;
-                wa = fmax(wa, fabs(a));
-                wb = fmax(wb, fabs(w));
+            // ---- seed at the first row: from the run-seed cache (the raw dot
+            // product QT(c0, qc) of an earlier length, advanced by the length
+            // recurrence) or directly (shifted by A, B; the raw product is kept
+            // for the next length)
+            double acc, delta, e_seed, e_delta;
+            bool cached = false;
+            double wa = 0.0, wb = 0.0;
+            if (p.wc_qt != nullptr) {
+                const int cm = p.wc_m[c0];
+                cached = p.wc_q[c0] == qc && cm > 0 && cm <= m && m - cm <= 32;
             }
+            if (p.dbg && lane == 0) {
+                atomicAdd(&p.dbg[6], 1ull);
+                if (cached) atomicAdd(&p.dbg[7], 1ull);
+            }
+            if (cached) {
+                const int cm = p.wc_m[c0];
+                double tsum = lane < m - cm ? p.t[c0 + cm + lane] * p.t[qc + cm + lane] : 0.0;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                delta += __shfl_xor_sync(0xffffffffu, delta, o);
-                wa = fmax(wa, __shfl_xor_sync(0xffffffffu, wa, o));
-                wb = fmax(wb, __shfl_xor_sync(0xffffffffu, wb, o));
+                for (int o = 16; o > 0; o >>= 1) tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
+                const double raw = p.wc_qt[c0] + tsum;  // QT_m(c0, qc) = QT_cm + sum_{l=cm}^{m-1} t t
+                const double2 c1 = p.pfx1[c0 + m], c2 = p.pfx1[c0], q1 = p.pfx1[qc + m], q2 = p.pfx1[qc];
+                const double Sc = (c1.x - c2.x) + (c1.y - c2.y), Sq = (q1.x - q2.x) + (q1.y - q2.y);
+                const double mAB = (double)m * A * B;
+                acc = raw - A * Sq - B * Sc + mAB;
+                delta = Sc - (double)m * A;
+                // conversion rounding (the raw value's own accumulated error is the
+                // resident term of the statistics band, as for the band-0 rows)
+                e_seed = 6.0 * kEps64 * (fabs(raw) + fabs(A * Sq) + fabs(B * Sc) + fabs(mAB));
+                e_delta = 6.0 * kEps64 * (fabs(Sc) + fabs((double)m * A));
+                if (lane == 0) p.wc_m[c0] = m;
+                if (lane == 0) p.wc_qt[c0] = raw;
+            } else {
+                double raw = 0.0;
+                acc = 0.0;
+                delta = 0.0;
+#pragma unroll 4
+                for (int pp = lane; pp < m; pp += 32) {
+                    const double tc = p.t[c0 + pp], tq = p.t[qc + pp];
+                    const double a = tc - A, w = tq - B;
+                    acc = fma(a, w, acc);
+                    raw = fma(tc, tq, raw);
+                    delta += a;
+                    wa = fmax(wa, fabs(a));
+                    wb = fmax(wb, fabs(w));
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                    raw += __shfl_xor_sync(0xffffffffu, raw, o);
+                    delta += __shfl_xor_sync(0xffffffffu, delta, o);
+                    wa = fmax(wa, __shfl_xor_sync(0xffffffffu, wa, o));
+                    wb = fmax(wb, __shfl_xor_sync(0xffffffffu, wb, o));
+                }
+                e_seed = (double)(m + 8) * kEps64 * (double)m * wa * wb;
+                e_delta = (double)(m + 8) * kEps64 * (double)m * wa;
+                if (p.wc_qt != nullptr && lane == 0) {
+                    p.wc_qt[c0] = raw;
+                    p.wc_m[c0] = m;
+                    p.wc_q[c0] = qc;
+                }
             }
-            // ---- walk increments of row s = lane, inclusive prefix scan
+            // ---- walk increments of row s = lane, inclusive prefix scans of the
+            // increments and of their magnitudes (the walk's rounding)
             const int q = qc + lane;
-            double term = 0.0, dterm = 0.0, ta = 0.0, tb = 0.0;
+            double term = 0.0, dterm = 0.0, sabs = 0.0, dabs = 0.0;
             if (lane >= 1 && mine) {
                 const double to = p.t[c - 1] - A, tn = p.t[c + m - 1] - A;
                 const double qo = p.t[q - 1] - B, qn = p.t[q + m - 1] - B;
                 term = fma(tn, qn, -to * qo);
                 dterm = tn - to;
-                ta = fabs(tn);
-                tb = fabs(qn);
+                sabs = fabs(tn * qn) + fabs(to * qo);
+                dabs = fabs(tn) + fabs(to);
             }
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const double u1 = __shfl_up_sync(0xffffffffu, term, o), u2 = __shfl_up_sync(0xffffffffu, dterm, o);
-                const double u3 = __shfl_up_sync(0xffffffffu, ta, o), u4 = __shfl_up_sync(0xffffffffu, tb, o);
+                const double u3 = __shfl_up_sync(0xffffffffu, sabs, o), u4 = __shfl_up_sync(0xffffffffu, dabs, o);
                 if (lane >= o) {
                     term += u1;
                     dterm += u2;
-                    ta = fmax(ta, u3);
-                    tb = fmax(tb, u4);
+                    sabs += u3;
+                    dabs += u4;
                 }
             }
             if (alive && p.nrm[q] > 0.f) {
                 const double qt = acc + term, dl = delta + dterm;
-                const double WA = fmax(wa, ta), WB = fmax(wb, tb);
                 const double dmu = p.mu[q] - B;
                 const double cov = qt - dmu * dl;
                 const double den = (double)m * p.sig[c] * p.sig[q];
-                const double err = ((double)(m + 8 + 16 * lane) * kEps64 * (double)m * WA * (WB + fabs(dmu)) +
-                                    4.0 * kEps64 * (fabs(qt) + fabs(cov))) /
+                // seed + walk (each increment two roundings, a 6-level scan) + the
+                // mean correction + the last operations
+                const double ew = (double)(2 * lane + 12) * kEps64;
+                const double err = (e_seed + ew * sabs + fabs(dmu) * (e_delta + ew * dabs) +
+                                    4.0 * kEps64 * (fabs(qt) + fabs(cov) + fabs(dmu * dl))) /
                                    den;
-                kill = cov / den - (err + xs) > p.thr0;
+                kill = cov / den - (err + (cached ? xs_res : xs)) > p.thr0;
             }
             if (kill) {
                 peer_kill(p.peers, p.alive, c);
@@ -1798,15 +1857,21 @@ __global__ void __launch_bounds__(kWitWarps * 32) k_witness(const ScanParams p, 
             tests += __popc(__ballot_sync(0xffffffffu, alive));
             kills += __popc(__ballot_sync(0xffffffffu, kill));
         }
-        // ---- phase 2: the rest of the run, 9 diagonals, one row at a time
+        // ---- the rest of the run goes to phase 2 (9 diagonals)
         unsigned rest = __ballot_sync(0xffffffffu, alive && !kill);
-        if (diag_ok) {
-            tests -= __popc(rest);  // counted again by wit_run9
-        }
-        while (rest) {
-            const int s2 = __ffs(rest) - 1;
-            rest &= rest - 1u;
-            wit_run9(p, c0 + s2, 1, kb, s_a[wp], s_w[wp], xs, tests, kills);
+        if (diag_ok) tests -= __popc(rest);  // counted by phase 2
+        if (INLINE2) {
+            const int wp = threadIdx.x >> 5;
+            while (rest) {
+                const int s2 = __ffs(rest) - 1;
+                rest &= rest - 1u;
+                wit_run9(p, c0 + s2, 1, kb, s_a[wp], s_w[wp], xs, tests, kills);
+            }
+        } else if (rest) {
+            int at = 0;
+            if (lane == 0) at = atomicAdd(&p.ctl->wn2, __popc(rest));
+            at = __shfl_sync(0xffffffffu, at, 0);
+            if ((rest >> lane) & 1u) wl2[at + __popc(rest & ((1u << lane) - 1u))] = make_int2(c, kb);
         }
     }
     if (lane == 0 && tests) {
@@ -1815,9 +1880,38 @@ __global__ void __launch_bounds__(kWitWarps * 32) k_witness(const ScanParams p, 
     }
 }
 
-void launch_witness(const ScanParams& p, int4* wl, cudaStream_t st) {
+// Phase 2: the rows phase 1 left, all 9 diagonals of the witness, one warp
+// per row (fetched dynamically), windows staged in shared memory.
+__global__ void __launch_bounds__(kWitWarps * 32) k_witness9(const ScanParams p, const int2* __restrict__ wl2) {
+    pdl_enter();
+    __shared__ __align__(16) double s_a[kWitWarps][kWitChunk];
+    __shared__ __align__(16) double s_w[kWitWarps][kWitChunk + 16];
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const double xs = stats_band(p, false) + kSlack + 1e-12;
+    const int total = p.ctl->wn2;
+    unsigned long long tests = 0, kills = 0;
+    for (;;) {
+        int e = 0;
+        if (lane == 0) e = atomicAdd(&p.ctl->wrun2, 1);
+        e = __shfl_sync(0xffffffffu, e, 0);
+        if (e >= total) break;
+        const int2 r = wl2[e];
+        wit_run9(p, r.x, 1, r.y, s_a[wp], s_w[wp], xs, tests, kills);
+    }
+    if (lane == 0 && tests) {
+        atomicAdd(&p.acc[3], tests);
+        atomicAdd(&p.acc[4], kills);
+    }
+}
+
+void launch_witness(const ScanParams& p, int4* wl, int2* wl2, cudaStream_t st) {
     launch_pdl(k_witness_list, std::max(1, std::min((p.N + 255) / 256, 148 * 8)), 256, st, p, wl);
-    launch_pdl(k_witness, 148 * 2, kWitWarps * 32, st, p, (const int4*)wl);
+    if (p.N < (1 << 18)) {
+        launch_pdl(k_witness<true>, 148 * 2, 256, st, p, (const int4*)wl, wl2);
+    } else {
+        launch_pdl(k_witness<false>, 148 * 8, 256, st, p, (const int4*)wl, wl2);
+        launch_pdl(k_witness9, 148 * 2, kWitWarps * 32, st, p, (const int2*)wl2);
+    }
 }
 
 // Overflow fallback, the analogue of the reference's full exact pass for a
@@ -1882,6 +1976,9 @@ __global__ void k_try_init(uint8_t* __restrict__ alive, unsigned* __restrict__ y
         ctl->bnb = 0;
         ctl->lk = 0.0;
         ctl->wn = 0;
+        ctl->wn2 = 0;
+        ctl->wrun = 0;
+        ctl->wrun2 = 0;
         for (int k = 0; k < 32; ++k) ctl->slotc[k] = 0;
         ctl->tepoch += 1;
         acc[0] = acc[1] = acc[2] = acc[3] = acc[4] = 0ull;
