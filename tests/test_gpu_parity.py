@@ -151,6 +151,24 @@ def test_merlin_golden_c2_schedule_knobs(engine, knobs):
             engine.set_param(k, v)
 
 
+@pytest.mark.parametrize("knobs", [dict(pass0_pk=0), dict(pass0_pk=1, wit_cache=0),
+                                   dict(pass0_pk=1, pk_rows=256, half_pk=1), dict(witness=0, row_cache=0)])
+def test_merlin_golden_c3s_schedule_knobs(engine, knobs):
+    # n = 5e5 (ECG-like): the pair-kill band 0 (both ends of every pair from one
+    # walk), the paired two-sided walk, the witness run-seed cache and other
+    # block sizes / strides all give the reference's records bit for bit
+    fx = load_golden("c3s.json")
+    engine.set_series(series_of(fx["input"]))
+    for k, v in knobs.items():
+        engine.set_param(k, v)
+    try:
+        rep = engine.merlin_full(fx["min_len"], fx["max_len"], top_k=fx["top_k"], seglen=fx["seglen"])
+        check_merlin(rep, fx)
+    finally:
+        for k, v in dict(pass0_pk=1, wit_cache=1, pk_rows=0, half_pk=3, witness=1, row_cache=1).items():
+            engine.set_param(k, v)
+
+
 @pytest.mark.slow
 def test_merlin_golden_c4(engine):
     # BASELINE config 4: n=1,000,000 random walk, lengths 512..1024 (513 lengths);
