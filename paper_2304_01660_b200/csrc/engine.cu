@@ -286,7 +286,7 @@ struct tsd_ctx {
     long long half_bands_m = 128;
     int pass0_pk = 1;  // band 0 walks every pair once and kills both ends (k_band0_pk)
     int pk_rows = 0;   // rows per block of the pair-kill walk (0: 384)
-    int half_pk = 3;   // its evaluation stride ((2j + step) % 3: spread over rows and partners)
+    int half_pk = 6;   // its evaluation stride ((j + 2 step) % 6: spread over rows and partners; 3: C4 545 ms, 6: 508, 9: 516)
     int pair_band0 = 1;  // both sides of band 0 in one packed-FP32x2 walk  // later passes use half_bands only from this length on
     int seed32_track = 1;    // FP32 seeds in the full-row launch (wider error band, half the seed cost; C4 -3.4%)
     int seed32_collect = 1;  // ... and in the collection launch
@@ -2083,7 +2083,7 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "half_bands_m") c->half_bands_m = (long long)v;
         else if (k == "pair_band0") c->pair_band0 = v != 0.0;
         else if (k == "pass0_pk") c->pass0_pk = v != 0.0;
-        else if (k == "half_pk") c->half_pk = std::max(1, std::min(3, (int)v));
+        else if (k == "half_pk") c->half_pk = v >= 9 ? 9 : (v >= 6 ? 6 : std::max(1, std::min(3, (int)v)));
         else if (k == "pk_rows") c->pk_rows = v <= 0 ? 0 : std::max(16, std::min(kMaxRows, (int)v));
         else if (k == "seed_w") c->seed_w = (float)std::max(0.01, v);
         else if (k == "band_keep") c->band_keep = (float)std::max(0.0, std::min(1.0, v));

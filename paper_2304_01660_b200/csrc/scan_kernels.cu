@@ -1263,7 +1263,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_band0_pk(const ScanParams p) {
                 // every row's cells AND every partner's cells (a partner's
                 // cells have j + step constant, so (j + step) % 3 would test
                 // a third of the partners fully and the rest never)
-                if ((2 * j + uu) % STRIDE == 0) {
+                if (STRIDE >= 6 ? (j + 2 * uu) % STRIDE == 0 : (2 * j + uu) % STRIDE == 0) {
+                    // (STRIDE 6 / 9: j + 2 step, also spread over rows and
+                    // partners; step = 9 blk + uu keeps every pattern compile-time)
                     const float2 x = __fmul2_rn(cov[j], rn[(j + uu) % kDiag]);
                     mx0 = fmaxf(mx0, x.x);
                     mx1 = fmaxf(mx1, x.y);
@@ -2875,6 +2877,10 @@ int band0_pk_slots() {
         cudaFuncSetAttribute(k_band0_pk<1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaFuncSetAttribute(k_band0_pk<2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaFuncSetAttribute(k_band0_pk<3>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_band0_pk<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        cudaFuncSetAttribute(k_band0_pk<6>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_band0_pk<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        cudaFuncSetAttribute(k_band0_pk<9>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_band0_pk<3>, kThreads, bytes);
         if (const char* e = std::getenv("TSD_SCAN_CTAS")) per = std::min(per, std::max(1, std::atoi(e)));
         g_pk_grid = sms * (per > 0 ? per : 1);
@@ -2886,6 +2892,8 @@ static void launch_band0_pk(const ScanParams& p, cudaStream_t st) {
     const int grid = band0_pk_slots();
     const size_t bytes = sizeof(PkSmem);
     if (p.half == 2) launch_pdl_smem(k_band0_pk<2>, grid, kThreads, bytes, st, p);
+    else if (p.half >= 9) launch_pdl_smem(k_band0_pk<9>, grid, kThreads, bytes, st, p);
+    else if (p.half >= 6) launch_pdl_smem(k_band0_pk<6>, grid, kThreads, bytes, st, p);
     else if (p.half >= 3) launch_pdl_smem(k_band0_pk<3>, grid, kThreads, bytes, st, p);
     else launch_pdl_smem(k_band0_pk<1>, grid, kThreads, bytes, st, p);
 }

@@ -1,5 +1,4 @@
 cd $GRAFT_REPO_ROOT
-python scripts/cmp_golden.py c4.json
-python scripts/cmp_golden.py c3.json
-python scripts/cmp_golden.py c2.json
-for c in c4 c5 c3 c2; do python scripts/tune.py $c wit_cache=1 2>&1 | tail -1; done
+python scripts/tune.py c4 pk_rows=320,352,384,416,448 2>&1 | tail -5
+python scripts/tune.py c3 pk_rows=448,480,512 2>&1 | tail -3
+python scripts/tune.py c5 pk_rows=448,480,512 2>&1 | tail -3
