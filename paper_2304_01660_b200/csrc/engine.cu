@@ -285,7 +285,8 @@ struct tsd_ctx {
     int half_pass0 = 3, half_bands = 3;
     long long half_bands_m = 128;
     int pass0_pk = 1;  // band 0 walks every pair once and kills both ends (k_band0_pk)
-    int pk_rows = 0;   // rows per block of the pair-kill walk (0: 384)
+    int pk_rows = 0;   // rows per block of the pair-kill walk (0: by the grid's waves)
+    int64_t pk_min_n = 1 << 15;  // the pair-kill walk from this many subsequences on (C2: 32.2 -> 30.4 ms; C1: 8.8 -> 9.3 ms, so not below)
     int half_pk = 6;   // its evaluation stride ((j + 2 step) % 6: spread over rows and partners; 3: C4 545 ms, 6: 508, 9: 516)
     int pair_band0 = 1;  // both sides of band 0 in one packed-FP32x2 walk  // later passes use half_bands only from this length on
     int seed32_track = 1;    // FP32 seeds in the full-row launch (wider error band, half the seed cost; C4 -3.4%)
@@ -544,6 +545,7 @@ struct tsd_ctx {
     // rows 421 ms / 384: 464 / 512: 428; C5 (N = 2e6) 512 rows 800 ms / 384:
     // 807.  The first target wave count with L <= 512 (nearest multiple of 32) wins.
     int pk_block_rows(int64_t N) const {
+        if (N < (1 << 18)) return 256;  // below a wave anyway (C2: 256 rows 30.4 ms, 128: 30.5, 512: 31.2)
         const double g = (double)band0_pk_slots();
         for (double w : {0.9, 2.2, 3.3, 4.4, 5.5, 6.6, 7.7}) {
             const int L = (int)std::lround((double)N / (2.0 * g * w) / 32.0) * 32;
@@ -569,7 +571,7 @@ struct tsd_ctx {
         // the paired walk only when its largest blocks still fill a wave
         // (measured: C4 / C5 gain 1-2%; at C2 the smaller blocks it would need
         // cost more in staging than the walk saves)
-        if (pass0_pk && pair_band0 != 0 && band0_sides == 2 && N >= (1 << 18)) {
+        if (pass0_pk && pair_band0 != 0 && band0_sides == 2 && N >= pk_min_n) {
             // pair-kill walk: a slot is two blocks' positive sides
             seed_pair = true;
             seed_L = pk_rows > 0 ? pk_rows : pk_block_rows(N);
@@ -2078,12 +2080,13 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "band0_sides") c->band0_sides = v <= 1.0 ? 1 : 2;
         else if (k == "track_chunks") c->track_chunks = std::max(1, std::min(16, (int)v));
         else if (k == "band_few") c->band_few = std::max(0, (int)v);
-        else if (k == "half_pass0") c->half_pass0 = std::max(1, std::min(3, (int)v));
+        else if (k == "half_pass0") c->half_pass0 = v >= 6 ? 6 : std::max(1, std::min(3, (int)v));
         else if (k == "half_bands") c->half_bands = std::max(1, std::min(3, (int)v));
         else if (k == "half_bands_m") c->half_bands_m = (long long)v;
         else if (k == "pair_band0") c->pair_band0 = v != 0.0;
         else if (k == "pass0_pk") c->pass0_pk = v != 0.0;
         else if (k == "half_pk") c->half_pk = v >= 9 ? 9 : (v >= 6 ? 6 : std::max(1, std::min(3, (int)v)));
+        else if (k == "pk_min_n") c->pk_min_n = (int64_t)v;
         else if (k == "pk_rows") c->pk_rows = v <= 0 ? 0 : std::max(16, std::min(kMaxRows, (int)v));
         else if (k == "seed_w") c->seed_w = (float)std::max(0.01, v);
         else if (k == "band_keep") c->band_keep = (float)std::max(0.0, std::min(1.0, v));

@@ -2918,6 +2918,7 @@ void launch_scan(int mode, const ScanParams& p, cudaStream_t st) {
                 break;
             }
             if (p.half == 2) launch_pdl(k_scan<kPrune, 2>, scan_grid<kPrune>(), kThreads, st, p);
+            else if (p.half >= 6) launch_pdl(k_scan<kPrune, 6>, scan_grid<kPrune>(), kThreads, st, p);
             else if (p.half >= 3) launch_pdl(k_scan<kPrune, 3>, scan_grid<kPrune>(), kThreads, st, p);
             else launch_pdl(k_scan<kPrune>, scan_grid<kPrune>(), kThreads, st, p);
             break;

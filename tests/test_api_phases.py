@@ -75,19 +75,27 @@ def test_stats_walk_offset_series_bitexact(engine, oracle):
     assert np.array_equal(mu, omu) and np.array_equal(sg, osg)
 
 
-def test_resident_seed_rows_follow_the_length_recurrence(engine, oracle):
+@pytest.mark.parametrize("pk", [0, 1])
+def test_resident_seed_rows_follow_the_length_recurrence(engine, oracle, pk):
     # north_star (a): QT_{m+1}(i, q) = QT_m(i, q) + t[i+m] t[q+m] on the device;
     # after 100 steps the rows equal direct FP64 dot products to ~1e-13 relative
+    # (the pair-kill band 0 keeps only the positive-side rows, b even)
     x = oracle.gen_randomwalk(12_000, 6)
-    engine.set_series(x)
-    m0, m1 = 16, 116
-    engine.stats_walk(m0, m1, fused=True)
-    info, rows = engine.seed_rows()
+    engine.set_param("pass0_pk", pk)
+    try:
+        engine.set_series(x)
+        m0, m1 = 16, 116
+        engine.stats_walk(m0, m1, fused=True)
+        info, rows = engine.seed_rows()
+    finally:
+        engine.set_param("pass0_pk", 1)
     m, L, kA, nb = (int(v) for v in info)
     assert m == m1 and nb > 0
     N = len(x) - m + 1
     worst = 0.0
     for b in range(0, nb, max(1, nb // 7)):
+        if pk and (b & 1):
+            continue
         j = b >> 1
         i = j * L + L - 1 if (b & 1) else j * L
         if i >= N:
