@@ -266,7 +266,14 @@ int tsd_fp32_peak_probe(int device, double* tflops);
  *   seed_w          cost-model weight of a seed element vs a walked row
  *   seed32_track, seed32_collect           FP32 seeds in those launches
  *   track_chunks    tracked full-row chunks (1: one catch-all launch)
- *   witness         kill witnesses of earlier tries tested before band pass 0 (1)
+ *   witness         kill witnesses of earlier tries, tested right after band pass 0 (1)
+ *   wit_cache       the witness test's run-seed cache (1)
+ *   band_few_wit    with witnesses: band passes stop at this many rows (0: auto)
+ *   pass0_pk        band 0 walks every pair once, both ends killed (1)
+ *   pk_min_n, pk_rows, half_pk   its minimum N, block rows (0: auto), stride (6)
+ *   row_cache, rc_min_m          resident full rows of anchors next to the
+ *                   previous tries' survivors (1, from m = 384)
+ *   dev_barrier     rank groups: device flag barriers (-1 auto, 0 host, 1 device)
  *   fused_peers     rank groups: peer stores inside the kernels (1)
  *   scan_events     bracket scans with events (per-phase timing; slower)
  *   result_prefix   records copied back with the try's single sync */
