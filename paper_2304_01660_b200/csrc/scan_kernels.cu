@@ -139,6 +139,8 @@ __device__ __noinline__ void slow_track(const F9 x, const F9 qn, float tz, float
                                         int qbase, int N, int m, double r_sq, double thr0, double E, double xs,
                                         uint8_t* alive, uint8_t* const* peer_alive, int npeer, int2* queue,
                                         int* queue_count, int queue_cap, int* wit) {
+    double best = 0.0;  // largest kill margin of this call (its diagonal becomes the witness)
+    int best_q = -1;
 #pragma unroll
     for (int j = 0; j < kDiag; ++j) {
         if (!(x.v[j] > tz)) continue;
@@ -159,12 +161,16 @@ __device__ __noinline__ void slow_track(const F9 x, const F9 qn, float tz, float
         if (corr - ec > thr0) {
             if (npeer > 1) for (int r = 0; r < npeer; ++r) peer_alive[r][c] = 0;
             else alive[c] = 0;
-            if (wit) wit[c] = q - c - kDiag / 2;  // the killer in the middle of the next try's 9
+            if (corr - ec - thr0 > best) {
+                best = corr - ec - thr0;
+                best_q = q;
+            }
         } else if (corr + ec >= thr0) {
             const int at = atomicAdd(queue_count, 1);
             if (at < queue_cap) queue[at] = make_int2(c, q);
         }
     }
+    if (wit && best_q >= 0) wit[c] = best_q - c - kDiag / 2;  // the killer in the middle of the next try's 9
 }
 
 // FP64 direct seeds: cov(c_first, q) for this thread's kDiag diagonals, q =
@@ -1687,6 +1693,7 @@ __device__ __forceinline__ void wit_run9(const ScanParams& p, int c0, int L, int
         }
         if (!p.alive[c]) continue;  // killed meanwhile (warp-uniform)
         bool kill = false;
+        double margin = -1.0;
         if (lane < kDiag && q >= 0 && q < N && abs(q - c) >= m && p.nrm[q] > 0.f) {
             const double dmu = p.mu[q] - B;
             const double cov = qt - dmu * delta;
@@ -1694,11 +1701,24 @@ __device__ __forceinline__ void wit_run9(const ScanParams& p, int c0, int L, int
             const double err = ((double)(m + 8 + 4 * s) * u_m * wa * (wb + fabs(dmu)) +
                                 4.0 * kEps64 * (fabs(qt) + fabs(cov))) /
                                den;
-            kill = cov / den - (err + xs) > p.thr0;
+            margin = cov / den - (err + xs) - p.thr0;
+            kill = margin > 0.0;
         }
         const unsigned km = __ballot_sync(0xffffffffu, kill);
         if (km) {
-            if (lane == __ffs(km) - 1) {
+            // the killer with the largest margin becomes the witness (the most
+            // likely to kill again at the next length)
+            int bl = lane;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double om = __shfl_xor_sync(0xffffffffu, margin, o);
+                const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+                if (om > margin || (om == margin && ol < bl)) {
+                    margin = om;
+                    bl = ol;
+                }
+            }
+            if (lane == bl) {
                 peer_kill(p.peers, p.alive, c);
                 peer_kill(p.peers, p.alive, q);
                 p.wit[c] = q - c - kDiag / 2;  // re-centred on the killing diagonal
