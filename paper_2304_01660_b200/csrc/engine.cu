@@ -98,6 +98,8 @@ constexpr int kCollCap = 1 << 23;
 struct tsd_ctx {
     int device = 0;
     cudaStream_t st = nullptr;
+    cudaStream_t st2 = nullptr;  // side stream (resident seeds built beside init_stats)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::string err;
 
     // series
@@ -1206,6 +1208,9 @@ void tsd_ctx_destroy(tsd_ctx* c) {
     for (int r = 0; r < (int)c->ipc_peer_ev.size(); ++r)
         if (r != c->rank && c->ipc_peer_ev[r]) cudaEventDestroy(c->ipc_peer_ev[r]);
     if (c->ipc_ev) cudaEventDestroy(c->ipc_ev);
+    if (c->st2) cudaStreamDestroy(c->st2);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     delete c->ipc_bar;
     c->t.release();
     c->mu.release();
@@ -1528,11 +1533,25 @@ int tsd_merlin(tsd_ctx* c, int64_t min_len, int64_t max_len, const tsd_merlin_op
         ck(cudaEventRecord(c->ev_t0, c->st), "event");
 
         std::vector<double> history;
-        c->init_stats_dev(min_len);
         // band-0 seeds resident for the whole run when the band fits (kA = maxL
-        // keeps every band-0 diagonal a non-self match at every length)
+        // keeps every band-0 diagonal a non-self match at every length); they
+        // depend on the series only, so they are built on a side stream while
+        // the single-threaded Eq. 4 running sums of init_stats run
         c->seed_m = -1;
-        if ((int64_t)max_len + kW < n - max_len + 1) c->seed_init(min_len, max_len);
+        const bool seeded = (int64_t)max_len + kW < n - max_len + 1;
+        if (seeded) {
+            if (!c->st2) ck(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking), "stream");
+            if (!c->ev_fork) ck(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "event");
+            if (!c->ev_join) ck(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "event");
+            ck(cudaEventRecord(c->ev_fork, c->st), "event");
+            ck(cudaStreamWaitEvent(c->st2, c->ev_fork, 0), "event wait");
+            std::swap(c->st, c->st2);
+            c->seed_init(min_len, max_len);  // on the side stream
+            std::swap(c->st, c->st2);
+            ck(cudaEventRecord(c->ev_join, c->st2), "event");
+        }
+        c->init_stats_dev(min_len);
+        if (seeded) ck(cudaStreamWaitEvent(c->st, c->ev_join, 0), "event wait");
         c->rc_reset();
         // every discovery starts from scratch: no kill witnesses from an earlier call
         if (c->wit.p) ck(cudaMemsetAsync(c->wit.p, 0x80, c->wit.cap * sizeof(int), c->st), "memset");
