@@ -631,6 +631,7 @@ struct tsd_ctx {
         p.world = world;
         p.acc = acc.p;
         p.peers = peers;
+        p.pfx1 = pfx1.p;
         if (debug) {
             dbgc.ensure(8);
             p.dbg = dbgc.p;

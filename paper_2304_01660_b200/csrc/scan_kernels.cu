@@ -399,7 +399,12 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
         float acc[kDiag];
 #pragma unroll
         for (int i = 0; i < kDiag; ++i) acc[i] = 0.f;
-        float delta = 0.f, wmax = 0.f;
+        float wmax = 0.f;
+        // sum_p (t[c+p] - mu_c) exactly from the double-double prefix sums (no
+        // FADD per element in the loop; its rounding, ~u (|S_c| + m |mu_c|), is
+        // orders below kSlack in correlation units)
+        const double2 pc1 = p.pfx1[c_first + m], pc0 = p.pfx1[c_first];
+        const double delta = ((pc1.x - pc0.x) + (pc1.y - pc0.y)) - (double)m * mu_c;
         for (int pc = 0; pc < m; pc += kSeedChunk) {
             const int len = min(kSeedChunk, m - pc);
             __syncthreads();
@@ -417,19 +422,22 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
 #pragma unroll
             for (int i = 0; i < kDiag - 1; ++i) w[i] = S.u.seed32.win[o_t + i];
             int pp = 0;
-            for (; pp + kDiag <= len; pp += kDiag) {
+            // 18 elements per iteration: the broadcast row values as 9 float2
+            // loads (pp stays a multiple of 18, so 8-byte aligned)
+            for (; pp + 2 * kDiag <= len; pp += 2 * kDiag) {
+                float2 a2[kDiag];
 #pragma unroll
-                for (int uu = 0; uu < kDiag; ++uu) {
+                for (int i = 0; i < kDiag; ++i) a2[i] = reinterpret_cast<const float2*>(S.u.seed32.a + pp)[i];
+#pragma unroll
+                for (int uu = 0; uu < 2 * kDiag; ++uu) {
                     w[(uu + kDiag - 1) % kDiag] = S.u.seed32.win[o_t + pp + uu + kDiag - 1];
-                    const float av = S.u.seed32.a[pp + uu];
-                    delta += av;
+                    const float av = (uu & 1) ? a2[uu >> 1].y : a2[uu >> 1].x;
 #pragma unroll
                     for (int i = 0; i < kDiag; ++i) acc[i] = fmaf(av, w[(uu + i) % kDiag], acc[i]);
                 }
             }
             for (; pp < len; ++pp) {
                 const float av = S.u.seed32.a[pp];
-                delta += av;
 #pragma unroll
                 for (int i = 0; i < kDiag; ++i) acc[i] = fmaf(av, S.u.seed32.win[o_t + pp + i], acc[i]);
             }
@@ -446,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
 #pragma unroll
         for (int i = 0; i < kDiag; ++i) {
             const int q = qlo + o_t + i;
-            seedv[i] = (q >= 0 && q < N) ? (double)acc[i] - (p.mu[q] - anchor) * (double)delta : 0.0;
+            seedv[i] = (q >= 0 && q < N) ? (double)acc[i] - (p.mu[q] - anchor) * delta : 0.0;
         }
         if (dir > 0) {
 #pragma unroll
