@@ -351,6 +351,10 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
             ext = 0;
         }
     }
+    if (MODE == kPruneTrack && p.dbg && tid == 0) {
+        atomicAdd(&p.dbg[rc >= 0 ? 8 : (td.seed >= 0 ? 11 : 9)], 1ull);
+        atomicAdd(&p.dbg[10], (unsigned long long)td.rows);
+    }
     const int rows = td.rows;
     const int dir = td.dir;
     const int N = p.N;
