@@ -1768,11 +1768,11 @@ __global__ void __launch_bounds__(256) k_witness(const ScanParams p, const int4*
     const double xs_res = stats_band(p, true) + kSlack + 1e-12;  // cached raw seeds: the resident term
     const int total = p.ctl->wn;
     unsigned long long tests = 0, kills = 0;
-    for (;;) {
-        // runs are fetched one at a time per warp (their costs vary widely)
-        int e = 0;
-        if (lane == 0) e = atomicAdd(&p.ctl->wrun, 1);
-        e = __shfl_sync(0xffffffffu, e, 0);
+    // runs are dealt one at a time per warp (their costs vary widely): the
+    // first by warp index, the rest from a counter (one shared counter hit by
+    // every warp of the grid serialised the whole kernel at C4)
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    for (int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);;) {
         if (e >= total) break;
         const int4 run = wl[e];
         const int c0 = run.x, L = run.y, kb = run.z;  // kb: the run's (own or borrowed) witness
@@ -1907,6 +1907,8 @@ __global__ void __launch_bounds__(256) k_witness(const ScanParams p, const int4*
             at = __shfl_sync(0xffffffffu, at, 0);
             if ((rest >> lane) & 1u) wl2[at + __popc(rest & ((1u << lane) - 1u))] = make_int2(c, kb);
         }
+        if (lane == 0) e = nwarps + atomicAdd(&p.ctl->wrun, 1);
+        e = __shfl_sync(0xffffffffu, e, 0);
     }
     if (lane == 0 && tests) {
         atomicAdd(&p.acc[3], tests);
@@ -1924,13 +1926,12 @@ __global__ void __launch_bounds__(kWitWarps * 32) k_witness9(const ScanParams p,
     const double xs = stats_band(p, false) + kSlack + 1e-12;
     const int total = p.ctl->wn2;
     unsigned long long tests = 0, kills = 0;
-    for (;;) {
-        int e = 0;
-        if (lane == 0) e = atomicAdd(&p.ctl->wrun2, 1);
-        e = __shfl_sync(0xffffffffu, e, 0);
-        if (e >= total) break;
+    const int nwarps = gridDim.x * kWitWarps;
+    for (int e = blockIdx.x * kWitWarps + wp; e < total;) {  // first row by warp index, then a counter
         const int2 r = wl2[e];
         wit_run9(p, r.x, 1, r.y, s_a[wp], s_w[wp], xs, tests, kills);
+        if (lane == 0) e = nwarps + atomicAdd(&p.ctl->wrun2, 1);
+        e = __shfl_sync(0xffffffffu, e, 0);
     }
     if (lane == 0 && tests) {
         atomicAdd(&p.acc[3], tests);
