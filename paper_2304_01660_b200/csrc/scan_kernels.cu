@@ -1907,6 +1907,7 @@ __global__ void __launch_bounds__(256) k_witness(const ScanParams p, const int4*
             at = __shfl_sync(0xffffffffu, at, 0);
             if ((rest >> lane) & 1u) wl2[at + __popc(rest & ((1u << lane) - 1u))] = make_int2(c, kb);
         }
+        if (total <= nwarps) break;  // one run per warp at most: no counter traffic
         if (lane == 0) e = nwarps + atomicAdd(&p.ctl->wrun, 1);
         e = __shfl_sync(0xffffffffu, e, 0);
     }
@@ -1930,6 +1931,7 @@ __global__ void __launch_bounds__(kWitWarps * 32) k_witness9(const ScanParams p,
     for (int e = blockIdx.x * kWitWarps + wp; e < total;) {  // first row by warp index, then a counter
         const int2 r = wl2[e];
         wit_run9(p, r.x, 1, r.y, s_a[wp], s_w[wp], xs, tests, kills);
+        if (total <= nwarps) break;
         if (lane == 0) e = nwarps + atomicAdd(&p.ctl->wrun2, 1);
         e = __shfl_sync(0xffffffffu, e, 0);
     }
