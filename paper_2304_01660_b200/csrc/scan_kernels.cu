@@ -1274,7 +1274,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_band0_pk(const ScanParams p) {
                 cov[j] = __ffma2_rn(cdf, make_float2(rd[rj].z, rd[rj].w), cov[j]);
                 cov[j] = __ffma2_rn(make_float2(rd[rj].x, rd[rj].y), cdg, cov[j]);
             }
-            float mx0 = -FLT_MAX, mx1 = -FLT_MAX;
+            bool h0 = false, h1 = false;
 #pragma unroll
             for (int j = 0; j < kDiag; ++j)
                 // sampled cells: (2j + step) % 3 == 0 spreads the samples over
@@ -1285,14 +1285,16 @@ __global__ void __launch_bounds__(kThreads, 4) k_band0_pk(const ScanParams p) {
                     // (STRIDE 6 / 9: j + 2 step, also spread over rows and
                     // partners; step = 9 blk + uu keeps every pattern compile-time)
                     const float2 x = __fmul2_rn(cov[j], rn[(j + uu) % kDiag]);
-                    mx0 = fmaxf(mx0, x.x);
-                    mx1 = fmaxf(mx1, x.y);
-                    // the partner q of this cell (u = ss + ub + j) dies with the row
-                    if (x.x > tc.x) hA[ss + j] = 1;
-                    if (x.y > tc.y) hB[ss + j] = 1;
+                    // the row dies if any sampled cell passes (NaN never does),
+                    // and the partner q of the cell (u = ss + ub + j) with it
+                    const bool b0 = x.x > tc.x, b1 = x.y > tc.y;
+                    if (b0) hA[ss + j] = 1;
+                    if (b1) hB[ss + j] = 1;
+                    h0 |= b0;
+                    h1 |= b1;
                 }
-            hit0 |= (mx0 > tc.x ? 1u : 0u) << (sh + uu);
-            hit1 |= (mx1 > tc.y ? 1u : 0u) << (sh + uu);
+            hit0 |= (h0 ? 1u : 0u) << (sh + uu);
+            hit1 |= (h1 ? 1u : 0u) << (sh + uu);
             rd[uu % kDiag] = qdp[ss + kDiag];
             rn[uu % kDiag] = qnp[ss + kDiag];
         }
