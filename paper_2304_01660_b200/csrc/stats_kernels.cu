@@ -354,17 +354,37 @@ __global__ void __launch_bounds__(256, 6) k_next_length(const double* __restrict
                               float* __restrict__ nrm, int* __restrict__ cr, int* __restrict__ cr_next, int L, int kA,
                               int nb, int bstep, double* __restrict__ qt, int* __restrict__ deg,
                               const double2* __restrict__ P1, const double2* __restrict__ P2,
-                              int* __restrict__ degc, int* __restrict__ deg2) {
+                              int* __restrict__ degc, int* __restrict__ deg2, int qblocks) {
     pdl_enter();
     const int m1 = m + 1, cnt = n - m;
     if (blockIdx.x == 0 && threadIdx.x < kCrInts) cr_next[threadIdx.x] = 0;
+    if ((int)blockIdx.x < qblocks) {
+        // the first qblocks blocks advance the resident seed rows, the rest the
+        // statistics: two independent load chains side by side instead of one
+        // after the other in every block.  One row per block iteration: no
+        // 64-bit index division, the row value t[i+m] is a broadcast, qt and
+        // t[q+m] are coalesced.
+        for (int b = blockIdx.x * bstep; b < nb; b += qblocks * bstep) {  // bstep 2: positive sides only
+            const int j = b >> 1;
+            const int i = (b & 1) ? j * L + L - 1 : j * L;
+            if (i >= cnt) continue;
+            const double ti = t[i + m];
+            double* row = qt + (size_t)b * kW;
+            for (int u = threadIdx.x; u < kW; u += blockDim.x) {
+                const int q = (b & 1) ? i - kA - u : i + kA + u;
+                if (q >= 0 && q < cnt) row[u] = fma(ti, t[q + m], row[u]);
+            }
+        }
+        return;
+    }
     float amax = 0.f, bmax = 0.f;
     const double sqm = sqrt((double)m1), inv_m1 = 1.0 / (double)m1;
     const int lane = threadIdx.x & 31;
     // each warp advances 32 consecutive windows and stores the last 31: lane 0's
     // window is the halo whose new mean the next lane needs for dg (every lane
     // runs exactly one advance; no lane recomputes a neighbour's)
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const int gw = ((blockIdx.x - qblocks) * blockDim.x + threadIdx.x) >> 5,
+              nw = ((gridDim.x - qblocks) * blockDim.x) >> 5;
     for (int base = gw * 31; base < cnt; base += nw * 31) {  // warp-uniform
         const int i = base + lane - 1;
         double u = 0.0, s = 0.0;
@@ -393,21 +413,6 @@ __global__ void __launch_bounds__(256, 6) k_next_length(const double* __restrict
         }
     }
     stats_max_commit(amax, bmax, cr);
-    if (qt != nullptr) {
-        // one seed row per block iteration: no 64-bit index division, the row
-        // value t[i+m] is a broadcast, qt and t[q+m] are coalesced
-        for (int b = blockIdx.x * bstep; b < nb; b += gridDim.x * bstep) {  // bstep 2: positive sides only
-            const int j = b >> 1;
-            const int i = (b & 1) ? j * L + L - 1 : j * L;
-            if (i >= cnt) continue;
-            const double ti = t[i + m];
-            double* row = qt + (size_t)b * kW;
-            for (int u = threadIdx.x; u < kW; u += blockDim.x) {
-                const int q = (b & 1) ? i - kA - u : i + kA + u;
-                if (q >= 0 && q < cnt) row[u] = fma(ti, t[q + m], row[u]);
-            }
-        }
-    }
 }
 
 static int grid_for(long long work, int threads) {
@@ -450,8 +455,10 @@ void launch_next_length(const double* t, int n, int m, const double* mu_in, cons
                         double* sig_out, float* df, float* dg, float* nrm, int* cr, int* cr_next, int L, int kA,
                         int nb, int bstep, double* qt, int* deg, const double2* P1, const double2* P2, int* degc, int* deg2,
                         cudaStream_t st) {
-    launch_pdl(k_next_length, grid_for(n - m, 256), 256, st, t, n, m, mu_in, sig_in, mu_out, sig_out, df, dg, nrm, cr,
-               cr_next, L, kA, nb, bstep, qt, deg, P1, P2, degc, deg2);
+    const int rows = qt != nullptr ? (nb + bstep - 1) / bstep : 0;
+    const int qblocks = std::min(rows, 148 * 4);
+    launch_pdl(k_next_length, grid_for(n - m, 256) + qblocks, 256, st, t, n, m, mu_in, sig_in, mu_out, sig_out, df, dg,
+               nrm, cr, cr_next, L, kA, nb, bstep, qt, deg, P1, P2, degc, deg2, qblocks);
 }
 
 }  // namespace tsd
