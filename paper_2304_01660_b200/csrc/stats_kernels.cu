@@ -370,9 +370,22 @@ __global__ void __launch_bounds__(256, 6) k_next_length(const double* __restrict
             if (i >= cnt) continue;
             const double ti = t[i + m];
             double* row = qt + (size_t)b * kW;
-            for (int u = threadIdx.x; u < kW; u += blockDim.x) {
+            // every load of the row slice first (5 entries per thread in flight)
+            constexpr int kPer = (kW + 255) / 256;
+            double rv[kPer], tv[kPer];
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) {
+                const int u = threadIdx.x + k * 256;
                 const int q = (b & 1) ? i - kA - u : i + kA + u;
-                if (q >= 0 && q < cnt) row[u] = fma(ti, t[q + m], row[u]);
+                const bool ok = u < kW && q >= 0 && q < cnt;
+                rv[k] = ok ? row[u] : 0.0;
+                tv[k] = ok ? t[q + m] : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) {
+                const int u = threadIdx.x + k * 256;
+                const int q = (b & 1) ? i - kA - u : i + kA + u;
+                if (u < kW && q >= 0 && q < cnt) row[u] = fma(ti, tv[k], rv[k]);
             }
         }
         return;
