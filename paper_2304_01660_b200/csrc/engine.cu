@@ -633,9 +633,9 @@ struct tsd_ctx {
         p.peers = peers;
         p.pfx1 = pfx1.p;
         if (debug) {
-            if (dbgc.cap < 12) {
-                dbgc.ensure(12);
-                ck(cudaMemset(dbgc.p, 0, 12 * sizeof(unsigned long long)), "memset");
+            if (dbgc.cap < 16) {
+                dbgc.ensure(16);
+                ck(cudaMemset(dbgc.p, 0, 16 * sizeof(unsigned long long)), "memset");
             }
             p.dbg = dbgc.p;
         }
@@ -726,12 +726,16 @@ struct tsd_ctx {
         sync();
         const TryCtl& c = *h_ctl.p;
         if (dbgc.p) {
-            unsigned long long d[12] = {};
+            unsigned long long d[16] = {};
             ck(cudaMemcpy(d, dbgc.p, sizeof d, cudaMemcpyDeviceToHost), "D2H");
             fprintf(stderr, "[tsd] slots prune %llu/%llu track %llu/%llu collect %llu/%llu witness runs %llu cached %llu\n",
                     d[1], d[0], d[3], d[2], d[5], d[4], d[6], d[7]);
             fprintf(stderr, "[tsd] track tiles: row-cache %llu direct %llu resident %llu rows %llu\n", d[8], d[9], d[11],
                     d[10]);
+            fprintf(stderr, "[tsd] slowest collection tile: %llu cycles, rows %llu k0 %lld evals %llu\n", d[12], d[13],
+                    (long long)d[14] - (1ll << 30), d[15]);
+            unsigned long long z = 0;
+            ck(cudaMemcpy(dbgc.p + 12, &z, sizeof z, cudaMemcpyHostToDevice), "H2D");
         }
         fprintf(stderr,
                 "[tsd] m=%lld r2=%.6g %s pass=%d groups=%d span=%d alive=%d stop=%d queue=%d band=[%d,+%d) "

@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
         if (work) atomicAdd(&p.dbg[2 * MODE + 1], 1ull);
     }
     if (!work) continue;
+    const long long t_start = (MODE == kCollect && p.dbg) ? clock64() : 0;
     // Row cache (full rows / collection): a resident raw QT row of an anchor
     // row at most min(m/2, room) rows before the tile's first row (dir > 0) or
     // after its last (dir < 0) replaces the tile's m-long direct seeds; the
@@ -785,6 +786,15 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
         atomicAdd(&p.acc[0], (unsigned long long)rows * (unsigned long long)kW);
         atomicAdd(&p.acc[1], (unsigned long long)evals * (unsigned long long)(kW / STRIDE));
         if (td.seed < 0 && rc < 0) atomicAdd(&p.acc[2], (unsigned long long)kW);
+        if (MODE == kCollect && p.dbg) {  // TSD_DEBUG: the slowest collection tile
+            const unsigned long long dt = (unsigned long long)(clock64() - t_start);
+            if (dt > p.dbg[12]) {
+                p.dbg[12] = dt;
+                p.dbg[13] = (unsigned long long)rows;
+                p.dbg[14] = (unsigned long long)(td.k0 + (1 << 30));
+                p.dbg[15] = (unsigned long long)evals;
+            }
+        }
     }
     }  // persistent tile loop
 }
