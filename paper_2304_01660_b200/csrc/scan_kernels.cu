@@ -327,7 +327,9 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
         if (work) atomicAdd(&p.dbg[2 * MODE + 1], 1ull);
     }
     if (!work) continue;
+#ifdef TSD_TILE_TIMING
     const long long t_start = (MODE == kCollect && p.dbg) ? clock64() : 0;
+#endif
     // Row cache (full rows / collection): a resident raw QT row of an anchor
     // row at most min(m/2, room) rows before the tile's first row (dir > 0) or
     // after its last (dir < 0) replaces the tile's m-long direct seeds; the
@@ -786,7 +788,8 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
         atomicAdd(&p.acc[0], (unsigned long long)rows * (unsigned long long)kW);
         atomicAdd(&p.acc[1], (unsigned long long)evals * (unsigned long long)(kW / STRIDE));
         if (td.seed < 0 && rc < 0) atomicAdd(&p.acc[2], (unsigned long long)kW);
-        if (MODE == kCollect && p.dbg) {  // TSD_DEBUG: the slowest collection tile
+#ifdef TSD_TILE_TIMING
+        if (MODE == kCollect && p.dbg) {  // build flag + TSD_DEBUG: the slowest collection tile
             const unsigned long long dt = (unsigned long long)(clock64() - t_start);
             if (dt > p.dbg[12]) {
                 p.dbg[12] = dt;
@@ -795,6 +798,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
                 p.dbg[15] = (unsigned long long)evals;
             }
         }
+#endif
     }
     }  // persistent tile loop
 }
