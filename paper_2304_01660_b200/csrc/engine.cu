@@ -284,12 +284,16 @@ struct tsd_ctx {
     // band-pass evaluation density, 1 cell in N (kills stay certain; a row a pass
     // misses is walked again later).  Measured: C2 41.0 -> 39.5 ms, C4 1060 ->
     // 1013 ms with 1/3 in pass 0 and 1/2 in the later band passes.
-    int half_pass0 = 3, half_bands = 3;
+    // later band passes: 20 = the middle slot of every thread's 9 diagonals
+    // only (every 9th diagonal, fully; the other slots' walks and seeds are
+    // dead code): C4 476 -> 427 ms, C5 629 -> 582 ms (3: every slot, 1 step in 3)
+    int half_pass0 = 3, half_bands = 20;
     long long half_bands_m = 128;
     int pass0_pk = 1;  // band 0 walks every pair once and kills both ends (k_band0_pk)
     int pk_rows = 0;   // rows per block of the pair-kill walk (0: by the grid's waves)
     int64_t pk_min_n = 1 << 15;  // the pair-kill walk from this many subsequences on (C2: 32.2 -> 30.4 ms; C1: 8.8 -> 9.3 ms, so not below)
-    int half_pk = 6;   // its evaluation stride ((j + 2 step) % 6: spread over rows and partners; 3: C4 545 ms, 6: 508, 9: 516)
+    int half_pk = 20;  // pass-0 pattern (pk_sampled): 20 = slot 0 of every thread, every step (C4 480 -> 466 ms,
+                       // C5 663 -> 627 ms); 6 = even slots, (j + 2 step) % 6; 12 = slots 0/3/6, one per step
     int pair_band0 = 1;  // both sides of band 0 in one packed-FP32x2 walk  // later passes use half_bands only from this length on
     int seed32_track = 1;    // FP32 seeds in the full-row launch (wider error band, half the seed cost; C4 -3.4%)
     int seed32_collect = 1;  // ... and in the collection launch
@@ -2110,11 +2114,13 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "track_chunks") c->track_chunks = std::max(1, std::min(16, (int)v));
         else if (k == "band_few") c->band_few = std::max(0, (int)v);
         else if (k == "half_pass0") c->half_pass0 = v >= 6 ? 6 : std::max(1, std::min(3, (int)v));
-        else if (k == "half_bands") c->half_bands = std::max(1, std::min(3, (int)v));
+        else if (k == "half_bands") c->half_bands = v == 20 ? 20 : std::max(1, std::min(3, (int)v));
         else if (k == "half_bands_m") c->half_bands_m = (long long)v;
         else if (k == "pair_band0") c->pair_band0 = v != 0.0;
         else if (k == "pass0_pk") c->pass0_pk = v != 0.0;
-        else if (k == "half_pk") c->half_pk = v >= 9 ? 9 : (v >= 6 ? 6 : std::max(1, std::min(3, (int)v)));
+        else if (k == "half_pk")
+            c->half_pk = (v == 12 || v == 15 || v == 16 || v == 20 || v == 21) ? (int)v
+                         : v >= 9 ? 9 : (v >= 6 ? 6 : std::max(1, std::min(3, (int)v)));
         else if (k == "pk_min_n") c->pk_min_n = (int64_t)v;
         else if (k == "pk_rows") c->pk_rows = v <= 0 ? 0 : std::max(16, std::min(kMaxRows, (int)v));
         else if (k == "seed_w") c->seed_w = (float)std::max(0.01, v);

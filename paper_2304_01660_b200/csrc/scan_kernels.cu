@@ -236,6 +236,27 @@ __device__ __forceinline__ void seed_fp64(const ScanParams& p, int c_first, int 
     }
 }
 
+// Band-pass evaluation pattern: cell (slot j, step uu) of the thread's 9
+// diagonals.  STRIDE 2 / 3: (j + step) % STRIDE, every slot.  STRIDE 20: the
+// middle slot only, every step -- every 9th diagonal of the band, each fully;
+// the other 8 slots are never read, so the compiler drops their walks AND their
+// m-long seeds (the middle slot reads the same seed on both sides).
+template <int STRIDE>
+__device__ __forceinline__ constexpr bool scan_sampled(int j, int uu) {
+    return STRIDE == 20 ? j == kDiag / 2 : (j + uu) % STRIDE == 0;
+}
+template <int STRIDE>
+__device__ __forceinline__ constexpr int scan_walked_slots() {
+    return STRIDE == 20 ? 1 : kDiag;
+}
+template <int STRIDE>
+__device__ __forceinline__ constexpr int scan_evals_per_row() {  // per thread-slice of 9 diagonals, x kThreads / 9
+    int n = 0;
+    for (int j = 0; j < kDiag; ++j)
+        for (int uu = 0; uu < kDiag; ++uu) n += scan_sampled<STRIDE>(j, uu) ? 1 : 0;
+    return n * kThreads / kDiag;
+}
+
 template <int MODE, int STRIDE = 1>
 __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(const ScanParams p) {
     pdl_enter();
@@ -657,7 +678,7 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
                     mx = -FLT_MAX;
 #pragma unroll
                     for (int j = 0; j < kDiag; ++j)
-                        if ((j + uu) % STRIDE == 0) mx = fmaxf(mx, cov[j] * rn[(j + uu) % kDiag]);
+                        if (scan_sampled<STRIDE>(j, uu)) mx = fmaxf(mx, cov[j] * rn[(j + uu) % kDiag]);
                 } else {
 #pragma unroll
                     for (int j = 0; j < kDiag; ++j) x[j] = cov[j] * rn[(j + uu) % kDiag];
@@ -785,9 +806,13 @@ __global__ void __launch_bounds__(kThreads, MODE == kPruneTrack ? 4 : 6) k_scan(
         }
     }
     if (tid == 0) {
-        atomicAdd(&p.acc[0], (unsigned long long)rows * (unsigned long long)kW);
-        atomicAdd(&p.acc[1], (unsigned long long)evals * (unsigned long long)(kW / STRIDE));
-        if (td.seed < 0 && rc < 0) atomicAdd(&p.acc[2], (unsigned long long)kW);
+        // walked cells, evaluated cells and direct seed dots actually computed
+        // (slots a pattern never reads are neither walked nor seeded)
+        constexpr int kWalked = MODE == kPrune ? scan_walked_slots<STRIDE>() * kThreads : kW;
+        constexpr int kEvals = MODE == kPrune && STRIDE > 1 ? scan_evals_per_row<STRIDE>() : kW / STRIDE;
+        atomicAdd(&p.acc[0], (unsigned long long)rows * (unsigned long long)kWalked);
+        atomicAdd(&p.acc[1], (unsigned long long)evals * (unsigned long long)kEvals);
+        if (td.seed < 0 && rc < 0) atomicAdd(&p.acc[2], (unsigned long long)kWalked);
 #ifdef TSD_TILE_TIMING
         if (MODE == kCollect && p.dbg) {  // build flag + TSD_DEBUG: the slowest collection tile
             const unsigned long long dt = (unsigned long long)(clock64() - t_start);
@@ -1068,6 +1093,40 @@ __global__ void __launch_bounds__(kThreads, 4) k_band0_pair(const ScanParams p) 
     }  // persistent tile loop
 }
 
+// Sampled cells of the pair-kill walk: slot j (diagonal ub + j of the thread)
+// at step uu of a 9-step block.  A slot that no pattern ever samples is never
+// read, so the compiler drops its walk too: STRIDE 6 samples the even slots
+// only (5 of 9 walked), 12 / 15 / 16 three slots (3 of 9 walked: slots 0, 3, 6
+// or 0, 4, 8).  Every pattern meets each partner q of a walked slot.
+template <int STRIDE>
+__device__ __forceinline__ constexpr bool pk_sampled(int j, int uu) {
+    return STRIDE == 20   ? (j == 0)
+           : STRIDE == 21 ? ((j == 0 && uu % 2 == 0) || (j == 4 && (uu == 1 || uu == 3 || uu == 6 || uu == 8)))
+           : STRIDE == 12 ? (j % 3 == 0 && (j / 3 + uu) % 3 == 0)
+           : STRIDE == 16 ? (j % 3 == 0 && (j / 3 + uu) % 3 != 2)
+           : STRIDE == 15 ? (j % 4 == 0 && (j / 4 + uu) % 3 == 0)
+           : STRIDE >= 6  ? (j + 2 * uu) % STRIDE == 0
+                          : (2 * j + uu) % STRIDE == 0;
+}
+
+template <int STRIDE>
+__device__ __forceinline__ constexpr int pk_walked_slots() {
+    int n = 0;
+    for (int j = 0; j < kDiag; ++j) {
+        bool any = false;
+        for (int uu = 0; uu < kDiag; ++uu) any = any || pk_sampled<STRIDE>(j, uu);
+        n += any ? 1 : 0;
+    }
+    return n;
+}
+template <int STRIDE>
+__device__ __forceinline__ constexpr int pk_samples() {  // sampled (slot, step) pairs per 9-step block
+    int n = 0;
+    for (int j = 0; j < kDiag; ++j)
+        for (int uu = 0; uu < kDiag; ++uu) n += pk_sampled<STRIDE>(j, uu) ? 1 : 0;
+    return n;
+}
+
 // ---------------------------------------------------------------------------
 // Band 0, every unordered pair once (pair-kill walk).
 //
@@ -1299,7 +1358,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_band0_pk(const ScanParams p) {
                 // every row's cells AND every partner's cells (a partner's
                 // cells have j + step constant, so (j + step) % 3 would test
                 // a third of the partners fully and the rest never)
-                if (STRIDE >= 6 ? (j + 2 * uu) % STRIDE == 0 : (2 * j + uu) % STRIDE == 0) {
+                if (pk_sampled<STRIDE>(j, uu)) {
                     // (STRIDE 6 / 9: j + 2 step, also spread over rows and
                     // partners; step = 9 blk + uu keeps every pattern compile-time)
                     const float2 x = __fmul2_rn(cov[j], rn[(j + uu) % kDiag]);
@@ -1332,8 +1391,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_band0_pk(const ScanParams p) {
     for (int u = tid; u < nqB; u += kThreads)
         if (S.qhit[1][u]) peer_kill(p.peers, p.alive, qbB + u);
     if (tid == 0) {
-        atomicAdd(&p.acc[0], (unsigned long long)kW * (unsigned long long)((vA ? rowsA : 0) + (vB ? rowsB : 0)));
-        atomicAdd(&p.acc[1], (unsigned long long)evals * (unsigned long long)(kW / STRIDE));
+        // cells actually walked (slots that are never sampled are not walked)
+        // and cells evaluated, per row of a walked side
+        atomicAdd(&p.acc[0], (unsigned long long)(pk_walked_slots<STRIDE>() * kThreads) *
+                                 (unsigned long long)((vA ? rowsA : 0) + (vB ? rowsB : 0)));
+        atomicAdd(&p.acc[1], (unsigned long long)evals * (unsigned long long)(pk_samples<STRIDE>() * kThreads / kDiag));
     }
     }  // persistent tile loop
 }
@@ -2936,6 +2998,16 @@ int band0_pk_slots() {
         cudaFuncSetAttribute(k_band0_pk<6>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaFuncSetAttribute(k_band0_pk<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         cudaFuncSetAttribute(k_band0_pk<9>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_band0_pk<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        cudaFuncSetAttribute(k_band0_pk<12>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_band0_pk<15>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        cudaFuncSetAttribute(k_band0_pk<15>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_band0_pk<20>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        cudaFuncSetAttribute(k_band0_pk<20>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_band0_pk<21>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        cudaFuncSetAttribute(k_band0_pk<21>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_band0_pk<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        cudaFuncSetAttribute(k_band0_pk<16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_band0_pk<3>, kThreads, bytes);
         if (const char* e = std::getenv("TSD_SCAN_CTAS")) per = std::min(per, std::max(1, std::atoi(e)));
         g_pk_grid = sms * (per > 0 ? per : 1);
@@ -2947,6 +3019,11 @@ static void launch_band0_pk(const ScanParams& p, cudaStream_t st) {
     const int grid = band0_pk_slots();
     const size_t bytes = sizeof(PkSmem);
     if (p.half == 2) launch_pdl_smem(k_band0_pk<2>, grid, kThreads, bytes, st, p);
+    else if (p.half == 12) launch_pdl_smem(k_band0_pk<12>, grid, kThreads, bytes, st, p);
+    else if (p.half == 20) launch_pdl_smem(k_band0_pk<20>, grid, kThreads, bytes, st, p);
+    else if (p.half == 21) launch_pdl_smem(k_band0_pk<21>, grid, kThreads, bytes, st, p);
+    else if (p.half == 15) launch_pdl_smem(k_band0_pk<15>, grid, kThreads, bytes, st, p);
+    else if (p.half == 16) launch_pdl_smem(k_band0_pk<16>, grid, kThreads, bytes, st, p);
     else if (p.half >= 9) launch_pdl_smem(k_band0_pk<9>, grid, kThreads, bytes, st, p);
     else if (p.half >= 6) launch_pdl_smem(k_band0_pk<6>, grid, kThreads, bytes, st, p);
     else if (p.half >= 3) launch_pdl_smem(k_band0_pk<3>, grid, kThreads, bytes, st, p);
@@ -2972,7 +3049,8 @@ void launch_scan(int mode, const ScanParams& p, cudaStream_t st) {
                 launch_band0_pair(p, st);
                 break;
             }
-            if (p.half == 2) launch_pdl(k_scan<kPrune, 2>, scan_grid<kPrune>(), kThreads, st, p);
+            if (p.half == 20) launch_pdl(k_scan<kPrune, 20>, scan_grid<kPrune>(), kThreads, st, p);
+            else if (p.half == 2) launch_pdl(k_scan<kPrune, 2>, scan_grid<kPrune>(), kThreads, st, p);
             else if (p.half >= 6) launch_pdl(k_scan<kPrune, 6>, scan_grid<kPrune>(), kThreads, st, p);
             else if (p.half >= 3) launch_pdl(k_scan<kPrune, 3>, scan_grid<kPrune>(), kThreads, st, p);
             else launch_pdl(k_scan<kPrune>, scan_grid<kPrune>(), kThreads, st, p);

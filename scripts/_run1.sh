@@ -1,8 +1,3 @@
 #!/bin/bash
-timeout 600 python scripts/cmp_golden.py c4.json 2>&1 | tail -1
-timeout 600 python scripts/cmp_golden.py c3s.json 2>&1 | tail -1
-timeout 600 python scripts/cmp_golden.py c5s.json 2>&1 | tail -1
-timeout 900 python scripts/tune.py c4 wit_wide=0,1 2>&1 | tail -2
-timeout 900 python scripts/tune.py c4 wit_wide=0,1 2>&1 | tail -2
-timeout 900 python scripts/tune.py c5 wit_wide=0,1 2>&1 | tail -2
-timeout 900 python scripts/tune.py c3 wit_wide=0,1 2>&1 | tail -2
+for g in c1.json c2.json c3s.json c4.json c5s.json small.json; do timeout 900 python scripts/cmp_golden.py $g 2>&1 | tail -1; done
+timeout 2000 python -m pytest tests -q -m gpu -x 2>&1 | tail -2
