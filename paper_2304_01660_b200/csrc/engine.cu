@@ -306,10 +306,18 @@ struct tsd_ctx {
     // Measured (rows left after which the band passes stop): C4 720 / 702 /
     // 772 ms at 16 / 64 / 256, C3 432 / 426 ms at 16 / 64, C2 33.4 / 32.5 /
     // 31.2 ms at 16 / 64 / 256.  0: automatic (256 below N = 2^18, else 64).
+    // With the one-slot band passes (half_bands 20) a pass costs about a ninth
+    // of its seeds, so from m = few_m on (where full-row seeds are longest)
+    // the passes go on down to few_lo rows: C4 417 -> 367 ms; below it 64
+    // stays best (C5 583 vs 594 ms at 2, C3 376 vs 380 ms).
     int band_few_wit = 0;
-    int few_rows(int64_t N) const {
+    int64_t few_m = 512;
+    int few_lo = 2;
+    int few_rows(int64_t N, int64_t m) const {
         if (!witness) return std::max<int>(band_few, (int)(N / 4096));
-        return band_few_wit > 0 ? band_few_wit : (N < (1 << 18) ? 256 : 64);
+        if (band_few_wit > 0) return band_few_wit;
+        if (N < (1 << 18)) return 256;
+        return m >= few_m ? few_lo : 64;
     }
     int result_prefix = 1024;  // records copied back with the try's single round trip
     // knife-edge queue / near-pair buffer capacities (settable below the
@@ -715,7 +723,7 @@ struct tsd_ctx {
         slots.ensure(group_slots(N));
         bcost.ensure((size_t)compact_blocks(N) * 6);
         launch_compact_group(alive.p, N, list.p, lbstat.p, epoch, ctl.p, gate, groups.p, slots.p, (int)m,
-                             sparse_rows, band_keep, few_rows(N), seed_w, bcost.p, band_slots(N), st);
+                             sparse_rows, band_keep, few_rows(N, m), seed_w, bcost.p, band_slots(N), st);
         ck(cudaGetLastError(), "compact");
         ctr.kernel_launches += 1;
         // fused peers: no rank's next scan may store kills into this rank's
@@ -2132,6 +2140,8 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "witness") c->witness = v != 0.0;
         else if (k == "row_cache") c->row_cache = v != 0.0;
         else if (k == "wit_cache") c->wit_cache = v != 0.0;
+        else if (k == "few_m") c->few_m = (int64_t)v;
+        else if (k == "few_lo") c->few_lo = std::max(1, (int)v);
         else if (k == "dev_barrier") {
             c->dev_barrier = v < 0 ? -1 : (v != 0.0 ? 1 : 0);
             c->use_dev_bar = c->world > 1 && c->peers.n > 1 && c->dev_barrier != 0;

@@ -1,3 +1,4 @@
 #!/bin/bash
-for g in c1.json c2.json c3s.json c4.json c5s.json small.json; do timeout 900 python scripts/cmp_golden.py $g 2>&1 | tail -1; done
-timeout 2000 python -m pytest tests -q -m gpu -x 2>&1 | tail -2
+timeout 900 python scripts/tune.py c5 few_m=256,384,512,700 2>&1 | tail -4
+timeout 900 python scripts/tune.py c4 few_m=512 few_lo=1,2,4 2>&1 | tail -3
+timeout 900 python scripts/tune.py c3 few_m=256,384,512 2>&1 | tail -3
