@@ -2113,6 +2113,7 @@ __device__ __forceinline__ bool gated_off(const TryCtl* ctl, int gate) {
 constexpr int kCompactBlock = 1024;
 constexpr int kCompactItems = 4;  // flags per thread
 constexpr int kCompactTile = kCompactBlock * kCompactItems;
+constexpr int kListPath = kCompactTile;  // list-path compaction up to this many previous rows
 
 // block-wide exclusive scan of one int per thread (blockDim.x == 1024); returns
 // the exclusive prefix, *total receives the block sum
@@ -2350,6 +2351,112 @@ __global__ void k_track_init(TryCtl* ctl, int N, int m, int bands_ran, int scan_
     track_schedule(ctl, N, m, ctl->alive == 0 ? 0 : ctl->G, scan_slots);
 }
 
+// Finalisation of one compaction (the last CTA of the sweep, or the single
+// CTA of the list path): break rule, span choice, groups, next-pass bands.
+// s_cost[0][k] holds the total grouping cost of span 16 << k; list_only forces
+// the groups straight from the list (the list path fills no span-block slots).
+__device__ __forceinline__ void compact_finalize(int total, TryCtl* ctl, int gate, const int* __restrict__ out,
+                                                 int2* __restrict__ groups, const int2* __restrict__ slots,
+                                                 int nb, int n, int m, int fixed_span, float band_keep,
+                                                 int scan_slots, int band_few, double (*s_cost)[kSpans],
+                                                 int* wsum, int& s_k, bool list_only) {
+    if (threadIdx.x == 0) {
+        ctl->cticket = 0;
+        ctl->cdone = 0;
+        if (gate >= 0) {
+            const int prev = ctl->alive;
+            ctl->prev = prev;
+            ctl->passes = gate + 1;
+            if (total == 0 || total <= band_few) {
+                ctl->stop = gate;
+                ctl->stop_why = 1;
+            } else if ((double)total > (double)band_keep * (double)prev) {
+                ctl->stop = gate;
+                ctl->stop_why = 2;
+            }
+            // next band pass (gate + 1): starts where this one ended
+            if (gate >= 1) ctl->bK0 += ctl->bnb * kW;
+        }
+        ctl->alive = total;
+        int k = 5;  // dense lists (>= 1 row in 64 undecided): whole 512-row blocks
+        if (fixed_span > 0) {
+            k = 0;
+            while (k < 5 && (16 << k) < fixed_span) ++k;
+        } else if (total > 0 && (total < kDenseMin ||
+                                 (long long)total * 64 < (long long)(__ldcg(&out[total - 1]) - __ldcg(&out[0]) + 1))) {
+            double best = 1e300;
+            for (int x = 0; x < kSpans; ++x) {
+                const double v = s_cost[0][x];
+                if (v < best) {
+                    best = v;
+                    k = x;
+                }
+            }
+        }
+        s_k = k;
+        ctl->span = 16 << k;
+    }
+    __syncthreads();
+    const int k = s_k;
+    const int nslot = nb * (256 >> k);
+    int carry = 0;
+    if (list_only || total <= nslot) {
+        // short list (the usual case after pass 0): the groups straight from the
+        // list — an entry starts a group when its span-block differs from its
+        // predecessor's — instead of a sweep over every span-block slot
+        const int sh = 4 + k;
+        for (int b0 = 0; b0 < total; b0 += blockDim.x) {
+            const int e = b0 + threadIdx.x;
+            int r = 0, st = 0, en = 0;
+            if (e < total) {
+                r = __ldcg(&out[e]);
+                st = e == 0 || (__ldcg(&out[e - 1]) >> sh) != (r >> sh);
+                en = e + 1 == total || (__ldcg(&out[e + 1]) >> sh) != (r >> sh);
+            }
+            int t2;
+            const int g = carry + block_exscan(st, wsum, &t2) + st - 1;
+            if (e < total) {
+                if (st) groups[g].x = r;
+                if (en) groups[g].y = r;
+            }
+            carry += t2;
+        }
+    } else {
+        const int2* sl = slots + slot_region(k, nb);
+        for (int b0 = 0; b0 < nslot; b0 += blockDim.x) {
+            const int e = b0 + threadIdx.x;
+            int2 v = make_int2(0, -1);
+            if (e < nslot) v = __ldcg(&sl[e]);
+            const int ff = v.y >= 0 ? 1 : 0;
+            int t2;
+            const int p2 = carry + block_exscan(ff, wsum, &t2);
+            if (ff) groups[p2] = v;
+            carry += t2;
+        }
+    }
+    if (threadIdx.x == 0) {
+        ctl->G = carry;
+        if (gate == kGateTrack) track_next(ctl, n, m, carry, scan_slots);
+        if (gate >= 0 && ctl->stop == INT_MAX) {
+            // Bands of the next pass: at least 2^p (the doubling schedule), and
+            // enough to fill one wave of the persistent scan grid — a pass with
+            // fewer tiles than CTAs costs one tile's latency anyway, so the
+            // extra bands come free and kill more rows before the full rows.
+            const long long k_max = (long long)n - 1, K0 = ctl->bK0;
+            const long long left = K0 <= k_max ? (k_max - K0 + kW) / kW : 0;
+            if (left <= 0 || carry == 0) {
+                ctl->stop = gate;
+                ctl->stop_why = 1;
+            } else {
+                long long nb = 1ll << min(gate + 1, 5);
+                const long long fill = (scan_slots + 2ll * carry - 1) / (2ll * carry);
+                if (fill > nb) nb = fill;
+                ctl->bnb = (int)(nb < left ? nb : left);
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restrict__ a, int n, int* __restrict__ out,
                                                         unsigned long long* status, unsigned epoch, TryCtl* ctl,
                                                         int gate, int2* __restrict__ groups,
@@ -2365,6 +2472,63 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
     __shared__ double s_cost[32][kSpans];
     const int nb = gridDim.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    // List path: after band pass >= 1 the undecided rows are a subset of the
+    // previous compaction's list (rows only die within a try), so a short list
+    // is filtered in one CTA instead of sweeping all n flags.  (The list size
+    // only shrinks, so a CTA starting after CTA 0 finished still takes it.)
+    if (gate >= 1 && ctl->alive <= kListPath) {
+        if (blockIdx.x != 0) return;
+        __shared__ int s_l[kListPath];
+        const int prev = ctl->alive;
+        int rr[kCompactItems], ff[kCompactItems], cnt = 0;
+#pragma unroll
+        for (int k = 0; k < kCompactItems; ++k) {
+            const int e = threadIdx.x * kCompactItems + k;
+            rr[k] = e < prev ? out[e] : 0;
+            ff[k] = (e < prev && a[rr[k]]) ? 1 : 0;
+            cnt += ff[k];
+        }
+        int tot;
+        int pos = block_exscan(cnt, wsum, &tot);
+#pragma unroll
+        for (int k = 0; k < kCompactItems; ++k)
+            if (ff[k]) s_l[pos++] = rr[k];
+        __syncthreads();
+        const double cm = (double)seed_w * (double)m + (double)(1 + kDiag);
+        double c6[kSpans];
+#pragma unroll
+        for (int k = 0; k < kSpans; ++k) c6[k] = 0.0;
+        for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+            const int r = s_l[e];
+            out[e] = r;
+            const int rp = e > 0 ? s_l[e - 1] : -1, rn = e + 1 < tot ? s_l[e + 1] : -1;
+#pragma unroll
+            for (int k = 0; k < kSpans; ++k) {
+                const int sh = 4 + k;
+                const bool st = e == 0 || (rp >> sh) != (r >> sh);
+                const bool en = e + 1 == tot || (rn >> sh) != (r >> sh);
+                // per span-block: cm + last - first (as the sweep's per-block costs)
+                c6[k] += (st ? cm - (double)r : 0.0) + (en ? (double)r : 0.0);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kSpans; ++k) {
+            double v = c6[k];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) s_cost[w][k] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < kSpans) {
+            double v = 0.0;
+            for (int x = 0; x < 32; ++x) v += s_cost[x][threadIdx.x];
+            s_cost[0][threadIdx.x] = v;
+        }
+        __syncthreads();
+        compact_finalize(tot, ctl, gate, out, groups, slots, nb, n, m, fixed_span, band_keep, scan_slots, band_few,
+                         s_cost, wsum, s_k, true);
+        return;
+    }
     if (threadIdx.x == 0) s_bid = atomicAdd(&ctl->cticket, 1);
     __syncthreads();
     const int bid = s_bid;
@@ -2523,101 +2687,8 @@ __global__ void __launch_bounds__(1024) k_compact_group(const uint8_t* __restric
         }
         __syncthreads();
     }
-    if (threadIdx.x == 0) {
-        ctl->cticket = 0;
-        ctl->cdone = 0;
-        if (gate >= 0) {
-            const int prev = ctl->alive;
-            ctl->prev = prev;
-            ctl->passes = gate + 1;
-            if (total == 0 || total <= band_few) {
-                ctl->stop = gate;
-                ctl->stop_why = 1;
-            } else if ((double)total > (double)band_keep * (double)prev) {
-                ctl->stop = gate;
-                ctl->stop_why = 2;
-            }
-            // next band pass (gate + 1): starts where this one ended
-            if (gate >= 1) ctl->bK0 += ctl->bnb * kW;
-        }
-        ctl->alive = total;
-        int k = 5;  // dense lists (>= 1 row in 64 undecided): whole 512-row blocks
-        if (fixed_span > 0) {
-            k = 0;
-            while (k < 5 && (16 << k) < fixed_span) ++k;
-        } else if (total > 0 && (total < kDenseMin ||
-                                 (long long)total * 64 < (long long)(__ldcg(&out[total - 1]) - __ldcg(&out[0]) + 1))) {
-            double best = 1e300;
-            for (int x = 0; x < kSpans; ++x) {
-                const double v = s_cost[0][x];
-                if (v < best) {
-                    best = v;
-                    k = x;
-                }
-            }
-        }
-        s_k = k;
-        ctl->span = 16 << k;
-    }
-    __syncthreads();
-    const int k = s_k;
-    const int nslot = nb * (256 >> k);
-    int carry = 0;
-    if (total <= nslot) {
-        // short list (the usual case after pass 0): the groups straight from the
-        // list — an entry starts a group when its span-block differs from its
-        // predecessor's — instead of a sweep over every span-block slot
-        const int sh = 4 + k;
-        for (int b0 = 0; b0 < total; b0 += blockDim.x) {
-            const int e = b0 + threadIdx.x;
-            int r = 0, st = 0, en = 0;
-            if (e < total) {
-                r = __ldcg(&out[e]);
-                st = e == 0 || (__ldcg(&out[e - 1]) >> sh) != (r >> sh);
-                en = e + 1 == total || (__ldcg(&out[e + 1]) >> sh) != (r >> sh);
-            }
-            int t2;
-            const int g = carry + block_exscan(st, wsum, &t2) + st - 1;
-            if (e < total) {
-                if (st) groups[g].x = r;
-                if (en) groups[g].y = r;
-            }
-            carry += t2;
-        }
-    } else {
-        const int2* sl = slots + slot_region(k, nb);
-        for (int b0 = 0; b0 < nslot; b0 += blockDim.x) {
-            const int e = b0 + threadIdx.x;
-            int2 v = make_int2(0, -1);
-            if (e < nslot) v = __ldcg(&sl[e]);
-            const int ff = v.y >= 0 ? 1 : 0;
-            int t2;
-            const int p2 = carry + block_exscan(ff, wsum, &t2);
-            if (ff) groups[p2] = v;
-            carry += t2;
-        }
-    }
-    if (threadIdx.x == 0) {
-        ctl->G = carry;
-        if (gate == kGateTrack) track_next(ctl, n, m, carry, scan_slots);
-        if (gate >= 0 && ctl->stop == INT_MAX) {
-            // Bands of the next pass: at least 2^p (the doubling schedule), and
-            // enough to fill one wave of the persistent scan grid — a pass with
-            // fewer tiles than CTAs costs one tile's latency anyway, so the
-            // extra bands come free and kill more rows before the full rows.
-            const long long k_max = (long long)n - 1, K0 = ctl->bK0;
-            const long long left = K0 <= k_max ? (k_max - K0 + kW) / kW : 0;
-            if (left <= 0 || carry == 0) {
-                ctl->stop = gate;
-                ctl->stop_why = 1;
-            } else {
-                long long nb = 1ll << min(gate + 1, 5);
-                const long long fill = (scan_slots + 2ll * carry - 1) / (2ll * carry);
-                if (fill > nb) nb = fill;
-                ctl->bnb = (int)(nb < left ? nb : left);
-            }
-        }
-    }
+    compact_finalize(total, ctl, gate, out, groups, slots, nb, n, m, fixed_span, band_keep, scan_slots, band_few,
+                     s_cost, wsum, s_k, false);
 }
 
 // per-survivor interval [lo, hi] of the exact nn^2 from the tracked route maxima
