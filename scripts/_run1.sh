@@ -1,2 +1,4 @@
 #!/bin/bash
-timeout 900 python scripts/tune.py c4 band_fill=0,12,16,32,48 2>&1 | tail -5
+timeout 900 python scripts/tune.py c4 half_pk=20,22,23 2>&1 | tail -3
+timeout 900 python scripts/tune.py c5 half_pk=20,22,23 2>&1 | tail -3
+timeout 900 python scripts/tune.py c2 half_pk=20,22,23 2>&1 | tail -3
