@@ -127,6 +127,7 @@ struct tsd_ctx {
     DBuf<double> seedqt;
     int64_t seed_m = -1;
     int seed_L = 0, seed_kA = 0, seed_nb = 0, seed_bstep = 1;
+    int seed_ustep = 1;  // entry stride of the resident rows: 9 when pass 0 reads slot 0 only (half_pk 20)
     bool seed_pair = false;  // band 0 of this run walks both sides together (k_band0_pair)
     DBuf<int> cand;
     DBuf<float> ythr;
@@ -536,7 +537,8 @@ struct tsd_ctx {
         degc.ensure(N1);
         deg2.ensure(N1);
         launch_next_length(t.p, (int)n, (int)m, mu.p, sig.p, mu2.p, sig2.p, df.p, dg.p, nrm.p, cr, crn, seed_L, seed_kA,
-                           seed_nb, seed_bstep, with_seed ? seedqt.p : nullptr, deg.p, pfx1.p, pfx2.p, degc.p, deg2.p, st);
+                           seed_nb, seed_bstep, seed_ustep, with_seed ? seedqt.p : nullptr, deg.p, pfx1.p, pfx2.p, degc.p,
+                           deg2.p, st);
         ck(cudaGetLastError(), "next length");
         ctr.kernel_launches += 1;
         std::swap(mu.p, mu2.p);
@@ -590,21 +592,23 @@ struct tsd_ctx {
             seed_pair = true;
             seed_L = pk_rows > 0 ? pk_rows : pk_block_rows(N);
             seed_bstep = 2;  // the walk reads the positive-side rows only
+            seed_ustep = half_pk == 20 ? kDiag : 1;  // ... and, for pattern 20, slot 0 of every thread
         } else {
             seed_pair = pair_band0 != 0 && band0_sides == 2 && block_rows(N, true) == kMaxRows;
             seed_L = block_rows(N, seed_pair);
             seed_bstep = 1;
+            seed_ustep = 1;
         }
         seed_kA = (int)kA;
         seed_nb = 2 * (int)((N + seed_L - 1) / seed_L);
         seedqt.ensure((size_t)seed_nb * kW);
-        launch_seed_init(t.p, (int)n, (int)m, seed_L, seed_kA, seed_nb, seed_bstep, seedqt.p, st);
+        launch_seed_init(t.p, (int)n, (int)m, seed_L, seed_kA, seed_nb, seed_bstep, seed_ustep, seedqt.p, st);
         ck(cudaGetLastError(), "seed init");
         ctr.kernel_launches += 1;
         seed_m = m;
     }
     void seed_advance() {  // seed_m -> seed_m + 1
-        launch_seed_advance(t.p, (int)n, (int)seed_m, seed_L, seed_kA, seed_nb, seed_bstep, seedqt.p, st);
+        launch_seed_advance(t.p, (int)n, (int)seed_m, seed_L, seed_kA, seed_nb, seed_bstep, seed_ustep, seedqt.p, st);
         ck(cudaGetLastError(), "seed advance");
         ctr.kernel_launches += 1;
         ++seed_m;

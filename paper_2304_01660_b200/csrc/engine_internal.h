@@ -55,8 +55,8 @@ void launch_dd_prefix(const double* t, int n, double2* tot1, double2* tot2, doub
 // advance + derive (+ seed rows when qt != nullptr) of one MERLIN length step
 void launch_next_length(const double* t, int n, int m, const double* mu_in, const double* sig_in, double* mu_out,
                         double* sig_out, float* df, float* dg, float* nrm, int* cr, int* cr_next, int L, int kA,
-                        int nb, int bstep, double* qt, int* deg, const double2* P1, const double2* P2, int* degc,
-                        int* deg2, cudaStream_t st);
+                        int nb, int bstep, int ustep, double* qt, int* deg, const double2* P1, const double2* P2,
+                        int* degc, int* deg2, cudaStream_t st);
 
 size_t scan_smem_bytes();
 void scan_configure();
@@ -105,8 +105,9 @@ void launch_rc_fill(const double* t, int n, int m, int a, double* qt, cudaStream
 void launch_rc_advance(const double* t, int n, int m, const RcRows& rows, long long stride, double* qt,
                        cudaStream_t st);
 // bstep 2: the positive-side rows only (even indices; the pair-kill band 0)
-void launch_seed_init(const double* t, int n, int m, int L, int kA, int nb, int bstep, double* qt, cudaStream_t st);
-void launch_seed_advance(const double* t, int n, int m, int L, int kA, int nb, int bstep, double* qt,
+void launch_seed_init(const double* t, int n, int m, int L, int kA, int nb, int bstep, int ustep, double* qt,
+                      cudaStream_t st);
+void launch_seed_advance(const double* t, int n, int m, int L, int kA, int nb, int bstep, int ustep, double* qt,
                          cudaStream_t st);
 void launch_gather_nn(const int* list, const int* cnt, const unsigned long long* nnkey, double* out,
                       cudaStream_t st);

@@ -2886,7 +2886,7 @@ __device__ __forceinline__ bool seed_pair(int b, int u, int L, int kA, int N, in
     return i < N && q >= 0 && q < N;
 }
 
-__global__ void k_seed_init(const double* __restrict__ t, int n, int m, int L, int kA, int nb, int bstep,
+__global__ void k_seed_init(const double* __restrict__ t, int n, int m, int L, int kA, int nb, int bstep, int ustep,
                             double* __restrict__ qt) {
     const int N = n - m + 1;
     const long long total = (long long)nb * kW;
@@ -2896,21 +2896,21 @@ __global__ void k_seed_init(const double* __restrict__ t, int n, int m, int L, i
         if (b % bstep) continue;  // rows the pair-kill walk never reads
         int i, q;
         double s = 0.0;
-        if (seed_pair(b, (int)(e % kW), L, kA, N, i, q))
+        if ((int)(e % kW) % ustep == 0 && seed_pair(b, (int)(e % kW), L, kA, N, i, q))  // ... and entries
             for (int k = 0; k < m; ++k) s = fma(t[i + k], t[q + k], s);
         qt[e] = s;
     }
 }
 
 __global__ void k_seed_advance(const double* __restrict__ t, int n, int m, int L, int kA, int nb, int bstep,
-                               double* __restrict__ qt) {
+                               int ustep, double* __restrict__ qt) {
     pdl_enter();
     const int N1 = n - m;  // subsequence count of length m+1
     const long long total = (long long)nb * kW;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
         const int b = (int)(e / kW);
-        if (b % bstep) continue;
+        if (b % bstep || (int)(e % kW) % ustep) continue;
         int i, q;
         if (seed_pair(b, (int)(e % kW), L, kA, N1, i, q)) qt[e] = fma(t[i + m], t[q + m], qt[e]);
     }
@@ -2989,13 +2989,13 @@ void launch_rc_advance(const double* t, int n, int m, const RcRows& rows, long l
     launch_pdl(k_rc_advance, dim3(148 * 2, rows.n > 0 ? rows.n : 1), 256, st, t, n, m, rows, stride, qt);
 }
 
-void launch_seed_init(const double* t, int n, int m, int L, int kA, int nb, int bstep, double* qt, cudaStream_t st) {
-    k_seed_init<<<148 * 8, 256, 0, st>>>(t, n, m, L, kA, nb, bstep, qt);
+void launch_seed_init(const double* t, int n, int m, int L, int kA, int nb, int bstep, int ustep, double* qt, cudaStream_t st) {
+    k_seed_init<<<148 * 8, 256, 0, st>>>(t, n, m, L, kA, nb, bstep, ustep, qt);
 }
 
-void launch_seed_advance(const double* t, int n, int m, int L, int kA, int nb, int bstep, double* qt,
+void launch_seed_advance(const double* t, int n, int m, int L, int kA, int nb, int bstep, int ustep, double* qt,
                          cudaStream_t st) {
-    launch_pdl(k_seed_advance, 148 * 8, 256, st, t, n, m, L, kA, nb, bstep, qt);
+    launch_pdl(k_seed_advance, 148 * 8, 256, st, t, n, m, L, kA, nb, bstep, ustep, qt);
 }
 
 static int grid_for(long long work, int threads) {

@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(256, 6) k_next_length(const double* __restrict
                               const double* __restrict__ sig_in, double* __restrict__ mu_out,
                               double* __restrict__ sig_out, float* __restrict__ df, float* __restrict__ dg,
                               float* __restrict__ nrm, int* __restrict__ cr, int* __restrict__ cr_next, int L, int kA,
-                              int nb, int bstep, double* __restrict__ qt, int* __restrict__ deg,
+                              int nb, int bstep, int ustep, double* __restrict__ qt, int* __restrict__ deg,
                               const double2* __restrict__ P1, const double2* __restrict__ P2,
                               int* __restrict__ degc, int* __restrict__ deg2, int qblocks) {
     pdl_enter();
@@ -370,12 +370,13 @@ __global__ void __launch_bounds__(256, 6) k_next_length(const double* __restrict
             if (i >= cnt) continue;
             const double ti = t[i + m];
             double* row = qt + (size_t)b * kW;
-            // every load of the row slice first (5 entries per thread in flight)
+            // every load of the row slice first (5 entries per thread in flight);
+            // ustep > 1: only the entries the pass-0 walk reads (every ustep-th)
             constexpr int kPer = (kW + 255) / 256;
             double rv[kPer], tv[kPer];
 #pragma unroll
             for (int k = 0; k < kPer; ++k) {
-                const int u = threadIdx.x + k * 256;
+                const int u = (threadIdx.x + k * 256) * ustep;
                 const int q = (b & 1) ? i - kA - u : i + kA + u;
                 const bool ok = u < kW && q >= 0 && q < cnt;
                 rv[k] = ok ? row[u] : 0.0;
@@ -383,7 +384,7 @@ __global__ void __launch_bounds__(256, 6) k_next_length(const double* __restrict
             }
 #pragma unroll
             for (int k = 0; k < kPer; ++k) {
-                const int u = threadIdx.x + k * 256;
+                const int u = (threadIdx.x + k * 256) * ustep;
                 const int q = (b & 1) ? i - kA - u : i + kA + u;
                 if (u < kW && q >= 0 && q < cnt) row[u] = fma(ti, tv[k], rv[k]);
             }
@@ -466,12 +467,12 @@ void launch_dd_prefix(const double* t, int n, double2* tot1, double2* tot2, doub
 
 void launch_next_length(const double* t, int n, int m, const double* mu_in, const double* sig_in, double* mu_out,
                         double* sig_out, float* df, float* dg, float* nrm, int* cr, int* cr_next, int L, int kA,
-                        int nb, int bstep, double* qt, int* deg, const double2* P1, const double2* P2, int* degc, int* deg2,
-                        cudaStream_t st) {
+                        int nb, int bstep, int ustep, double* qt, int* deg, const double2* P1, const double2* P2,
+                        int* degc, int* deg2, cudaStream_t st) {
     const int rows = qt != nullptr ? (nb + bstep - 1) / bstep : 0;
     const int qblocks = std::min(rows, 148 * 4);
     launch_pdl(k_next_length, grid_for(n - m, 256) + qblocks, 256, st, t, n, m, mu_in, sig_in, mu_out, sig_out, df, dg,
-               nrm, cr, cr_next, L, kA, nb, bstep, qt, deg, P1, P2, degc, deg2, qblocks);
+               nrm, cr, cr_next, L, kA, nb, bstep, ustep, qt, deg, P1, P2, degc, deg2, qblocks);
 }
 
 }  // namespace tsd

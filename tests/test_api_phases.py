@@ -79,7 +79,8 @@ def test_stats_walk_offset_series_bitexact(engine, oracle):
 def test_resident_seed_rows_follow_the_length_recurrence(engine, oracle, pk):
     # north_star (a): QT_{m+1}(i, q) = QT_m(i, q) + t[i+m] t[q+m] on the device;
     # after 100 steps the rows equal direct FP64 dot products to ~1e-13 relative
-    # (the pair-kill band 0 keeps only the positive-side rows, b even)
+    # (the pair-kill band 0 keeps only the positive-side rows, b even, and with
+    # its default pattern only the entries its walk reads, u a multiple of 9)
     x = oracle.gen_randomwalk(12_000, 6)
     engine.set_param("pass0_pk", pk)
     try:
@@ -100,7 +101,7 @@ def test_resident_seed_rows_follow_the_length_recurrence(engine, oracle, pk):
         i = j * L + L - 1 if (b & 1) else j * L
         if i >= N:
             continue
-        for u in (0, 1, 77, 1151):
+        for u in ((0, 9, 72, 1143) if pk else (0, 1, 77, 1151)):
             q = i - kA - u if (b & 1) else i + kA + u
             if not (0 <= q < N):
                 continue
