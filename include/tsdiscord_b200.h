@@ -260,7 +260,9 @@ int tsd_fp32_peak_probe(int device, double* tflops);
  *   err_scale       err_k of the FP32 error bound (default 4; a smaller value
  *                   voids the bound's proof)
  *   band_passes     cap on band passes per try;  band_few / band_keep: break rule
- *   half_pass0, half_bands, half_bands_m   reduced-density evaluation strides
+ *   half_pass0, half_bands, half_bands_m   reduced-density evaluation patterns
+ *                   (half_bands 20: the middle slot of every thread only, the
+ *                   default; 2 / 3: every slot, 1 step in 2 / 3)
  *   pair_band0      paired both-sides band-0 walk for large series (1)
  *   band0_sides     sides of band 0 (2)
  *   seed_w          cost-model weight of a seed element vs a walked row
@@ -268,9 +270,13 @@ int tsd_fp32_peak_probe(int device, double* tflops);
  *   track_chunks    tracked full-row chunks (1: one catch-all launch)
  *   witness         kill witnesses of earlier tries, tested right after band pass 0 (1)
  *   wit_cache       the witness test's run-seed cache (1)
- *   band_few_wit    with witnesses: band passes stop at this many rows (0: auto)
+ *   band_few_wit    with witnesses: band passes stop at this many rows (0: auto:
+ *                   256 below N = 2^18, else few_lo from m = few_m on, else 64)
+ *   few_m, few_lo   (512, 2)
  *   pass0_pk        band 0 walks every pair once, both ends killed (1)
- *   pk_min_n, pk_rows, half_pk   its minimum N, block rows (0: auto), stride (6)
+ *   pk_min_n, pk_rows, half_pk   its minimum N, block rows (0: auto), pattern
+ *                   (20: slot 0 of every thread, the default; 6 / 9: strides;
+ *                   12, 15, 16: three slots)
  *   row_cache, rc_min_m          resident full rows of anchors next to the
  *                   previous tries' survivors (1, from m = 384)
  *   dev_barrier     rank groups: device flag barriers (-1 auto, 0 host, 1 device)
