@@ -276,7 +276,7 @@ int tsd_fp32_peak_probe(int device, double* tflops);
  *   pass0_pk        band 0 walks every pair once, both ends killed (1)
  *   pk_min_n, pk_rows, half_pk   its minimum N, block rows (0: auto), pattern
  *                   (20: slot 0 of every thread, the default; 6 / 9: strides;
- *                   12, 15, 16: three slots)
+ *                   12, 16: three slots)
  *   row_cache, rc_min_m          resident full rows of anchors next to the
  *                   previous tries' survivors (1, from m = 384)
  *   dev_barrier     rank groups: device flag barriers (-1 auto, 0 host, 1 device)

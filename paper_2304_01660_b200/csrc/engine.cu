@@ -2131,7 +2131,7 @@ int tsd_set_param(tsd_ctx* c, const char* key, double v) {
         else if (k == "pair_band0") c->pair_band0 = v != 0.0;
         else if (k == "pass0_pk") c->pass0_pk = v != 0.0;
         else if (k == "half_pk")
-            c->half_pk = (v == 12 || v == 15 || v == 16 || v == 20 || v == 21) ? (int)v
+            c->half_pk = (v == 12 || v == 16 || v == 20) ? (int)v
                          : v >= 9 ? 9 : (v >= 6 ? 6 : std::max(1, std::min(3, (int)v)));
         else if (k == "pk_min_n") c->pk_min_n = (int64_t)v;
         else if (k == "pk_rows") c->pk_rows = v <= 0 ? 0 : std::max(16, std::min(kMaxRows, (int)v));

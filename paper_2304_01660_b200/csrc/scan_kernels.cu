@@ -1096,15 +1096,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_band0_pair(const ScanParams p) 
 // Sampled cells of the pair-kill walk: slot j (diagonal ub + j of the thread)
 // at step uu of a 9-step block.  A slot that no pattern ever samples is never
 // read, so the compiler drops its walk too: STRIDE 6 samples the even slots
-// only (5 of 9 walked), 12 / 15 / 16 three slots (3 of 9 walked: slots 0, 3, 6
-// or 0, 4, 8).  Every pattern meets each partner q of a walked slot.
+// only (5 of 9 walked), 12 / 16 three slots (slots 0, 3, 6), 20 slot 0 alone.
+// Every pattern meets each partner q of a walked slot once per 9 steps.
 template <int STRIDE>
 __device__ __forceinline__ constexpr bool pk_sampled(int j, int uu) {
     return STRIDE == 20   ? (j == 0)
-           : STRIDE == 21 ? ((j == 0 && uu % 2 == 0) || (j == 4 && (uu == 1 || uu == 3 || uu == 6 || uu == 8)))
            : STRIDE == 12 ? (j % 3 == 0 && (j / 3 + uu) % 3 == 0)
            : STRIDE == 16 ? (j % 3 == 0 && (j / 3 + uu) % 3 != 2)
-           : STRIDE == 15 ? (j % 4 == 0 && (j / 4 + uu) % 3 == 0)
            : STRIDE >= 6  ? (j + 2 * uu) % STRIDE == 0
                           : (2 * j + uu) % STRIDE == 0;
 }
@@ -3071,12 +3069,8 @@ int band0_pk_slots() {
         cudaFuncSetAttribute(k_band0_pk<9>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaFuncSetAttribute(k_band0_pk<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         cudaFuncSetAttribute(k_band0_pk<12>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaFuncSetAttribute(k_band0_pk<15>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-        cudaFuncSetAttribute(k_band0_pk<15>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaFuncSetAttribute(k_band0_pk<20>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         cudaFuncSetAttribute(k_band0_pk<20>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cudaFuncSetAttribute(k_band0_pk<21>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-        cudaFuncSetAttribute(k_band0_pk<21>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaFuncSetAttribute(k_band0_pk<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         cudaFuncSetAttribute(k_band0_pk<16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_band0_pk<3>, kThreads, bytes);
@@ -3092,8 +3086,6 @@ static void launch_band0_pk(const ScanParams& p, cudaStream_t st) {
     if (p.half == 2) launch_pdl_smem(k_band0_pk<2>, grid, kThreads, bytes, st, p);
     else if (p.half == 12) launch_pdl_smem(k_band0_pk<12>, grid, kThreads, bytes, st, p);
     else if (p.half == 20) launch_pdl_smem(k_band0_pk<20>, grid, kThreads, bytes, st, p);
-    else if (p.half == 21) launch_pdl_smem(k_band0_pk<21>, grid, kThreads, bytes, st, p);
-    else if (p.half == 15) launch_pdl_smem(k_band0_pk<15>, grid, kThreads, bytes, st, p);
     else if (p.half == 16) launch_pdl_smem(k_band0_pk<16>, grid, kThreads, bytes, st, p);
     else if (p.half >= 9) launch_pdl_smem(k_band0_pk<9>, grid, kThreads, bytes, st, p);
     else if (p.half >= 6) launch_pdl_smem(k_band0_pk<6>, grid, kThreads, bytes, st, p);
